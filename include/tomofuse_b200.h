@@ -1,0 +1,155 @@
+/*
+ * tomofuse-b200 C ABI: the drop-in boundary for the reference's FBP hot path.
+ *
+ * The reference (`/root/reference/pkg/src/tomofuse/fbp.py`) is a pure-Python
+ * package; its reconstruction "plugin surface" is the function set
+ * preprocess / filter_multiplier / offset_weights / ramp_filter /
+ * back_project / quantize / reconstruct.  Each entry point below replaces one
+ * of them (cited per function).  The Python mirror
+ * `paper_2505_13955_b200.fbp` binds this library with ctypes and keeps the
+ * reference signatures, argument meaning and ValueError behaviour; see
+ * INTEGRATION.md for the binding a tomofuse maintainer would add.
+ *
+ * Conventions
+ *  - Plain pointers + sizes; no torch types.  Device pointers are caller-owned
+ *    device memory; `stream` is a cudaStream_t passed as void*.
+ *  - Work is stream-ordered and reentrant; plans are immutable after creation
+ *    and may be shared by concurrent streams.  Hot calls never allocate.
+ *  - Array order follows the reference: sinograms are angle-major
+ *    (n_proj, n_rows, n_chan) (fbp.py:206), volumes are (z, y, x)
+ *    (geometry.py:94-97).
+ *  - Every call returns a tf_status; tf_error_string() gives the text the
+ *    Python layer raises as ValueError / RuntimeError.
+ */
+#ifndef TOMOFUSE_B200_H
+#define TOMOFUSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TF_API __attribute__((visibility("default")))
+#else
+#define TF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TF_OK = 0,
+    TF_ERR_INVALID_ARGUMENT = 1, /* maps to ValueError */
+    TF_ERR_CUDA = 2,             /* CUDA runtime/driver failure */
+    TF_ERR_UNSUPPORTED = 3,      /* geometry outside the compiled kernels */
+    TF_ERR_OUT_OF_MEMORY = 4
+} tf_status;
+
+/* Scan + grid description: AcquisitionParams (geometry.py:27-70) and
+ * VolumeDims (geometry.py:73-97) flattened into one POD. */
+typedef struct {
+    int32_t n_proj, n_rows, n_chan;
+    int32_t nx, ny;
+    int32_t offset_chan; /* 0 for normal scans (ScanMode.NORMAL) */
+    int32_t scan_mode;   /* 0 = NORMAL, 1 = OFFSET (geometry.py:22-24) */
+    int32_t reserved;
+    double angle_span;   /* radians */
+    double pixel_pitch;  /* detector pitch, um */
+    double voxel_pitch;  /* voxel pitch, um */
+} tf_geometry;
+
+typedef enum { TF_FILTER_RAMLAK = 0, TF_FILTER_SHEPPLOGAN = 1 } tf_filter_kind;
+
+typedef enum { TF_F32 = 0, TF_F64 = 1 } tf_dtype;
+
+typedef struct tf_filter_plan tf_filter_plan;
+typedef struct tf_bp_plan tf_bp_plan;
+
+TF_API const char* tf_error_string(int status);
+/* Last error detail of the calling thread (messages match the reference's
+ * ValueError texts where one exists). */
+TF_API const char* tf_last_error(void);
+TF_API int tf_version(void);
+
+/* ---- host-side plan math (tiny tables; fp64, bit-for-bit the reference) -- */
+
+/* Replaces fbp.filter_multiplier (fbp.py:105-116): Re(rfft(h))/pixel_pitch,
+ * written to host_out[0 .. padded/2]. */
+TF_API int tf_filter_multiplier(int kind, int64_t padded, double pixel_pitch, double* host_out);
+
+/* Replaces fbp.offset_weights (fbp.py:147-183): n_chan fp64 weights. */
+TF_API int tf_offset_weights(const tf_geometry* g, int feather_band, double* host_out);
+
+/* ---- filtering: preprocess + blur + ramp (fbp.py:75-83, 119-131) -------- */
+
+/* Plan for lines of n_chan channels. `padded` is the reference's FilterSpec
+ * padding (0 = next pow2 >= 2n); it is validated (>= 2n) exactly like
+ * FilterSpec.padded_length (fbp.py:48-60).  The filtered result is
+ * independent of the pad length once pad >= 2n, so the kernel always
+ * transforms at the internal length next_pow2(2n). */
+TF_API int tf_filter_plan_create(int n_chan, int kind, int64_t padded, double pixel_pitch, double blur_sigma,
+                          tf_filter_plan** plan);
+TF_API int tf_filter_plan_destroy(tf_filter_plan* plan);
+
+/* Filters n_lines lines.  in: n_lines x n_chan fp32 raw counts (i0 > 0:
+ * Beer-Lambert -ln(max(raw,1)/i0) is fused in) or optical depth (i0 <= 0).
+ * out: filtered fp32; line l goes to out + l_dst*n_chan where, for
+ * n_slabs > 0, lines are (angle, row) pairs of an angle-major block with
+ * `rows_per_angle` rows and rows are regrouped slab-major for a row-slab
+ * all-to-all: row r in slab s = [slab_row0[s], slab_row0[s+1]) of angle a
+ * goes to element offset slab_base[s] + (a*(slab_row0[s+1]-slab_row0[s]) +
+ * r - slab_row0[s]) * n_chan.  n_slabs == 0 keeps the natural layout.
+ * in == out (in-place) is allowed for the natural layout. */
+TF_API int tf_filter(const tf_filter_plan* plan, const float* in, float* out, int64_t n_lines, float i0,
+              int rows_per_angle, int n_slabs, const int32_t* slab_row0, const int64_t* slab_base,
+              void* stream);
+
+/* Beer-Lambert only (fbp.py:75-83): fp32 or fp64 counts -> fp64 depth
+ * (the reference's output dtype), computed in fp64. */
+TF_API int tf_preprocess(const void* raw, int raw_dtype, double* out, int64_t n, double i0, void* stream);
+
+/* ---- back-projection (fbp.py:186-252) ---------------------------------- */
+
+TF_API int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_plan** plan);
+TF_API int tf_bp_plan_destroy(tf_bp_plan* plan);
+
+/* Bytes of the z-blocked staging buffer for `n_rows` rows. */
+TF_API int64_t tf_bp_stage_bytes(const tf_bp_plan* plan, int n_rows);
+
+/* Converts filtered rows [r0, r1) of an angle-major fp32 sinogram (row pitch
+ * n_chan, angle pitch `rows_per_angle`*n_chan) into the z-blocked staging
+ * layout, applying the offset-scan feather (fbp.py:242).  `stage` must hold
+ * tf_bp_stage_bytes(plan, r1-r0) bytes. */
+TF_API int tf_bp_stage(const tf_bp_plan* plan, const float* sino, int rows_per_angle, int r0, int r1, void* stage,
+                void* stream);
+
+enum {
+    TF_BP_ACCUMULATE = 1, /* add to the unscaled partial sums already in vol */
+    TF_BP_FINALIZE = 2    /* apply FoV mask + angle_span/n_proj scale (fbp.py:246-251) */
+};
+
+/* Back-projects angles [a0, a1) of a staged slab of `n_rows` rows into
+ * vol (n_rows, ny, nx) fp32, restricted to tile [x0,x1) x [y0,y1)
+ * (fbp.py:191-193).  Voxels outside the tile are not written.  With
+ * flags = TF_BP_FINALIZE a single call reproduces back_project(); angle
+ * chunks may be chained with TF_BP_ACCUMULATE (summation order stays
+ * ascending in angle, fbp.py:198-201). */
+TF_API int tf_backproject(const tf_bp_plan* plan, const void* stage, int n_rows, float* vol, int a0, int a1, int x0,
+                   int x1, int y0, int y1, int flags, void* stream);
+
+/* ---- quantize (fbp.py:255-259) ------------------------------------------ */
+/* vol is fp32 or fp64 (vol_dtype); arithmetic is fp64, round-half-even,
+ * bit-identical to numpy for the same input values. */
+TF_API int tf_quantize(const void* vol, int vol_dtype, uint16_t* out, int64_t n, double lo, double hi, void* stream);
+
+/* ---- synthetic input: analytic 3-D Shepp-Logan raw counts -------------- */
+/* Writes raw counts i0*exp(-p) (fp32) for angles [a0,a1), rows [r0,r1) into
+ * out (a1-a0, r1-r0, n_chan).  Attenuation max `mu_max` (1/um). */
+TF_API int tf_phantom_sinogram(const tf_geometry* g, int a0, int a1, int r0, int r1, double i0, double mu_max,
+                        float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TOMOFUSE_B200_H */

@@ -1,0 +1,446 @@
+// K2: voxel-driven back-projection (replaces fbp.back_project, fbp.py:186-252).
+//
+// Data layout in HBM ("z-blocked staging", written by tf_bp_stage):
+//   stage[(k * nzb + zb) * n_chan + c][zi]  fp32, zi in [0, 36)
+// i.e. for every angle k and block of 32 detector rows zb, each channel c
+// holds the 32 rows contiguously (+4 zero pad floats: a 144-B row pitch puts
+// consecutive channels in distinct 16-B bank quads, so the LDS.128 gathers
+// below are conflict-free without a swizzle).  Feather weights
+// (fbp.py:242) are folded in while staging.
+//
+// Kernel structure (one CTA = 16x16 voxel columns x one 32-row z-block):
+//   * warp 8 is a TMA producer: per angle it computes, in fp64, the channel
+//     window [c_lo, c_lo+W) the tile's rays hit, and issues one
+//     cp.async.bulk.tensor box {36, W, 1} into a 3-stage x 4-angle smem ring
+//     (mbarrier full/empty pipeline).  Out-of-detector channels come back as
+//     zeros from the TMA OOB fill -- the reference's zero guard.
+//   * warps 0-7 each own 32 voxel columns x 32 rows in registers; per angle a
+//     thread forms t in fp32 *relative to the tile origin* (origin and window
+//     offset in fp64: |error| ~1e-6 channels even at 8192 channels, where a
+//     plain fp32 t would be off by ~5e-4), then gathers the two taps for all
+//     32 rows with 2x8 LDS.128 and accumulates with 64 FFMA.
+//   * epilogue: FoV mask evaluated in fp64 exactly as fbp.py:247-250, scale by
+//     float32(angle_span / n_proj) (fbp.py:251), coalesced stores.
+// Tiles wholly outside the field of view skip the angle loop.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+struct tf_bp_plan {
+    tf_geometry g;
+    int feather_band;
+    double2* d_trig;  // (cos, sin) of k * (span / n_proj), fp64 libm, per angle
+    float* d_w;       // feather weights (fp32, as numpy casts them)
+    int W;            // channel window per tile-angle
+    double cx, cy, scale, axis, R2, sc2;
+    float angle_wf;
+};
+
+namespace tf {
+namespace {
+
+constexpr int TX = 16, TY = 16;           // voxel columns per CTA
+constexpr int NCW = 8;                    // consumer warps
+constexpr int NTHREADS = NCW * 32 + 32;   // + 1 producer warp
+constexpr int STAGES = 3, APS = 4;        // ring: 3 stages x 4 angles
+constexpr int ACC = kZB;                  // rows per thread
+
+struct BPArgs {
+    const double2* trig;
+    float* vol;
+    int a0, a1, nzb, n_rows, nx, ny, n_chan;
+    int x0, x1, y0, y1;
+    int ntx;
+    int W, slot_bytes;
+    int flags;
+    double cx, cy, scale, axis, R2, sc2;
+    float angle_wf;
+};
+
+__device__ __forceinline__ bool outside_fov(int x, int y, const BPArgs& a) {
+    // ((x-cx)^2 + (y-cy)^2) * scale^2 > R^2, no FMA contraction (fbp.py:247-250)
+    double dx = __dsub_rn((double)x, a.cx), dy = __dsub_rn((double)y, a.cy);
+    double rr = __dmul_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), a.sc2);
+    return rr > a.R2;
+}
+
+__global__ void __launch_bounds__(NTHREADS, 2)
+    bp_kernel(const __grid_constant__ CUtensorMap map, const BPArgs args) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int tx = blockIdx.x % args.ntx, ty = blockIdx.x / args.ntx, zb = blockIdx.y;
+    const int X0 = tx * TX, Y0 = ty * TY;
+
+    // ---- tile-level early outs (uniform over the CTA, before any barrier)
+    const int xe = min(X0 + TX, args.nx), ye = min(Y0 + TY, args.ny);
+    const int ux0 = max(X0, args.x0), ux1 = min(xe, args.x1);
+    const int uy0 = max(Y0, args.y0), uy1 = min(ye, args.y1);
+    if (ux0 >= ux1 || uy0 >= uy1) return;  // nothing of the requested tile here
+    {
+        // nearest voxel of the tile to the rotation centre decides "all outside"
+        int nxv = (int)fmin(fmax(rint(args.cx), (double)X0), (double)(xe - 1));
+        int nyv = (int)fmin(fmax(rint(args.cy), (double)Y0), (double)(ye - 1));
+        bool all_out = true;
+        for (int ddx = -1; ddx <= 1; ++ddx)
+            for (int ddy = -1; ddy <= 1; ++ddy) {
+                int xx = min(max(nxv + ddx, X0), xe - 1), yy = min(max(nyv + ddy, Y0), ye - 1);
+                all_out = all_out && outside_fov(xx, yy, args);
+            }
+        if (all_out) {
+            if (args.flags & TF_BP_FINALIZE) {
+                const int nz = min(kZB, args.n_rows - zb * kZB);
+                const size_t plane = (size_t)args.nx * args.ny;
+                for (int i = threadIdx.x; i < TX * TY * nz; i += blockDim.x) {
+                    int z = i / (TX * TY), r = i % (TX * TY);
+                    int x = X0 + (r % TX), y = Y0 + (r / TX);
+                    if (x >= ux0 && x < ux1 && y >= uy0 && y < uy1)
+                        args.vol[(size_t)(zb * kZB + z) * plane + (size_t)y * args.nx + x] = 0.f;
+                }
+            }
+            return;
+        }
+    }
+
+    uint8_t* ring = smem;
+    float4* prm = reinterpret_cast<float4*>(smem + STAGES * APS * args.slot_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(prm + STAGES * APS);
+    uint64_t* empty = full + STAGES;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    const int n_ang = args.a1 - args.a0;
+    const int n_it = (n_ang + APS - 1) / APS;
+
+    if (warp == NCW) {
+        // ================= TMA producer (one thread)
+        if (lane == 0) {
+            tma_prefetch_desc(&map);
+            const double dX = (double)X0 - args.cx, dY = (double)Y0 - args.cy;
+            const uint32_t box_bytes = (uint32_t)(kZP * 4 * args.W);
+            for (int it = 0; it < n_it; ++it) {
+                const int s = it % STAGES;
+                const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+                mbar_wait(&empty[s], ph ^ 1u);
+                const int kb = args.a0 + it * APS;
+                const int na = min(APS, args.a1 - kb);
+                int c_lo[APS];
+                for (int a = 0; a < na; ++a) {
+                    const double2 cs = args.trig[kb + a];
+                    // t at the tile origin, same operation order as geometry.py:151-153
+                    double t0 = __dadd_rn(__dmul_rn(dX, cs.x), __dmul_rn(dY, cs.y));
+                    t0 = __dadd_rn(__dmul_rn(t0, args.scale), args.axis);
+                    const double B = cs.x * args.scale, C = cs.y * args.scale;
+                    const double tmin = t0 + fmin(0.0, B * (TX - 1)) + fmin(0.0, C * (TY - 1));
+                    c_lo[a] = (int)floor(tmin);
+                    prm[s * APS + a] = make_float4((float)(t0 - (double)c_lo[a]), (float)B, (float)C, 0.f);
+                }
+                mbar_arrive_expect_tx(&full[s], box_bytes * (uint32_t)na);
+                for (int a = 0; a < na; ++a)
+                    tma_load_3d(ring + (size_t)(s * APS + a) * args.slot_bytes, &map, &full[s], 0, c_lo[a],
+                                (kb + a) * args.nzb + zb);
+            }
+        }
+        return;
+    }
+
+    // ================= consumers
+    // warp patch 8x4 voxels, lanes in 4x2 quads (keeps each LDS.128 phase's
+    // channels within 8 consecutive rows -> distinct bank quads)
+    const int q = lane >> 3, i8 = lane & 7;
+    const int lx = (q & 1) * 4 + (i8 & 3), ly = (q >> 1) * 2 + (i8 >> 2);
+    const int dx = (warp & 1) * 8 + lx, dy = (warp >> 1) * 4 + ly;
+    const int x = X0 + dx, y = Y0 + dy;
+    const float fdx = (float)dx, fdy = (float)dy;
+    const size_t plane = (size_t)args.nx * args.ny;
+    const int nz = min(kZB, args.n_rows - zb * kZB);
+    const bool mine = x >= ux0 && x < ux1 && y >= uy0 && y < uy1;
+
+    float acc[ACC];
+#pragma unroll
+    for (int j = 0; j < ACC; ++j) acc[j] = 0.f;
+    if ((args.flags & TF_BP_ACCUMULATE) && mine) {
+#pragma unroll
+        for (int j = 0; j < ACC; ++j)
+            if (j < nz) acc[j] = args.vol[(size_t)(zb * kZB + j) * plane + (size_t)y * args.nx + x];
+    }
+
+    for (int it = 0; it < n_it; ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+        mbar_wait(&full[s], ph);
+        const int na = min(APS, n_ang - it * APS);
+        for (int a = 0; a < na; ++a) {
+            const float4 p = prm[s * APS + a];
+            float t = fmaf(fdy, p.z, fmaf(fdx, p.y, p.x));
+            t = fmaxf(t, 0.f);
+            const float fl = floorf(t);
+            const float f = t - fl;
+            const float w0 = 1.f - f;
+            const float* p0 = reinterpret_cast<const float*>(ring + (s * APS + a) * args.slot_bytes +
+                                                             (int)fl * kRowBytes);
+            const float* p1 = p0 + kZP;
+#pragma unroll
+            for (int c = 0; c < ACC / 4; ++c) {
+                const float4 u = *reinterpret_cast<const float4*>(p0 + 4 * c);
+                const float4 v = *reinterpret_cast<const float4*>(p1 + 4 * c);
+                acc[4 * c + 0] = fmaf(v.x, f, fmaf(u.x, w0, acc[4 * c + 0]));
+                acc[4 * c + 1] = fmaf(v.y, f, fmaf(u.y, w0, acc[4 * c + 1]));
+                acc[4 * c + 2] = fmaf(v.z, f, fmaf(u.z, w0, acc[4 * c + 2]));
+                acc[4 * c + 3] = fmaf(v.w, f, fmaf(u.w, w0, acc[4 * c + 3]));
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+    if (!mine) return;
+    float scale = 1.f;
+    bool zero = false;
+    if (args.flags & TF_BP_FINALIZE) {
+        scale = args.angle_wf;
+        zero = outside_fov(x, y, args);
+    }
+    float* out = args.vol + (size_t)(zb * kZB) * plane + (size_t)y * args.nx + x;
+#pragma unroll
+    for (int j = 0; j < ACC; ++j)
+        if (j < nz) out[(size_t)j * plane] = zero ? 0.f : acc[j] * scale;
+}
+
+// ---- staging: angle-major rows -> z-blocked, feather-weighted ------------
+__global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ sino, float* __restrict__ stage,
+                                                    const float* __restrict__ w, int n_proj, int n_chan,
+                                                    int rows_per_angle, int r0, int n_rows, int nzb) {
+    __shared__ float tile[kZB][33];
+    const int nch = (n_chan + 31) / 32;
+    const long long total = (long long)n_proj * nzb * nch;
+    for (long long blk = blockIdx.x; blk < total; blk += gridDim.x) {
+        const int cb = (int)(blk % nch);
+        const long long kz = blk / nch;
+        const int zb = (int)(kz % nzb);
+        const int k = (int)(kz / nzb);
+        const int c0 = cb * 32;
+        // load 32 rows x 32 channels (coalesced along channels)
+        for (int i = threadIdx.x; i < kZB * 32; i += 256) {
+            const int zi = i >> 5, c = i & 31;
+            const int row = zb * kZB + zi;
+            float v = 0.f;
+            if (row < n_rows && c0 + c < n_chan)
+                v = sino[((size_t)k * rows_per_angle + r0 + row) * n_chan + c0 + c] * w[c0 + c];
+            tile[zi][c] = v;
+        }
+        __syncthreads();
+        // write 32 channels x 36 floats, contiguous
+        float* dst = stage + (((size_t)k * nzb + zb) * n_chan + c0) * kZP;
+        const int nc = min(32, n_chan - c0);
+        for (int i = threadIdx.x; i < nc * (kZP / 4); i += 256) {
+            const int c = i / (kZP / 4), z4 = (i % (kZP / 4)) * 4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (z4 < kZB) v = make_float4(tile[z4][c], tile[z4 + 1][c], tile[z4 + 2][c], tile[z4 + 3][c]);
+            *reinterpret_cast<float4*>(dst + (size_t)c * kZP + z4) = v;
+        }
+        __syncthreads();
+    }
+}
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                      CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t encode_fn() {
+    static PFN_encodeTiled_t fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+    }
+    return fn;
+}
+
+int bp_smem_bytes(int slot_bytes) {
+    return STAGES * APS * slot_bytes + STAGES * APS * (int)sizeof(float4) + 2 * STAGES * (int)sizeof(uint64_t);
+}
+
+}  // namespace
+}  // namespace tf
+
+using namespace tf;
+
+extern "C" int tf_offset_weights(const tf_geometry* g, int band, double* w) {
+    if (!g || !w) return set_error(TF_ERR_INVALID_ARGUMENT, "null argument");
+    const int n = g->n_chan;
+    if (g->scan_mode == 0) {  // fbp.py:157-158
+        for (int i = 0; i < n; ++i) w[i] = 1.0;
+        return TF_OK;
+    }
+    if (band < 1) return set_error(TF_ERR_INVALID_ARGUMENT, "feather band must be >= 1 channel");
+    const double c0 = (n - 1) / 2.0 - g->offset_chan;  // axis_channel, geometry.py:64-67
+    for (int i = 0; i < n; ++i) {                      // fbp.py:161-183
+        const double c = (double)i;
+        const double near_edge = g->offset_chan > 0 ? c : (double)(n - 1) - c;
+        const double own = std::min(std::max(near_edge / band, 0.0), 1.0);
+        const double m = 2.0 * c0 - c;
+        double other = 0.0;
+        if (m >= 0 && m <= n - 1) {
+            const double mn = g->offset_chan > 0 ? m : (double)(n - 1) - m;
+            other = std::min(std::max(mn / band, 0.0), 1.0);
+        }
+        const double tot = own + other;
+        w[i] = tot > 0 ? own / tot : 0.0;
+    }
+    return TF_OK;
+}
+
+extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_plan** plan) {
+    if (!g || !plan) return set_error(TF_ERR_INVALID_ARGUMENT, "null argument");
+    *plan = nullptr;
+    if (g->n_proj < 1 || g->n_rows < 1 || g->n_chan < 2 || g->nx < 2 || g->ny < 2)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "invalid geometry sizes");
+    if (!(g->angle_span > 0) || !(g->pixel_pitch > 0) || !(g->voxel_pitch > 0))
+        return set_error(TF_ERR_INVALID_ARGUMENT, "spans and pitches must be positive");
+    if (g->scan_mode == 0 && g->offset_chan != 0)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "normal scan requires offset_chan == 0");
+    std::vector<double> w(g->n_chan);
+    int st = tf_offset_weights(g, feather_band, w.data());
+    if (st) return st;
+    auto* p = new tf_bp_plan();
+    p->g = *g;
+    p->feather_band = feather_band;
+    p->scale = g->voxel_pitch / g->pixel_pitch;
+    // window: max over angles of the tile's channel extent + 2 taps + floor slack
+    const double ext = std::sqrt((double)(TX - 1) * (TX - 1) + (double)(TY - 1) * (TY - 1)) * p->scale;
+    p->W = (int)std::ceil(ext + 3.0);
+    if (bp_smem_bytes((kRowBytes * p->W + 127) / 128 * 128) > 227 * 1024) {
+        delete p;
+        return set_error(TF_ERR_UNSUPPORTED, "voxel/pixel pitch ratio %.3g too large for the tile window",
+                         p->scale);
+    }
+    p->cx = (g->nx - 1) / 2.0;
+    p->cy = (g->ny - 1) / 2.0;
+    p->axis = (g->n_chan - 1) / 2.0 - g->offset_chan;
+    const double half = (g->n_chan - 1) / 2.0;  // fbp.py:134-144
+    const double R = g->scan_mode ? half + std::fabs((double)g->offset_chan) : half;
+    p->R2 = R * R;
+    p->sc2 = p->scale * p->scale;
+    const double step = g->angle_span / g->n_proj;
+    p->angle_wf = (float)step;
+    std::vector<double2> trig(g->n_proj);
+    for (int k = 0; k < g->n_proj; ++k) {  // theta_k = k * (span / n_proj), geometry.py:69-70
+        const double th = (double)k * step;
+        trig[k] = make_double2(cos(th), sin(th));
+    }
+    std::vector<float> wf(g->n_chan);
+    for (int i = 0; i < g->n_chan; ++i) wf[i] = (float)w[i];
+    cudaError_t e = cudaMalloc(&p->d_trig, sizeof(double2) * g->n_proj);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_w, sizeof(float) * g->n_chan);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_trig, trig.data(), sizeof(double2) * g->n_proj, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_w, wf.data(), sizeof(float) * g->n_chan, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        tf_bp_plan_destroy(p);
+        return set_error(TF_ERR_CUDA, "bp plan setup failed: %s", cudaGetErrorString(e));
+    }
+    *plan = p;
+    return TF_OK;
+}
+
+extern "C" int tf_bp_plan_destroy(tf_bp_plan* p) {
+    if (!p) return TF_OK;
+    cudaFree(p->d_trig);
+    cudaFree(p->d_w);
+    delete p;
+    return TF_OK;
+}
+
+extern "C" int64_t tf_bp_stage_bytes(const tf_bp_plan* p, int n_rows) {
+    if (!p || n_rows < 0) return -1;
+    const int64_t nzb = (n_rows + kZB - 1) / kZB;
+    return (int64_t)p->g.n_proj * nzb * p->g.n_chan * kZP * (int64_t)sizeof(float);
+}
+
+extern "C" int tf_bp_stage(const tf_bp_plan* p, const float* sino, int rows_per_angle, int r0, int r1,
+                           void* stage, void* stream) {
+    if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null bp plan");
+    if (!(0 <= r0 && r0 <= r1 && r1 <= rows_per_angle))
+        return set_error(TF_ERR_INVALID_ARGUMENT, "row range (%d, %d) out of bounds", r0, r1);
+    const int n_rows = r1 - r0;
+    if (n_rows == 0) return TF_OK;
+    if (!sino || !stage) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    const int nzb = (n_rows + kZB - 1) / kZB;
+    const long long total = (long long)p->g.n_proj * nzb * ((p->g.n_chan + 31) / 32);
+    const int grid = (int)std::min<long long>(total, 148LL * 16);
+    stage_kernel<<<grid, 256, 0, as_stream(stream)>>>(sino, static_cast<float*>(stage), p->d_w, p->g.n_proj,
+                                                      p->g.n_chan, rows_per_angle, r0, n_rows, nzb);
+    return check_launch("stage_kernel");
+}
+
+extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows, float* vol, int a0, int a1,
+                              int x0, int x1, int y0, int y1, int flags, void* stream) {
+    if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null bp plan");
+    const tf_geometry& g = p->g;
+    if (!(0 <= a0 && a0 <= a1 && a1 <= g.n_proj))
+        return set_error(TF_ERR_INVALID_ARGUMENT, "angle range (%d, %d) out of bounds", a0, a1);
+    if (!(0 <= x0 && x0 <= x1 && x1 <= g.nx && 0 <= y0 && y0 <= y1 && y1 <= g.ny))
+        return set_error(TF_ERR_INVALID_ARGUMENT, "tile (%d, %d, %d, %d) out of bounds", x0, x1, y0, y1);
+    if (n_rows < 0) return set_error(TF_ERR_INVALID_ARGUMENT, "n_rows must be >= 0");
+    if (n_rows == 0 || x0 == x1 || y0 == y1) return TF_OK;
+    if (!stage || !vol) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    const int nzb = (n_rows + kZB - 1) / kZB;
+    if (a0 == a1 && !(flags & TF_BP_FINALIZE)) return TF_OK;
+
+    PFN_encodeTiled_t enc = encode_fn();
+    if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    CUtensorMap map;
+    cuuint64_t dims[3] = {(cuuint64_t)kZP, (cuuint64_t)g.n_chan, (cuuint64_t)g.n_proj * (cuuint64_t)nzb};
+    cuuint64_t strides[2] = {(cuuint64_t)kRowBytes, (cuuint64_t)kRowBytes * (cuuint64_t)g.n_chan};
+    cuuint32_t box[3] = {(cuuint32_t)kZP, (cuuint32_t)p->W, 1u};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(stage), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+
+    BPArgs a{};
+    a.trig = p->d_trig;
+    a.vol = vol;
+    a.a0 = a0;
+    a.a1 = a1;
+    a.nzb = nzb;
+    a.n_rows = n_rows;
+    a.nx = g.nx;
+    a.ny = g.ny;
+    a.n_chan = g.n_chan;
+    a.x0 = x0;
+    a.x1 = x1;
+    a.y0 = y0;
+    a.y1 = y1;
+    a.ntx = (g.nx + TX - 1) / TX;
+    a.W = p->W;
+    a.slot_bytes = ((kRowBytes * p->W) + 127) / 128 * 128;
+    a.flags = flags;
+    a.cx = p->cx;
+    a.cy = p->cy;
+    a.scale = p->scale;
+    a.axis = p->axis;
+    a.R2 = p->R2;
+    a.sc2 = p->sc2;
+    a.angle_wf = p->angle_wf;
+    const int smem = bp_smem_bytes(a.slot_bytes);
+    TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int nty = (g.ny + TY - 1) / TY;
+    dim3 grid((unsigned)(a.ntx * nty), (unsigned)nzb);
+    bp_kernel<<<grid, NTHREADS, smem, as_stream(stream)>>>(map, a);
+    return check_launch("bp_kernel");
+}

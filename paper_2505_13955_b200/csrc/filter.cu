@@ -1,0 +1,419 @@
+// K1: fused Beer-Lambert + optional Gaussian blur + ramp filter.
+//
+// Replaces fbp.preprocess (fbp.py:75-83) and fbp.ramp_filter (fbp.py:119-131)
+// on the reconstruction path.  The reference zero-pads every (angle, row)
+// line to P >= 2n, multiplies its rfft by the real even spectrum of the
+// band-limited ramp kernel (fbp.py:86-116) and keeps the first n samples.
+// Because the multiplier is real and even, two real lines are filtered by one
+// complex FFT (line a in the real part, line b in the imaginary part).  The
+// FFT is a shared-memory Stockham transform, radix 16/8/4/2, one CTA per
+// line pair, fp32 with fp64-derived twiddles.  Output equals the linear
+// convolution with taps |d| <= n-1 for any pad >= 2n, so the transform
+// always runs at next_pow2(2n) whatever FilterSpec.padding says.
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+struct tf_filter_plan {
+    int n;             // channels
+    int P;             // internal transform length (pow2 >= 2n)
+    int log2P;
+    int threads;
+    int blur_radius;
+    float2* d_tw;      // exp(-2 pi i m / P), m in [0, P)
+    float* d_mult;     // multiplier / P, m in [0, P/2]
+    float* d_blur;     // 2*radius+1 Gaussian weights (or null)
+};
+
+namespace tf {
+namespace {
+
+// ---------------------------------------------------------------- host math
+// Band-limited kernel tap at lag d (fbp.py:86-102).
+double kernel_tap(int kind, long long d) {
+    const double pi2 = M_PI * M_PI;
+    if (kind == TF_FILTER_RAMLAK) {
+        if (d == 0) return 0.25;
+        if (d % 2 == 0) return 0.0;
+        return -1.0 / (pi2 * (double)(d * d));
+    }
+    return -2.0 / (pi2 * (4.0 * (double)d * (double)d - 1.0));
+}
+
+// In-place iterative radix-2 complex FFT (fp64), forward sign.
+void fft_pow2(std::vector<std::complex<double>>& a) {
+    const size_t n = a.size();
+    for (size_t i = 1, j = 0; i < n; ++i) {
+        size_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) std::swap(a[i], a[j]);
+    }
+    for (size_t len = 2; len <= n; len <<= 1) {
+        for (size_t i = 0; i < n; i += len) {
+            for (size_t k = 0; k < len / 2; ++k) {
+                double ang = -2.0 * M_PI * (double)k / (double)len;
+                std::complex<double> w(cos(ang), sin(ang));
+                std::complex<double> u = a[i + k], v = a[i + k + len / 2] * w;
+                a[i + k] = u + v;
+                a[i + k + len / 2] = u - v;
+            }
+        }
+    }
+}
+
+void multiplier_fp64(int kind, long long P, double pitch, double* out) {
+    // h on the circular grid (lags m <= P/2 positive, the rest negative)
+    std::vector<double> h((size_t)P);
+    for (long long m = 0; m < P; ++m) h[(size_t)m] = kernel_tap(kind, m <= P / 2 ? m : m - P);
+    const long long nout = P / 2 + 1;
+    if ((P & (P - 1)) == 0) {
+        std::vector<std::complex<double>> a((size_t)P);
+        for (long long m = 0; m < P; ++m) a[(size_t)m] = h[(size_t)m];
+        fft_pow2(a);
+        for (long long k = 0; k < nout; ++k) out[k] = a[(size_t)k].real() / pitch;
+    } else {  // explicit non-pow2 padding: direct real DFT (cos sum) with exact reduction
+        for (long long k = 0; k < nout; ++k) {
+            double s = 0.0;
+            for (long long m = 0; m < P; ++m) {
+                long long r = (m * k) % P;
+                s += h[(size_t)m] * cos(2.0 * M_PI * (double)r / (double)P);
+            }
+            out[k] = s / pitch;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- device FFT
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+
+__device__ __forceinline__ int pad_idx(int i) { return i + (i >> 4); }  // 1 float2 pad per 16
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+
+// exp(-2 pi i k / 16), k = 0..7
+__device__ __forceinline__ float2 w16(int k) {
+    constexpr float c1 = 0.92387953251128674f, s1 = 0.38268343236508978f, r2 = 0.70710678118654752f;
+    switch (k & 7) {
+        case 0: return make_float2(1.f, 0.f);
+        case 1: return make_float2(c1, -s1);
+        case 2: return make_float2(r2, -r2);
+        case 3: return make_float2(s1, -c1);
+        case 4: return make_float2(0.f, -1.f);
+        case 5: return make_float2(-s1, -c1);
+        case 6: return make_float2(-r2, -r2);
+        default: return make_float2(-c1, -s1);
+    }
+}
+
+// Forward DFT of R points held in registers (recursive radix-2 DIT; all
+// indices are compile-time so everything stays in registers).
+template <int R>
+__device__ __forceinline__ void dft(float2 (&v)[R]) {
+    if constexpr (R == 1) {
+        return;
+    } else if constexpr (R == 2) {
+        float2 a = v[0], b = v[1];
+        v[0] = make_float2(a.x + b.x, a.y + b.y);
+        v[1] = make_float2(a.x - b.x, a.y - b.y);
+    } else {
+        constexpr int M = R / 2;
+        float2 e[M], o[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            e[i] = v[2 * i];
+            o[i] = v[2 * i + 1];
+        }
+        dft<M>(e);
+        dft<M>(o);
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            float2 t = (k == 0) ? o[k] : cmul(o[k], w16(k * (16 / R)));
+            v[k] = make_float2(e[k].x + t.x, e[k].y + t.y);
+            v[k + M] = make_float2(e[k].x - t.x, e[k].y - t.y);
+        }
+    }
+}
+
+// One Stockham pass of radix R over a padded smem line of length P.
+template <int R>
+__device__ __forceinline__ void stockham_pass(float2* buf, const float2* __restrict__ tw, int P, int Ns, int tid,
+                                              int T) {
+    constexpr int MAXB = 16 / R;  // butterflies per thread held across the sync (P <= 16*T)
+    float2 v[MAXB][R];
+    const int nb = P / R;
+    const int stride = P / (Ns * R);
+#pragma unroll
+    for (int b = 0; b < MAXB; ++b) {
+        int j = tid + b * T;
+        if (j < nb) {
+            int k = j & (Ns - 1);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                float2 x = buf[pad_idx(j + r * nb)];
+                if (r > 0 && Ns > 1) x = cmul(x, __ldg(&tw[k * r * stride]));
+                v[b][r] = x;
+            }
+            dft<R>(v[b]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < MAXB; ++b) {
+        int j = tid + b * T;
+        if (j < nb) {
+            int k = j & (Ns - 1);
+            int base = (j - k) * R + k;
+#pragma unroll
+            for (int r = 0; r < R; ++r) buf[pad_idx(base + r * Ns)] = v[b][r];
+        }
+    }
+    __syncthreads();
+}
+
+__device__ void fft_forward(float2* buf, const float2* __restrict__ tw, int P, int log2P, int tid, int T) {
+    int Ns = 1, rem = log2P;
+    while (rem >= 4) {
+        stockham_pass<16>(buf, tw, P, Ns, tid, T);
+        Ns <<= 4;
+        rem -= 4;
+    }
+    if (rem == 3) stockham_pass<8>(buf, tw, P, Ns, tid, T);
+    else if (rem == 2) stockham_pass<4>(buf, tw, P, Ns, tid, T);
+    else if (rem == 1) stockham_pass<2>(buf, tw, P, Ns, tid, T);
+}
+
+struct SlabMap {
+    int n_slabs;
+    int rows_per_angle;
+    int32_t row0[9];
+    long long base[8];
+};
+
+__device__ __forceinline__ long long line_offset(long long l, int n, const SlabMap& m) {
+    if (m.n_slabs == 0) return l * n;
+    long long a = l / m.rows_per_angle;
+    int r = (int)(l - a * m.rows_per_angle);
+    int s = 0;
+#pragma unroll 1
+    while (s + 1 < m.n_slabs && r >= m.row0[s + 1]) ++s;
+    int rs = m.row0[s + 1] - m.row0[s];
+    return m.base[s] + (a * rs + (r - m.row0[s])) * (long long)n;
+}
+
+__global__ void __launch_bounds__(1024) ramp_filter_kernel(const float* __restrict__ in, float* out,
+                                                           long long n_lines, int n, int P, int log2P,
+                                                           const float2* __restrict__ tw,
+                                                           const float* __restrict__ mult,
+                                                           const float* __restrict__ blur, int radius,
+                                                           float i0, SlabMap map) {
+    extern __shared__ float2 sbuf[];
+    const int tid = threadIdx.x, T = blockDim.x;
+    const long long la = 2 * (long long)blockIdx.x;
+    const bool has_b = la + 1 < n_lines;
+    const float* pa = in + la * n;
+    const float* pb = in + (la + 1) * n;
+    const bool log_in = i0 > 0.f;
+
+    // load (+ Beer-Lambert) the two lines as one complex line, zero-padded
+    for (int m = tid; m < P; m += T) {
+        float2 z = make_float2(0.f, 0.f);
+        if (m < n) {
+            float a = pa[m];
+            float b = has_b ? pb[m] : 0.f;
+            if (log_in) {  // -ln(max(raw, 1) / i0), fbp.py:80-83
+                a = -logf(__fdiv_rn(fmaxf(a, 1.f), i0));
+                b = has_b ? -logf(__fdiv_rn(fmaxf(b, 1.f), i0)) : 0.f;
+            }
+            z = make_float2(a, b);
+        }
+        sbuf[pad_idx(m)] = z;
+    }
+    __syncthreads();
+
+    if (radius > 0) {  // scipy gaussian_filter1d(mode="nearest") restated (fbp.py:125-126)
+        float2 acc[16];
+        int cnt = 0;
+        for (int m = tid; m < n; m += T, ++cnt) {
+            float2 s = make_float2(0.f, 0.f);
+            for (int j = -radius; j <= radius; ++j) {
+                int c = min(max(m + j, 0), n - 1);
+                float wj = __ldg(&blur[j + radius]);
+                float2 x = sbuf[pad_idx(c)];
+                s.x = fmaf(wj, x.x, s.x);
+                s.y = fmaf(wj, x.y, s.y);
+            }
+            acc[cnt] = s;
+        }
+        __syncthreads();
+        cnt = 0;
+        for (int m = tid; m < n; m += T, ++cnt) sbuf[pad_idx(m)] = acc[cnt];
+        __syncthreads();
+    }
+
+    fft_forward(sbuf, tw, P, log2P, tid, T);
+
+    // X <- conj(X * M / P): the inverse transform is conj(FFT(conj(.)))
+    for (int m = tid; m < P; m += T) {
+        float g = __ldg(&mult[m <= P / 2 ? m : P - m]);
+        float2 x = sbuf[pad_idx(m)];
+        sbuf[pad_idx(m)] = make_float2(x.x * g, -x.y * g);
+    }
+    __syncthreads();
+
+    fft_forward(sbuf, tw, P, log2P, tid, T);
+
+    float* oa = out + line_offset(la, n, map);
+    float* ob = has_b ? out + line_offset(la + 1, n, map) : nullptr;
+    for (int m = tid; m < n; m += T) {
+        float2 y = sbuf[pad_idx(m)];
+        oa[m] = y.x;
+        if (has_b) ob[m] = -y.y;
+    }
+}
+
+template <typename T>
+__global__ void preprocess_kernel(const T* __restrict__ raw, double* __restrict__ out, long long n, double i0) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    long long step = (long long)gridDim.x * blockDim.x;
+    for (; i < n; i += step) {
+        double c = fmax((double)raw[i], 1.0);  // LOG_CLAMP_COUNTS, fbp.py:26
+        out[i] = -log(__ddiv_rn(c, i0));
+    }
+}
+
+}  // namespace
+}  // namespace tf
+
+using namespace tf;
+
+extern "C" int tf_filter_multiplier(int kind, int64_t padded, double pixel_pitch, double* host_out) {
+    if (kind != TF_FILTER_RAMLAK && kind != TF_FILTER_SHEPPLOGAN)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "unknown filter kind %d", kind);
+    if (padded < 1 || !(pixel_pitch > 0) || !host_out)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "invalid multiplier arguments");
+    multiplier_fp64(kind, padded, pixel_pitch, host_out);
+    return TF_OK;
+}
+
+extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, double pixel_pitch,
+                                     double blur_sigma, tf_filter_plan** plan) {
+    if (!plan) return set_error(TF_ERR_INVALID_ARGUMENT, "null plan pointer");
+    *plan = nullptr;
+    if (kind != TF_FILTER_RAMLAK && kind != TF_FILTER_SHEPPLOGAN)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "unknown filter kind %d", kind);
+    if (n_chan < 1) return set_error(TF_ERR_INVALID_ARGUMENT, "n_chan must be >= 1");
+    if (blur_sigma < 0) return set_error(TF_ERR_INVALID_ARGUMENT, "blur_sigma must be >= 0");
+    if (!(pixel_pitch > 0)) return set_error(TF_ERR_INVALID_ARGUMENT, "pixel_pitch must be positive");
+    const long long need = 2LL * n_chan;
+    if (padded != 0 && padded < need)  // FilterSpec.padded_length, fbp.py:50-55
+        return set_error(TF_ERR_INVALID_ARGUMENT, "padding %lld below required %lld for %d channels",
+                         (long long)padded, need, n_chan);
+    int P = 1;
+    while (P < need) P <<= 1;
+    if (P > 16 * 1024) return set_error(TF_ERR_UNSUPPORTED, "n_chan %d exceeds the 8192-channel filter kernel", n_chan);
+    auto* p = new tf_filter_plan();
+    p->n = n_chan;
+    p->P = P;
+    p->log2P = ilog2(P);
+    p->threads = std::max(32, std::min(1024, P / 16));
+    // twiddles in fp64, rounded once
+    std::vector<float2> tw(P);
+    for (int m = 0; m < P; ++m) {
+        double a = -2.0 * M_PI * (double)m / (double)P;
+        tw[m] = make_float2((float)cos(a), (float)sin(a));
+    }
+    std::vector<double> mult(P / 2 + 1);
+    multiplier_fp64(kind, P, pixel_pitch, mult.data());
+    std::vector<float> multf(P / 2 + 1);
+    for (int k = 0; k <= P / 2; ++k) multf[k] = (float)(mult[k] / (double)P);
+    int rad = 0;
+    std::vector<float> bw;
+    if (blur_sigma > 0) {  // scipy: radius = int(truncate * sigma + 0.5), truncate 4
+        rad = (int)(4.0 * blur_sigma + 0.5);
+        std::vector<double> w(2 * rad + 1);
+        double sum = 0;
+        for (int j = -rad; j <= rad; ++j) {
+            w[j + rad] = exp(-0.5 / (blur_sigma * blur_sigma) * (double)j * (double)j);
+            sum += w[j + rad];
+        }
+        bw.resize(2 * rad + 1);
+        for (int j = 0; j <= 2 * rad; ++j) bw[j] = (float)(w[j] / sum);
+        if (n_chan > 16 * p->threads) {
+            delete p;
+            return set_error(TF_ERR_UNSUPPORTED, "blur path supports n_chan <= 16*threads");
+        }
+    }
+    p->blur_radius = rad;
+    cudaError_t e = cudaMalloc(&p->d_tw, sizeof(float2) * P);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_mult, sizeof(float) * (P / 2 + 1));
+    if (e == cudaSuccess && rad > 0) e = cudaMalloc(&p->d_blur, sizeof(float) * (2 * rad + 1));
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_tw, tw.data(), sizeof(float2) * P, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_mult, multf.data(), sizeof(float) * (P / 2 + 1), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && rad > 0)
+        e = cudaMemcpy(p->d_blur, bw.data(), sizeof(float) * (2 * rad + 1), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        int smem = (P + P / 16) * (int)sizeof(float2);
+        e = cudaFuncSetAttribute(ramp_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    }
+    if (e != cudaSuccess) {
+        tf_filter_plan_destroy(p);
+        return set_error(TF_ERR_CUDA, "filter plan setup failed: %s", cudaGetErrorString(e));
+    }
+    *plan = p;
+    return TF_OK;
+}
+
+extern "C" int tf_filter_plan_destroy(tf_filter_plan* p) {
+    if (!p) return TF_OK;
+    cudaFree(p->d_tw);
+    cudaFree(p->d_mult);
+    cudaFree(p->d_blur);
+    delete p;
+    return TF_OK;
+}
+
+extern "C" int tf_filter(const tf_filter_plan* p, const float* in, float* out, int64_t n_lines, float i0,
+                         int rows_per_angle, int n_slabs, const int32_t* slab_row0, const int64_t* slab_base,
+                         void* stream) {
+    if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null filter plan");
+    if (n_lines < 0) return set_error(TF_ERR_INVALID_ARGUMENT, "n_lines must be >= 0");
+    if (n_lines == 0) return TF_OK;
+    if (!in || !out) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    SlabMap map{};
+    map.n_slabs = n_slabs;
+    map.rows_per_angle = rows_per_angle;
+    if (n_slabs > 0) {
+        if (n_slabs > 8 || rows_per_angle < 1 || !slab_row0 || !slab_base || in == out)
+            return set_error(TF_ERR_INVALID_ARGUMENT, "invalid slab map");
+        for (int s = 0; s <= n_slabs; ++s) map.row0[s] = slab_row0[s];
+        for (int s = 0; s < n_slabs; ++s) map.base[s] = slab_base[s];
+        if (map.row0[0] != 0 || map.row0[n_slabs] != rows_per_angle)
+            return set_error(TF_ERR_INVALID_ARGUMENT, "slab rows must cover [0, rows_per_angle)");
+    }
+    long long pairs = (n_lines + 1) / 2;
+    int smem = (p->P + p->P / 16) * (int)sizeof(float2);
+    ramp_filter_kernel<<<(unsigned)pairs, p->threads, smem, as_stream(stream)>>>(
+        in, out, n_lines, p->n, p->P, p->log2P, p->d_tw, p->d_mult, p->d_blur, p->blur_radius, i0, map);
+    return check_launch("ramp_filter_kernel");
+}
+
+extern "C" int tf_preprocess(const void* raw, int raw_dtype, double* out, int64_t n, double i0, void* stream) {
+    if (!(i0 > 0)) return set_error(TF_ERR_INVALID_ARGUMENT, "i0 must be positive, got %g", i0);
+    if (n < 0 || (raw_dtype != TF_F32 && raw_dtype != TF_F64)) return set_error(TF_ERR_INVALID_ARGUMENT, "bad arguments");
+    if (n == 0) return TF_OK;
+    if (!raw || !out) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    if (raw_dtype == TF_F32)
+        preprocess_kernel<float><<<blocks, 256, 0, as_stream(stream)>>>(static_cast<const float*>(raw), out, n, i0);
+    else
+        preprocess_kernel<double><<<blocks, 256, 0, as_stream(stream)>>>(static_cast<const double*>(raw), out, n, i0);
+    return check_launch("preprocess_kernel");
+}

@@ -1,0 +1,26 @@
+// Host-side plumbing shared by the tomofuse-b200 translation units.
+#pragma once
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/tomofuse_b200.h"
+
+namespace tf {
+
+int set_error(int status, const char* fmt, ...);
+int check_launch(const char* what);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+#define TF_CUDA_TRY(expr)                                                                            \
+    do {                                                                                             \
+        cudaError_t _e = (expr);                                                                     \
+        if (_e != cudaSuccess)                                                                       \
+            return ::tf::set_error(TF_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));   \
+    } while (0)
+
+}  // namespace tf

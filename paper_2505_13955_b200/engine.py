@@ -1,0 +1,111 @@
+"""Device-resident FBP engine: the reconstruction stage of `pipeline.run`
+(`/root/reference/pkg/src/tomofuse/pipeline.py:163-237`) as one GPU pass.
+
+One `SlabReconstructor` owns the HBM buffers for a row slab [r0, r1) of one
+specimen and runs, all on one CUDA stream:
+
+    raw counts (n_proj, k, n_chan) fp32
+      --K1 tf_filter--> filtered (Beer-Lambert + ramp, fp32)
+      --tf_bp_stage--> z-blocked staging (feather folded in)
+      --K2 tf_backproject--> volume (k, ny, nx) fp32
+      [--K3 tf_quantize--> uint16]
+
+which is exactly `preprocess -> ramp_filter -> astype(float32) ->
+back_project(dtype=float32)` of pipeline.py:176-222 / fbp.reconstruct.
+Buffers are allocated once; `run()` never allocates, so the step can be
+timed (and CUDA-graph captured) without allocator noise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from ._lib import check, lib
+from .fbp import FilterSpec, bp_plan, filter_plan
+from .geometry import AcquisitionParams, VolumeDims
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class SlabReconstructor:
+    def __init__(self, params: AcquisitionParams, dims: VolumeDims, spec: FilterSpec | None = None,
+                 i0: float = 1e5, feather_band: int = 32, rows: tuple[int, int] | None = None,
+                 device=None, in_place_filter: bool = False):
+        import torch
+
+        self.torch = torch
+        self.params, self.dims = params, dims
+        self.spec = spec if spec is not None else FilterSpec()
+        self.i0 = float(i0)
+        self.r0, self.r1 = rows if rows is not None else (0, params.n_rows)
+        self.k = self.r1 - self.r0
+        self.device = torch.device(device if device is not None else "cuda")
+        with torch.cuda.device(self.device):
+            self.fplan = filter_plan(params.n_chan, self.spec, params.pixel_pitch)
+            self.bplan = bp_plan(params, dims, feather_band)
+            self.in_place = in_place_filter
+            shape = (params.n_proj, self.k, params.n_chan)
+            self.filt = None if in_place_filter else torch.empty(shape, dtype=torch.float32,
+                                                                   device=self.device)
+            self.stage = torch.empty(self.bplan.stage_bytes(self.k), dtype=torch.uint8,
+                                     device=self.device)
+            self.vol = torch.empty((self.k, dims.ny, dims.nx), dtype=torch.float32,
+                                   device=self.device)
+
+    # -- individual kernels (stream = torch current stream unless given)
+    def _s(self, stream):
+        st = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        return ctypes.c_void_p(st.cuda_stream)
+
+    def filter(self, raw, out=None, stream=None, i0=None):
+        """K1 on raw counts (or depth when i0 <= 0)."""
+        out = out if out is not None else (raw if self.in_place else self.filt)
+        n_lines = raw.numel() // self.params.n_chan
+        check(lib().tf_filter(self.fplan.handle, _ptr(raw), _ptr(out), n_lines,
+                              self.i0 if i0 is None else float(i0), 0, 0, None, None, self._s(stream)))
+        return out
+
+    def stage_rows(self, filt, rows_per_angle=None, r0=0, stream=None):
+        rpa = rows_per_angle if rows_per_angle is not None else self.k
+        check(lib().tf_bp_stage(self.bplan.handle, _ptr(filt), rpa, r0, r0 + self.k, _ptr(self.stage),
+                                self._s(stream)))
+
+    def backproject(self, a0=0, a1=None, flags=_lib.TF_BP_FINALIZE, stream=None, vol=None):
+        a1 = self.params.n_proj if a1 is None else a1
+        vol = self.vol if vol is None else vol
+        check(lib().tf_backproject(self.bplan.handle, _ptr(self.stage), self.k, _ptr(vol), a0, a1,
+                                   0, self.dims.nx, 0, self.dims.ny, flags, self._s(stream)))
+        return vol
+
+    def quantize(self, lo, hi, out, stream=None):
+        check(lib().tf_quantize(_ptr(self.vol), _lib.TF_F32, _ptr(out), self.vol.numel(), float(lo),
+                                float(hi), self._s(stream)))
+        return out
+
+    def run(self, raw, stream=None):
+        """raw: device (n_proj, k, n_chan) fp32 counts -> self.vol."""
+        filt = self.filter(raw, stream=stream)
+        self.stage_rows(filt, stream=stream)
+        return self.backproject(stream=stream)
+
+    def updates(self) -> int:
+        """Voxel x projection updates of one run (pipeline.py:225-227 convention)."""
+        return self.params.n_proj * self.k * self.dims.nx * self.dims.ny
+
+
+def phantom_raw(params: AcquisitionParams, dims: VolumeDims, out, a0=0, a1=None, r0=0, r1=None,
+                i0=1e5, mu_max=3.5e-4, stream=None):
+    """Analytic 3-D Shepp-Logan raw counts (K4) into device tensor `out`
+    of shape (a1-a0, r1-r0, n_chan)."""
+    import torch
+
+    a1 = params.n_proj if a1 is None else a1
+    r1 = params.n_rows if r1 is None else r1
+    g = _lib.geometry(params, dims)
+    st = stream if stream is not None else torch.cuda.current_stream()
+    check(lib().tf_phantom_sinogram(ctypes.byref(g), a0, a1, r0, r1, float(i0), float(mu_max),
+                                    _ptr(out), ctypes.c_void_p(st.cuda_stream)))
+    return out
