@@ -1,0 +1,469 @@
+#!/usr/bin/env python
+"""Benchmark: FBP reconstruction of the 2048^3 / 1800-projection volume (C3).
+
+    python bench.py [--gpus N --steps K --warmup W]            # our sm_100a path
+    python bench.py --impl reference ...                        # CPU reference arm
+    torchrun --nproc-per-node N bench.py --gpus N ...           # z-slab multi-GPU
+
+A step = one complete reconstruction of the volume: raw counts (resident in
+HBM) -> K1 Beer-Lambert + ramp filter -> [row-slab exchange over NCCL] ->
+z-block staging -> K2 back-projection -> fp32 volume.  `value` is whole-job
+GUPS (voxel x projection updates / s, N_p*N^3 convention of
+pipeline.py:225-227) over the max-over-ranks device time; `e2e` is the same
+through host pinned buffers (H2D of the raw counts + D2H of the volume inside
+every timed step).  Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FDK backprojection GUPS & s/volume at 2048³ (1/2/4/8 B200) vs CPU ref"
+CONFIGS = {
+    "c1": dict(n=128, n_proj=180),
+    "c2": dict(n=512, n_proj=720),
+    "c3": dict(n=2048, n_proj=1800),
+}
+PITCH = 12.0   # um (config.py:40,47)
+I0 = 1e5       # config.py:59
+SM_COUNT = 148
+SMEM_BYTES_PER_CLK = 128  # per SM
+TX = TY = 16   # BP tile (csrc/backproject.cu)
+ZB = 32
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "allgather"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--cpu-angles", type=int, default=None,
+                    help="angles per CPU-baseline sample (default sized for ~10 s)")
+    return ap.parse_args()
+
+
+def geometry(cfg):
+    from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
+
+    n, n_proj = cfg["n"], cfg["n_proj"]
+    p = AcquisitionParams(n_proj=n_proj, n_rows=n, n_chan=n, pixel_pitch=PITCH)
+    d = VolumeDims(n, n, n, voxel_pitch=PITCH)
+    return p, d
+
+
+def workload_desc(cfg):
+    n, n_proj = cfg["n"], cfg["n_proj"]
+    return (f"{n}^3 volume from {n_proj} parallel-beam projections of {n}x{n}, span pi, "
+            f"Ram-Lak, pitch {PITCH:g} um, i0 {I0:g}")
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+        self.proc = None
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "200"], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power)}
+
+
+# ---------------------------------------------------------------- CPU reference arm
+def _cpu_worker(args):
+    """One process: the reference chain (numpy port, fp32 pipeline path of
+    pipeline.py:176-222) on one detector row and the first `na` angles."""
+    raw_row, n_proj_full, n, na = args
+    import numpy as np
+
+    from oracle import fbp_oracle as O
+
+    span = math.pi * na / n_proj_full  # same angular positions as the full scan
+    geom = O.make_geom(na, 1, n, pixel_pitch=PITCH, voxel_pitch=PITCH, span=span)
+    t0 = time.perf_counter()
+    depth = O.preprocess(raw_row, I0)
+    filt = O.ramp_filter(depth, pixel_pitch=PITCH).astype(np.float32)
+    O.back_project(filt, geom, dtype=np.float32)
+    return time.perf_counter() - t0
+
+
+def cpu_reference(cfg, steps, warmup, na=None, raw_rows=None):
+    """Times the reference algorithm (oracle numpy port) on all host cores:
+    one process per core, each a full slice x `na` angles.  Returns
+    (GUPS per step list, info)."""
+    import multiprocessing as mp
+
+    import numpy as np
+
+    from oracle import phantom_cpu
+
+    n, n_proj = cfg["n"], cfg["n_proj"]
+    cores = os.cpu_count() or 1
+    if na is None:  # ~8-10 s per step at ~0.03 GUPS per core
+        na = max(4, min(n_proj, int(2.5e8 / (n * n))))
+    rows = np.linspace(0, n - 1, cores).astype(int)
+    if raw_rows is None:
+        raw = phantom_cpu.raw_counts(n_proj, n, n, n, n, np.arange(na), rows, pixel_pitch=PITCH,
+                                     voxel_pitch=PITCH, i0=I0)
+    else:
+        raw = raw_rows[:na]
+    jobs = [(raw[:, i:i + 1, :].copy(), n_proj, n, na) for i in range(len(rows))]
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    ctx = mp.get_context("fork")
+    gups = []
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_worker, [(j[0][:1], n_proj, n, 1) for j in jobs])  # fork + import warm-up
+        for it in range(warmup + steps):
+            t0 = time.perf_counter()
+            pool.map(_cpu_worker, jobs, chunksize=1)
+            dt = time.perf_counter() - t0
+            if it >= warmup:
+                gups.append(len(jobs) * na * n * n / dt / 1e9)
+    cpu_model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu_model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    info = {"cores": cores, "kind": "port",
+            "sample": (f"{len(jobs)} processes x 1 detector row x first {na} of {n_proj} angles x full "
+                       f"{n}x{n} slice (preprocess + ramp_filter + back_project float32, numpy port of "
+                       f"fbp.py in oracle/fbp_oracle.py); rows {rows.tolist()}; CPU {cpu_model}"),
+            "updates_per_step": len(jobs) * na * n * n}
+    return gups, info
+
+
+def run_reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    gups, info = cpu_reference(cfg, args.steps, args.warmup, args.cpu_angles)
+    v = statistics.mean(gups)
+    n, n_proj = cfg["n"], cfg["n_proj"]
+    total = n_proj * n ** 3
+    line = {
+        "metric": METRIC, "value": round(v, 6), "unit": "GUPS", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(info["updates_per_step"] / (v * 1e9) * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (analytic 3-D Shepp-Logan raw counts)", "impl": "reference",
+        "config": {"workload": workload_desc(cfg), "volume": [n, n, n], "n_proj": n_proj},
+        "s_per_volume_extrapolated": round(total / (v * 1e9), 1),
+        "cpu_baseline": {"value": round(v, 6), "unit": "GUPS", "cores": info["cores"], "kind": info["kind"],
+                         "sample": info["sample"]},
+        "e2e": {"value": round(v, 6), "unit": "GUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def executed_updates(d, n_proj, k):
+    """Updates the BP kernel really executes: tiles wholly outside the FoV
+    are skipped (same fp64 test as bp_kernel), rows padded to 32."""
+    import numpy as np
+
+    cx, cy = (d.nx - 1) / 2.0, (d.ny - 1) / 2.0
+    R2 = ((d.nx - 1) / 2.0) ** 2  # normal scan, n_chan == nx, scale 1
+    active = 0
+    for ty in range(0, d.ny, TY):
+        for tx in range(0, d.nx, TX):
+            xs = np.arange(tx, min(tx + TX, d.nx))
+            ys = np.arange(ty, min(ty + TY, d.ny))
+            rr = ((xs[None, :] - cx) ** 2 + (ys[:, None] - cy) ** 2)
+            if (rr <= R2).any():
+                active += 1
+    return active * TX * TY * n_proj * (-(-k // ZB) * ZB), active
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_13955_b200.engine import SlabReconstructor, phantom_raw
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    p, d = geometry(cfg)
+    n, n_proj = cfg["n"], cfg["n_proj"]
+    total_updates = n_proj * n * n * n
+
+    # ---- setup: engine + synthetic raw counts generated on the device (K4)
+    if world > 1:
+        from paper_2505_13955_b200.distributed import ZSlabReconstructor
+
+        eng = ZSlabReconstructor(p, d, i0=I0, exchange_mode=args.exchange, device=dev)
+        raw = torch.empty(eng.chunk_shape(), dtype=torch.float32, device=dev)
+        phantom_raw(p, d, raw, a0=eng.a0, a1=eng.a1)
+        slab = eng.local
+        k_rows = eng.r1 - eng.r0
+
+        def step_parts():
+            eng.filter(raw)
+            eng.exchange()
+            eng.stage()
+            bp_ev[0].record()
+            eng.local.backproject()
+            bp_ev[1].record()
+    else:
+        eng = slab = SlabReconstructor(p, d, i0=I0, device=dev)
+        raw = torch.empty((n_proj, n, n), dtype=torch.float32, device=dev)
+        phantom_raw(p, d, raw)
+        k_rows = n
+
+        def step_parts():
+            eng.filter(raw)
+            eng.stage_rows(eng.filt)
+            bp_ev[0].record()
+            eng.backproject()
+            bp_ev[1].record()
+
+    torch.cuda.synchronize()
+    bp_ev = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+    for _ in range(args.warmup):
+        step_parts()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---- timed region: K device-resident steps
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for e in evs:
+        bp_ev = [e[1], e[2]]
+        e[0].record()
+        step_parts()
+        e[3].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [e[0].elapsed_time(e[3]) for e in evs]
+    bp_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    t_tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_tot, op=dist.ReduceOp.MAX)
+    ms_per_step = t_tot.item() / args.steps
+    gups = total_updates / (ms_per_step / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (K2 BP) on this rank
+    bp_avg_ms = statistics.mean(bp_ms)
+    exec_upd, active_tiles = executed_updates(d, n_proj, k_rows)
+    sm_mhz = clk.get("sm_mhz") or 1965.0
+    smem_peak = SMEM_BYTES_PER_CLK * SM_COUNT * sm_mhz * 1e6 / 1e9  # GB/s
+    smem_achieved = exec_upd * 8 / (bp_avg_ms / 1e3) / 1e9
+    fp32_peak_tflops = 128 * 2 * SM_COUNT * sm_mhz * 1e6 / 1e12
+    fp32_achieved = exec_upd * 4 / (bp_avg_ms / 1e3) / 1e12
+    slab_updates = n_proj * k_rows * n * n
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    stage_bytes = slab.stage.numel()
+    hbm_alg = stage_bytes + slab.vol.numel() * 4  # one pass over the staged slab + the volume write
+
+    # ---- e2e through host pinned buffers
+    e2e = None
+    if not args.no_e2e:
+        ke = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 2))
+        h_raw = torch.empty(raw.shape, dtype=torch.float32, pin_memory=True)
+        h_raw.copy_(raw)
+        h_vol = torch.empty(slab.vol.shape, dtype=torch.float32, pin_memory=True)
+
+        def e2e_step():
+            raw.copy_(h_raw, non_blocking=True)
+            if world > 1:
+                eng.run(raw)
+            else:
+                eng.run(raw)
+            h_vol.copy_(slab.vol, non_blocking=True)
+
+        e2e_step()  # warm the copy path
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record()
+        for _ in range(ke):
+            e2e_step()
+        eb.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([ea.elapsed_time(eb) / ke], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = te.item()
+        e2e = {"value": round(total_updates / (e2e_ms / 1e3) / 1e9, 3), "unit": "GUPS",
+               "h2d_bytes_per_step": int(raw.numel() * 4), "d2h_bytes_per_step": int(slab.vol.numel() * 4),
+               "s_per_volume": round(e2e_ms / 1e3, 4), "steps": ke,
+               "note": "per rank bytes; pinned host in/out, copies serial with compute on one stream"}
+
+    # ---- parity spot check on the bench data (rank 0): 2 rows x 256^2 centre tile vs the C oracle
+    parity = None
+    if rank == 0 and not args.no_parity and world == 1:
+        try:
+            from oracle import c_oracle as C
+            from oracle import fbp_oracle as O
+
+            rows = [n // 2, n // 3]
+            t = min(256, n)
+            x0 = (n - t) // 2
+            raw_rows = raw[:, rows].cpu().numpy()
+            filt = O.ramp_filter(O.preprocess(raw_rows, I0), pixel_pitch=PITCH)
+            geom = O.make_geom(n_proj, len(rows), n, pixel_pitch=PITCH, voxel_pitch=PITCH)
+            tile = (x0, x0 + t, x0, x0 + t)
+            ref = C.back_project(filt, geom, tile=tile)[:, x0:x0 + t, x0:x0 + t]
+            got = slab.vol[rows][:, x0:x0 + t, x0:x0 + t].cpu().numpy().astype(np.float64)
+            parity = {"rel_l2_vs_f64_oracle": float(np.linalg.norm(got - ref) / np.linalg.norm(ref)),
+                      "max_abs": float(np.abs(got - ref).max()), "rows": rows, "tile": list(tile)}
+        except Exception as ex:  # never let the checker break the bench line
+            parity = {"error": repr(ex)}
+
+    # ---- CPU baseline (rank 0, N=1 only): the reference chain on the same raw rows
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        na = args.cpu_angles or max(4, min(n_proj, int(2.5e8 / (n * n))))
+        rows_idx = np.linspace(0, n - 1, cores).astype(int)
+        raw_rows = raw[:na][:, rows_idx].cpu().numpy()
+        g_cpu, info = cpu_reference(cfg, 1, 0, na, raw_rows=raw_rows)
+        v = g_cpu[0]
+        cpu_baseline = {"value": round(v, 6), "unit": "GUPS", "cores": info["cores"], "kind": info["kind"],
+                        "sample": info["sample"] + " (same raw rows the GPU consumed)",
+                        "s_per_volume_extrapolated": round(total_updates / (v * 1e9), 1)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC,
+        "value": round(gups, 3),
+        "unit": "GUPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 3),
+        "s_per_volume": round(ms_per_step / 1e3, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (analytic 3-D Shepp-Logan raw counts generated on device, i0=1e5)",
+        "config": {"workload": workload_desc(cfg), "volume": [n, n, n], "n_proj": n_proj,
+                   "parallelism": f"z-slab x{world}" + (f" ({args.exchange} exchange)" if world > 1 else ""),
+                   "l2": "inputs larger than L2 (raw %.1f GB, volume %.1f GB per step)" % (
+                       raw.numel() * 4 / 1e9, slab.vol.numel() * 4 / 1e9),
+                   "step": "K1 filter (+Beer-Lambert) -> [exchange] -> stage -> K2 back-project"},
+        "roofline": {
+            "bound": "smem",
+            "kernel": "bp_kernel (K2)",
+            "achieved": round(smem_achieved, 1),
+            "peak": round(smem_peak, 1),
+            "unit": "GB/s",
+            "frac": round(smem_achieved / smem_peak, 4),
+            "traffic": None,
+            "peak_source": "derived: 128 B/clk/SM x 148 SMs x measured median SM clock "
+                           "(shared-memory data path; no tensor-core or HBM bound applies, SURVEY 8d)",
+            "algorithmic_bytes_per_update": 8,
+            "bp_ms_per_launch": round(bp_avg_ms, 3),
+            "executed_updates_per_launch": exec_upd,
+            "active_tiles": active_tiles,
+            "bp_gups_executed": round(exec_upd / (bp_avg_ms / 1e3) / 1e9, 1),
+            "bp_gups_full_count": round(slab_updates / (bp_avg_ms / 1e3) / 1e9, 1),
+            "fp32_tflops": round(fp32_achieved, 2),
+            "fp32_frac": round(fp32_achieved / fp32_peak_tflops, 4),
+            "hbm_gbs_algorithmic": round(hbm_alg / (bp_avg_ms / 1e3) / 1e9, 1),
+            "hbm_peak_measured": peaks.get("hbm_gbs"),
+        },
+        "clocks": clk,
+        "gpu_launches": 3 * args.steps,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if cpu_baseline is not None:
+        line["cpu_baseline"] = cpu_baseline
+    if parity is not None:
+        line["parity"] = parity
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

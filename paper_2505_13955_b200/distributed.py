@@ -1,0 +1,158 @@
+"""Multi-GPU z-slab reconstruction (one process per GPU, NCCL over NVLink).
+
+Replaces the reference's simulated P_row partition (partition.py:221,
+PAPER.md:253-255) and its in-process `Fabric` (fabric.py:25-127) with real
+devices:
+
+* rank g owns detector rows / volume slices `split_range(n_rows, N)[g]`
+  and back-projects ALL angles for them -- rows are independent
+  (pkg/tests/test_fbp.py:180-191), so there is no reduction and the N-GPU
+  volume is bitwise the 1-GPU volume;
+* rank g ingests and filters the angle chunk `split_range(n_proj, N)[g]`
+  (all rows), i.e. 1/N of the projections, as north_star prescribes;
+* filtered rows reach their owner through one collective:
+    - "alltoall" (default, minimal bytes): K1 writes its output already
+      grouped slab-major, so a single `all_to_all_single` lands every
+      owner's rows angle-ordered in its staging input;
+    - "allgather" (north_star's literal variant): `all_gather_into_tensor`
+      of the natural-layout chunks, N x the bytes, owners stage their rows.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from ._lib import check, lib
+from .engine import SlabReconstructor
+from .fbp import FilterSpec
+from .geometry import AcquisitionParams, VolumeDims, split_range
+
+
+def exchange_layout(world: int, rank: int, n_proj: int, n_rows: int, n_chan: int):
+    """Row-slab all-to-all layout for `rank`.
+
+    Returns (slabs, chunks, slab_row0, slab_base, in_splits, out_splits):
+    element offsets of each destination's block in the send buffer
+    (slab-major: [dest][angle][row-in-slab][chan]) and the split sizes of
+    `all_to_all_single`, in elements.
+    """
+    slabs = split_range(n_rows, world)
+    chunks = split_range(n_proj, world)
+    a0, a1 = chunks[rank]
+    A = a1 - a0
+    r0, r1 = slabs[rank]
+    slab_row0 = [s for s, _ in slabs] + [n_rows]
+    slab_base = [A * s * n_chan for s, _ in slabs]
+    in_splits = [A * (e - s) * n_chan for s, e in slabs]
+    out_splits = [(ce - cs) * (r1 - r0) * n_chan for cs, ce in chunks]
+    return slabs, chunks, slab_row0, slab_base, in_splits, out_splits
+
+
+def slab_major(chunk, slabs):
+    """Host/torch restatement of K1's slab-major output mapping (test helper
+    and documentation of tf_filter's slab map): (A, n_rows, n_chan) ->
+    flat [dest][A][rows_in_slab][n_chan]."""
+    import torch
+
+    return torch.cat([chunk[:, s:e].reshape(-1) for s, e in slabs])
+
+
+def exchange(send, recv, in_splits, out_splits, group=None):
+    import torch.distributed as dist
+
+    dist.all_to_all_single(recv, send, output_split_sizes=out_splits, input_split_sizes=in_splits,
+                           group=group)
+
+
+class ZSlabReconstructor:
+    """Per-rank state of an N-GPU z-slab reconstruction."""
+
+    def __init__(self, params: AcquisitionParams, dims: VolumeDims, spec: FilterSpec | None = None,
+                 i0: float = 1e5, feather_band: int = 32, exchange_mode: str = "alltoall",
+                 group=None, device=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch = torch
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.mode = exchange_mode
+        self.params, self.dims = params, dims
+        n_proj, n_rows, n_chan = params.n_proj, params.n_rows, params.n_chan
+        (self.slabs, self.chunks, row0, base, self.in_splits,
+         self.out_splits) = exchange_layout(self.world, self.rank, n_proj, n_rows, n_chan)
+        self.a0, self.a1 = self.chunks[self.rank]
+        self.r0, self.r1 = self.slabs[self.rank]
+        self.device = torch.device(device if device is not None else "cuda")
+        if exchange_mode == "allgather":
+            sizes = {e - s for s, e in self.chunks}
+            if len(sizes) != 1:
+                raise ValueError("allgather exchange needs n_proj divisible by the world size")
+        elif exchange_mode != "alltoall":
+            raise ValueError(f"unknown exchange mode {exchange_mode!r}")
+        # local slab engine; its `filt` buffer is the all-to-all landing zone
+        self.local = SlabReconstructor(params, dims, spec, i0, feather_band, rows=(self.r0, self.r1),
+                                       device=self.device)
+        A = self.a1 - self.a0
+        self.send = torch.empty(A * n_rows * n_chan, dtype=torch.float32, device=self.device)
+        if exchange_mode == "allgather":
+            self.gathered = torch.empty((n_proj, n_rows, n_chan), dtype=torch.float32,
+                                        device=self.device)
+            self._map = None
+        else:
+            self.gathered = None
+            self._map = ((ctypes.c_int32 * len(row0))(*row0), (ctypes.c_int64 * len(base))(*base))
+
+    def chunk_shape(self):
+        return (self.a1 - self.a0, self.params.n_rows, self.params.n_chan)
+
+    def _s(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def filter(self, raw_chunk):
+        """K1 over this rank's angle chunk, written in the exchange layout."""
+        p = self.params
+        n_lines = raw_chunk.numel() // p.n_chan
+        if self._map is None:
+            check(lib().tf_filter(self.local.fplan.handle, ctypes.c_void_p(raw_chunk.data_ptr()),
+                                  ctypes.c_void_p(self.send.data_ptr()), n_lines, self.local.i0,
+                                  0, 0, None, None, self._s()))
+        else:
+            row0, base = self._map
+            check(lib().tf_filter(self.local.fplan.handle, ctypes.c_void_p(raw_chunk.data_ptr()),
+                                  ctypes.c_void_p(self.send.data_ptr()), n_lines, self.local.i0,
+                                  p.n_rows, self.world, row0, base, self._s()))
+
+    def exchange(self):
+        import torch.distributed as dist
+
+        if self.mode == "allgather":
+            dist.all_gather_into_tensor(self.gathered.view(-1), self.send, group=self.group)
+        else:
+            exchange(self.send, self.local.filt.view(-1), self.in_splits, self.out_splits, self.group)
+
+    def stage(self):
+        if self.mode == "allgather":
+            self.local.stage_rows(self.gathered, rows_per_angle=self.params.n_rows, r0=self.r0)
+        else:
+            self.local.stage_rows(self.local.filt)
+
+    def run(self, raw_chunk):
+        """raw_chunk: device (A, n_rows, n_chan) fp32 counts of this rank's
+        angles -> this rank's volume slab (k, ny, nx) in self.local.vol."""
+        self.filter(raw_chunk)
+        self.exchange()
+        self.stage()
+        return self.local.backproject()
+
+    def updates(self) -> int:
+        return self.local.updates()
+
+    def exchange_bytes(self) -> int:
+        """Bytes this rank receives from peers per run."""
+        if self.mode == "allgather":
+            return int(np.prod(self.chunk_shape())) * 4 * (self.world - 1)
+        return sum(s for i, s in enumerate(self.out_splits) if i != self.rank) * 4
