@@ -125,7 +125,10 @@ TF_API int tf_bp_stage(const tf_bp_plan* plan, const float* sino, int rows_per_a
 
 enum {
     TF_BP_ACCUMULATE = 1, /* add to the unscaled partial sums already in vol */
-    TF_BP_FINALIZE = 2    /* apply FoV mask + angle_span/n_proj scale (fbp.py:246-251) */
+    TF_BP_FINALIZE = 2,   /* apply FoV mask + angle_span/n_proj scale (fbp.py:246-251) */
+    TF_BP_KERNEL_V1 = 4   /* force the 1-voxel 2-tap kernel (default: 2x2-block
+                             4-tap kernel when voxel/pixel pitch <= 1.4; both
+                             give bit-identical volumes) */
 };
 
 /* Back-projects angles [a0, a1) of a staged slab of `n_rows` rows into

@@ -16,7 +16,7 @@ _lib = None
 
 TF_OK, TF_ERR_INVALID_ARGUMENT, TF_ERR_CUDA, TF_ERR_UNSUPPORTED, TF_ERR_OOM = 0, 1, 2, 3, 4
 TF_F32, TF_F64 = 0, 1
-TF_BP_ACCUMULATE, TF_BP_FINALIZE = 1, 2
+TF_BP_ACCUMULATE, TF_BP_FINALIZE, TF_BP_KERNEL_V1 = 1, 2, 4
 KIND = {"ramlak": 0, "shepplogan": 1}
 
 

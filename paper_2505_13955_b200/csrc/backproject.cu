@@ -34,7 +34,7 @@ struct tf_bp_plan {
     int feather_band;
     double2* d_trig;  // (cos, sin) of k * (span / n_proj), fp64 libm, per angle
     float* d_w;       // feather weights (fp32, as numpy casts them)
-    int W;            // channel window per tile-angle
+    double ext;       // max channel extent of a tile's rays over all angles
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
 };
@@ -42,11 +42,29 @@ struct tf_bp_plan {
 namespace tf {
 namespace {
 
-constexpr int TX = 16, TY = 16;           // voxel columns per CTA
-constexpr int NCW = 8;                    // consumer warps
-constexpr int NTHREADS = NCW * 32 + 32;   // + 1 producer warp
-constexpr int STAGES = 3, APS = 4;        // ring: 3 stages x 4 angles
-constexpr int ACC = kZB;                  // rows per thread
+constexpr int TX = 16, TY = 16;           // voxel columns per CTA tile
+constexpr int STAGES = 3, APS = 4;        // smem ring: 3 stages x 4 angles
+
+// Consumer layouts.  A thread owns a VX x VY block of voxel columns and ZT of
+// the tile's 32 rows.  NT detector taps per block serve all its voxels:
+//   V1 (1x1, NT=2, ZT=32): the classic two-tap gather, 8 B of smem per update.
+//   V4 (2x2, NT=4, ZT=16): the 2x2 block's rays span < sqrt(2)*scale + 1
+//       channels, so 4 consecutive taps cover all four voxels; each tap row
+//       is read once per block, 4 B of smem per update (half of V1).  The
+//       per-voxel weights are tents sat(1 - |u - j|): exactly {1-f, f} on the
+//       two live taps and 0 elsewhere, so the FMA sequence -- and the result
+//       -- is bit-identical to V1.
+template <int VX, int VY, int NT, int ZT>
+struct Layout {
+    static constexpr int BX = TX / VX, BY = TY / VY;   // blocks per tile
+    static constexpr int COLS = BX * BY;               // threads per z-group
+    static constexpr int ZG = kZB / ZT;                // z-groups
+    static constexpr int NCT = COLS * ZG;              // consumer threads
+    static constexpr int NCW = NCT / 32;               // consumer warps
+    static constexpr int NTHREADS = NCT + 32;          // + TMA producer warp
+    static constexpr int WX = BX / 8;                  // warps across a z-group (8x4 blocks each)
+    static_assert(COLS % 32 == 0 && BX % 8 == 0 && BY % 4 == 0, "warp tiling");
+};
 
 struct BPArgs {
     const double2* trig;
@@ -67,8 +85,10 @@ __device__ __forceinline__ bool outside_fov(int x, int y, const BPArgs& a) {
     return rr > a.R2;
 }
 
-__global__ void __launch_bounds__(NTHREADS, 2)
+template <int VX, int VY, int NT, int ZT>
+__global__ void __launch_bounds__(Layout<VX, VY, NT, ZT>::NTHREADS, (VX * VY == 1) ? 2 : 3)
     bp_kernel(const __grid_constant__ CUtensorMap map, const BPArgs args) {
+    using L = Layout<VX, VY, NT, ZT>;
     extern __shared__ __align__(128) uint8_t smem[];
     const int tx = blockIdx.x % args.ntx, ty = blockIdx.x / args.ntx, zb = blockIdx.y;
     const int X0 = tx * TX, Y0 = ty * TY;
@@ -112,7 +132,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCW);
+            mbar_init(&empty[s], L::NCW);
         }
         fence_barrier_init();
     }
@@ -121,7 +141,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     const int n_ang = args.a1 - args.a0;
     const int n_it = (n_ang + APS - 1) / APS;
 
-    if (warp == NCW) {
+    if (warp == L::NCW) {
         // ================= TMA producer (one thread)
         if (lane == 0) {
             tma_prefetch_desc(&map);
@@ -154,24 +174,35 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     }
 
     // ================= consumers
-    // warp patch 8x4 voxels, lanes in 4x2 quads (keeps each LDS.128 phase's
-    // channels within 8 consecutive rows -> distinct bank quads)
+    // z-group per warp (all lanes of a warp read the same 16-B column of a
+    // tap row); a warp covers 8x4 blocks, each 8-lane LDS.128 phase a 4x2
+    // patch, so a phase's tap rows stay within 8 consecutive channels ->
+    // distinct bank quads (row pitch 144 B = 9 quads).
+    const int zg = threadIdx.x / L::COLS;
+    const int wg = (threadIdx.x % L::COLS) >> 5;
     const int q = lane >> 3, i8 = lane & 7;
-    const int lx = (q & 1) * 4 + (i8 & 3), ly = (q >> 1) * 2 + (i8 >> 2);
-    const int dx = (warp & 1) * 8 + lx, dy = (warp >> 1) * 4 + ly;
-    const int x = X0 + dx, y = Y0 + dy;
-    const float fdx = (float)dx, fdy = (float)dy;
+    const int bx = (wg % L::WX) * 8 + (q & 1) * 4 + (i8 & 3);
+    const int by = (wg / L::WX) * 4 + (q >> 1) * 2 + (i8 >> 2);
+    const int dx0 = bx * VX, dy0 = by * VY;
     const size_t plane = (size_t)args.nx * args.ny;
-    const int nz = min(kZB, args.n_rows - zb * kZB);
-    const bool mine = x >= ux0 && x < ux1 && y >= uy0 && y < uy1;
+    const int zrow0 = zb * kZB + zg * ZT;                 // first volume row of this thread
+    const int nz = min(ZT, args.n_rows - zrow0);          // may be <= 0 for a ragged last block
 
-    float acc[ACC];
+    float acc[VX * VY][ZT];
 #pragma unroll
-    for (int j = 0; j < ACC; ++j) acc[j] = 0.f;
-    if ((args.flags & TF_BP_ACCUMULATE) && mine) {
+    for (int v = 0; v < VX * VY; ++v)
 #pragma unroll
-        for (int j = 0; j < ACC; ++j)
-            if (j < nz) acc[j] = args.vol[(size_t)(zb * kZB + j) * plane + (size_t)y * args.nx + x];
+        for (int j = 0; j < ZT; ++j) acc[v][j] = 0.f;
+    if (args.flags & TF_BP_ACCUMULATE) {
+#pragma unroll
+        for (int v = 0; v < VX * VY; ++v) {
+            const int x = X0 + dx0 + (v % VX), y = Y0 + dy0 + (v / VX);
+            if (x >= ux0 && x < ux1 && y >= uy0 && y < uy1) {
+#pragma unroll
+                for (int j = 0; j < ZT; ++j)
+                    if (j < nz) acc[v][j] = args.vol[(size_t)(zrow0 + j) * plane + (size_t)y * args.nx + x];
+            }
+        }
     }
 
     for (int it = 0; it < n_it; ++it) {
@@ -181,39 +212,84 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         const int na = min(APS, n_ang - it * APS);
         for (int a = 0; a < na; ++a) {
             const float4 p = prm[s * APS + a];
-            float t = fmaf(fdy, p.z, fmaf(fdx, p.y, p.x));
-            t = fmaxf(t, 0.f);
-            const float fl = floorf(t);
-            const float f = t - fl;
-            const float w0 = 1.f - f;
-            const float* p0 = reinterpret_cast<const float*>(ring + (s * APS + a) * args.slot_bytes +
-                                                             (int)fl * kRowBytes);
-            const float* p1 = p0 + kZP;
+            const uint8_t* slot = ring + (s * APS + a) * args.slot_bytes + zg * ZT * 4;
+            if constexpr (NT == 2) {
+                float t = fmaf((float)dy0, p.z, fmaf((float)dx0, p.y, p.x));
+                t = fmaxf(t, 0.f);
+                const float fl = floorf(t);
+                const float f = t - fl;
+                const float w0 = 1.f - f;
+                const float* p0 = reinterpret_cast<const float*>(slot + (int)fl * kRowBytes);
+                const float* p1 = p0 + kZP;
 #pragma unroll
-            for (int c = 0; c < ACC / 4; ++c) {
-                const float4 u = *reinterpret_cast<const float4*>(p0 + 4 * c);
-                const float4 v = *reinterpret_cast<const float4*>(p1 + 4 * c);
-                acc[4 * c + 0] = fmaf(v.x, f, fmaf(u.x, w0, acc[4 * c + 0]));
-                acc[4 * c + 1] = fmaf(v.y, f, fmaf(u.y, w0, acc[4 * c + 1]));
-                acc[4 * c + 2] = fmaf(v.z, f, fmaf(u.z, w0, acc[4 * c + 2]));
-                acc[4 * c + 3] = fmaf(v.w, f, fmaf(u.w, w0, acc[4 * c + 3]));
+                for (int c = 0; c < ZT / 4; ++c) {
+                    const float4 u = *reinterpret_cast<const float4*>(p0 + 4 * c);
+                    const float4 v = *reinterpret_cast<const float4*>(p1 + 4 * c);
+                    acc[0][4 * c + 0] = fmaf(v.x, f, fmaf(u.x, w0, acc[0][4 * c + 0]));
+                    acc[0][4 * c + 1] = fmaf(v.y, f, fmaf(u.y, w0, acc[0][4 * c + 1]));
+                    acc[0][4 * c + 2] = fmaf(v.z, f, fmaf(u.z, w0, acc[0][4 * c + 2]));
+                    acc[0][4 * c + 3] = fmaf(v.w, f, fmaf(u.w, w0, acc[0][4 * c + 3]));
+                }
+            } else {
+                float t[VX * VY];
+                float tmin = 3.0e38f;
+#pragma unroll
+                for (int v = 0; v < VX * VY; ++v) {
+                    t[v] = fmaxf(fmaf((float)(dy0 + v / VX), p.z, fmaf((float)(dx0 + v % VX), p.y, p.x)), 0.f);
+                    tmin = fminf(tmin, t[v]);
+                }
+                const float fb = floorf(tmin);
+                float w[VX * VY][NT];
+#pragma unroll
+                for (int v = 0; v < VX * VY; ++v) {
+                    const float u = t[v] - fb;  // exact
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) w[v][j] = __saturatef(1.f - fabsf(u - (float)j));
+                }
+                const float* p0 = reinterpret_cast<const float*>(slot + (int)fb * kRowBytes);
+#pragma unroll
+                for (int c = 0; c < ZT / 4; ++c) {
+                    float4 T[NT];
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) T[j] = *reinterpret_cast<const float4*>(p0 + j * kZP + 4 * c);
+#pragma unroll
+                    for (int v = 0; v < VX * VY; ++v) {
+                        float a0 = acc[v][4 * c + 0], a1 = acc[v][4 * c + 1];
+                        float a2 = acc[v][4 * c + 2], a3 = acc[v][4 * c + 3];
+#pragma unroll
+                        for (int j = 0; j < NT; ++j) {
+                            a0 = fmaf(T[j].x, w[v][j], a0);
+                            a1 = fmaf(T[j].y, w[v][j], a1);
+                            a2 = fmaf(T[j].z, w[v][j], a2);
+                            a3 = fmaf(T[j].w, w[v][j], a3);
+                        }
+                        acc[v][4 * c + 0] = a0;
+                        acc[v][4 * c + 1] = a1;
+                        acc[v][4 * c + 2] = a2;
+                        acc[v][4 * c + 3] = a3;
+                    }
+                }
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
 
-    if (!mine) return;
-    float scale = 1.f;
-    bool zero = false;
-    if (args.flags & TF_BP_FINALIZE) {
-        scale = args.angle_wf;
-        zero = outside_fov(x, y, args);
-    }
-    float* out = args.vol + (size_t)(zb * kZB) * plane + (size_t)y * args.nx + x;
 #pragma unroll
-    for (int j = 0; j < ACC; ++j)
-        if (j < nz) out[(size_t)j * plane] = zero ? 0.f : acc[j] * scale;
+    for (int v = 0; v < VX * VY; ++v) {
+        const int x = X0 + dx0 + (v % VX), y = Y0 + dy0 + (v / VX);
+        if (!(x >= ux0 && x < ux1 && y >= uy0 && y < uy1)) continue;
+        float scale = 1.f;
+        bool zero = false;
+        if (args.flags & TF_BP_FINALIZE) {
+            scale = args.angle_wf;
+            zero = outside_fov(x, y, args);
+        }
+        float* out = args.vol + (size_t)zrow0 * plane + (size_t)y * args.nx + x;
+#pragma unroll
+        for (int j = 0; j < ZT; ++j)
+            if (j < nz) out[(size_t)j * plane] = zero ? 0.f : acc[v][j] * scale;
+    }
 }
 
 // ---- staging: angle-major rows -> z-blocked, feather-weighted ------------
@@ -319,10 +395,9 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     p->g = *g;
     p->feather_band = feather_band;
     p->scale = g->voxel_pitch / g->pixel_pitch;
-    // window: max over angles of the tile's channel extent + 2 taps + floor slack
-    const double ext = std::sqrt((double)(TX - 1) * (TX - 1) + (double)(TY - 1) * (TY - 1)) * p->scale;
-    p->W = (int)std::ceil(ext + 3.0);
-    if (bp_smem_bytes((kRowBytes * p->W + 127) / 128 * 128) > 227 * 1024) {
+    // window: max over angles of the tile's channel extent + taps + floor slack
+    p->ext = std::sqrt((double)(TX - 1) * (TX - 1) + (double)(TY - 1) * (TY - 1)) * p->scale;
+    if (bp_smem_bytes((kRowBytes * (int)std::ceil(p->ext + 3.0) + 127) / 128 * 128) > 227 * 1024) {
         delete p;
         return set_error(TF_ERR_UNSUPPORTED, "voxel/pixel pitch ratio %.3g too large for the tile window",
                          p->scale);
@@ -400,12 +475,17 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     const int nzb = (n_rows + kZB - 1) / kZB;
     if (a0 == a1 && !(flags & TF_BP_FINALIZE)) return TF_OK;
 
+    // kernel variant: the 2x2-block 4-tap gather needs the block's rays to span
+    // < 2 channels (sqrt(2) * voxel/pixel pitch ratio); else the 2-tap kernel
+    const bool v4 = !(flags & TF_BP_KERNEL_V1) && p->scale <= 1.4;
+    const int W = (int)std::ceil(p->ext + (v4 ? 4.0 : 3.0));
+
     PFN_encodeTiled_t enc = encode_fn();
     if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     CUtensorMap map;
     cuuint64_t dims[3] = {(cuuint64_t)kZP, (cuuint64_t)g.n_chan, (cuuint64_t)g.n_proj * (cuuint64_t)nzb};
     cuuint64_t strides[2] = {(cuuint64_t)kRowBytes, (cuuint64_t)kRowBytes * (cuuint64_t)g.n_chan};
-    cuuint32_t box[3] = {(cuuint32_t)kZP, (cuuint32_t)p->W, 1u};
+    cuuint32_t box[3] = {(cuuint32_t)kZP, (cuuint32_t)W, 1u};
     cuuint32_t estr[3] = {1u, 1u, 1u};
     CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(stage), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -427,8 +507,8 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     a.y0 = y0;
     a.y1 = y1;
     a.ntx = (g.nx + TX - 1) / TX;
-    a.W = p->W;
-    a.slot_bytes = ((kRowBytes * p->W) + 127) / 128 * 128;
+    a.W = W;
+    a.slot_bytes = ((kRowBytes * W) + 127) / 128 * 128;
     a.flags = flags;
     a.cx = p->cx;
     a.cy = p->cy;
@@ -438,9 +518,16 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     a.sc2 = p->sc2;
     a.angle_wf = p->angle_wf;
     const int smem = bp_smem_bytes(a.slot_bytes);
-    TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int nty = (g.ny + TY - 1) / TY;
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)nzb);
-    bp_kernel<<<grid, NTHREADS, smem, as_stream(stream)>>>(map, a);
+    if (v4) {
+        using L = Layout<2, 2, 4, 16>;
+        TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<2, 2, 4, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        bp_kernel<2, 2, 4, 16><<<grid, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
+    } else {
+        using L = Layout<1, 1, 2, 32>;
+        TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<1, 1, 2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        bp_kernel<1, 1, 2, 32><<<grid, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
+    }
     return check_launch("bp_kernel");
 }

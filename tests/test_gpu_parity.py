@@ -309,3 +309,36 @@ def test_row_slabs_are_bitwise(F):
         assert (part == full[r0:r1]).all()
     part = SlabReconstructor(p, d, i0=1e5, rows=(5, 6)).run(raw[:, 5:6].contiguous()).cpu()
     assert rel_l2(part.numpy(), full[5:6].numpy()) < 1e-6
+
+
+@pytest.mark.parametrize("case", ["normal", "offset", "pitch", "ragged"])
+def test_block_kernel_bitwise_equals_two_tap_kernel(F, case):
+    """K2's 2x2-block 4-tap gather (default) == the 1-voxel 2-tap kernel, bit
+    for bit: zero-weight taps are exact no-op FMAs."""
+    import torch
+
+    from paper_2505_13955_b200 import _lib
+    from paper_2505_13955_b200.engine import SlabReconstructor
+    from paper_2505_13955_b200.geometry import AcquisitionParams, ScanMode, VolumeDims
+
+    if case == "offset":
+        p = AcquisitionParams(n_proj=64, n_rows=33, n_chan=80, angle_span=2 * math.pi,
+                              scan_mode=ScanMode.OFFSET, offset_chan=13)
+        d = VolumeDims(100, 96, 33)
+    elif case == "pitch":
+        p = AcquisitionParams(n_proj=50, n_rows=32, n_chan=64, pixel_pitch=1.0)
+        d = VolumeDims(70, 70, 32, voxel_pitch=1.3)
+    elif case == "ragged":
+        p = AcquisitionParams(n_proj=37, n_rows=45, n_chan=61)
+        d = VolumeDims(61, 53, 45)
+    else:
+        p = AcquisitionParams(n_proj=90, n_rows=64, n_chan=128)
+        d = VolumeDims(128, 128, 64)
+    eng = SlabReconstructor(p, d, i0=1e5)
+    raw = _phantom_rows(p, d, 0, p.n_rows)
+    filt = eng.filter(raw)
+    eng.stage_rows(filt)
+    v4 = eng.backproject().clone()
+    v1 = eng.backproject(flags=_lib.TF_BP_FINALIZE | _lib.TF_BP_KERNEL_V1).clone()
+    assert torch.equal(v1, v4)
+    assert float(v4.abs().max()) > 0
