@@ -43,7 +43,6 @@ namespace tf {
 namespace {
 
 constexpr int TX = 16, TY = 16;           // voxel columns per CTA tile
-constexpr int STAGES = 3, APS = 4;        // smem ring: 3 stages x 4 angles
 
 // Consumer layouts.  A thread owns a VX x VY block of voxel columns and ZT of
 // the tile's 32 rows.  NT detector taps per block serve all its voxels:
@@ -54,8 +53,12 @@ constexpr int STAGES = 3, APS = 4;        // smem ring: 3 stages x 4 angles
 //       per-voxel weights are tents sat(1 - |u - j|): exactly {1-f, f} on the
 //       two live taps and 0 elsewhere, so the FMA sequence -- and the result
 //       -- is bit-identical to V1.
-template <int VX, int VY, int NT, int ZT>
+template <int VX, int VY, int NT, int ZT, int STAGES_ = 3, int APS_ = 4, bool PIPE_ = false, int MINB_ = 2>
 struct Layout {
+    static constexpr int STAGES = STAGES_, APS = APS_, RING = STAGES_ * APS_;  // smem ring of angle slots
+    static constexpr bool PIPE = PIPE_;  // software-pipeline the next angle's setup under this angle's FMAs
+    static constexpr int MINB = MINB_;
+    static constexpr int VX_ = VX, VY_ = VY, NT_ = NT, ZT_ = ZT;
     static constexpr int BX = TX / VX, BY = TY / VY;   // blocks per tile
     static constexpr int COLS = BX * BY;               // threads per z-group
     static constexpr int ZG = kZB / ZT;                // z-groups
@@ -85,10 +88,14 @@ __device__ __forceinline__ bool outside_fov(int x, int y, const BPArgs& a) {
     return rr > a.R2;
 }
 
-template <int VX, int VY, int NT, int ZT>
-__global__ void __launch_bounds__(Layout<VX, VY, NT, ZT>::NTHREADS, (VX * VY == 1) ? 2 : 3)
+template <class L>
+struct Setup;
+
+template <class L>
+__global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     bp_kernel(const __grid_constant__ CUtensorMap map, const BPArgs args) {
-    using L = Layout<VX, VY, NT, ZT>;
+    constexpr int VX = L::VX_, VY = L::VY_, NT = L::NT_, ZT = L::ZT_;
+    constexpr int STAGES = L::STAGES, APS = L::APS;
     extern __shared__ __align__(128) uint8_t smem[];
     const int tx = blockIdx.x % args.ntx, ty = blockIdx.x / args.ntx, zb = blockIdx.y;
     const int X0 = tx * TX, Y0 = ty * TY;
@@ -205,74 +212,99 @@ __global__ void __launch_bounds__(Layout<VX, VY, NT, ZT>::NTHREADS, (VX * VY == 
         }
     }
 
-    for (int it = 0; it < n_it; ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
-        mbar_wait(&full[s], ph);
-        const int na = min(APS, n_ang - it * APS);
-        for (int a = 0; a < na; ++a) {
-            const float4 p = prm[s * APS + a];
-            const uint8_t* slot = ring + (s * APS + a) * args.slot_bytes + zg * ZT * 4;
-            if constexpr (NT == 2) {
-                float t = fmaf((float)dy0, p.z, fmaf((float)dx0, p.y, p.x));
-                t = fmaxf(t, 0.f);
-                const float fl = floorf(t);
-                const float f = t - fl;
-                const float w0 = 1.f - f;
-                const float* p0 = reinterpret_cast<const float*>(slot + (int)fl * kRowBytes);
-                const float* p1 = p0 + kZP;
+    // per-angle setup: detector coordinates -> tap row + interpolation weights
+    const uint8_t* ring_z = ring + zg * ZT * 4;
+    auto setup = [&](int g, const float*& p0, float (&w)[VX * VY][NT]) {
+        const int slot = g & (L::RING - 1);
+        const float4 p = prm[slot];
+        const uint8_t* base = ring_z + slot * args.slot_bytes;
+        if constexpr (NT == 2) {
+            float t = fmaf((float)dy0, p.z, fmaf((float)dx0, p.y, p.x));
+            t = fmaxf(t, 0.f);
+            const float fl = floorf(t);
+            const float f = t - fl;
+            w[0][0] = 1.f - f;
+            w[0][1] = f;
+            p0 = reinterpret_cast<const float*>(base + (int)fl * kRowBytes);
+        } else {
+            float t[VX * VY];
+            float tmin = 3.0e38f;
 #pragma unroll
-                for (int c = 0; c < ZT / 4; ++c) {
-                    const float4 u = *reinterpret_cast<const float4*>(p0 + 4 * c);
-                    const float4 v = *reinterpret_cast<const float4*>(p1 + 4 * c);
-                    acc[0][4 * c + 0] = fmaf(v.x, f, fmaf(u.x, w0, acc[0][4 * c + 0]));
-                    acc[0][4 * c + 1] = fmaf(v.y, f, fmaf(u.y, w0, acc[0][4 * c + 1]));
-                    acc[0][4 * c + 2] = fmaf(v.z, f, fmaf(u.z, w0, acc[0][4 * c + 2]));
-                    acc[0][4 * c + 3] = fmaf(v.w, f, fmaf(u.w, w0, acc[0][4 * c + 3]));
+            for (int v = 0; v < VX * VY; ++v) {
+                t[v] = fmaxf(fmaf((float)(dy0 + v / VX), p.z, fmaf((float)(dx0 + v % VX), p.y, p.x)), 0.f);
+                tmin = fminf(tmin, t[v]);
+            }
+            const float fb = floorf(tmin);
+#pragma unroll
+            for (int v = 0; v < VX * VY; ++v) {
+                const float u = t[v] - fb;  // exact
+#pragma unroll
+                for (int j = 0; j < NT; ++j) w[v][j] = __saturatef(1.f - fabsf(u - (float)j));
+            }
+            p0 = reinterpret_cast<const float*>(base + (int)fb * kRowBytes);
+        }
+    };
+    auto accumulate = [&](const float* p0, const float (&w)[VX * VY][NT]) {
+#pragma unroll
+        for (int c = 0; c < ZT / 4; ++c) {
+            float4 T[NT];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) T[j] = *reinterpret_cast<const float4*>(p0 + j * kZP + 4 * c);
+#pragma unroll
+            for (int v = 0; v < VX * VY; ++v) {
+                float a0 = acc[v][4 * c + 0], a1 = acc[v][4 * c + 1];
+                float a2 = acc[v][4 * c + 2], a3 = acc[v][4 * c + 3];
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    a0 = fmaf(T[j].x, w[v][j], a0);
+                    a1 = fmaf(T[j].y, w[v][j], a1);
+                    a2 = fmaf(T[j].z, w[v][j], a2);
+                    a3 = fmaf(T[j].w, w[v][j], a3);
                 }
-            } else {
-                float t[VX * VY];
-                float tmin = 3.0e38f;
-#pragma unroll
-                for (int v = 0; v < VX * VY; ++v) {
-                    t[v] = fmaxf(fmaf((float)(dy0 + v / VX), p.z, fmaf((float)(dx0 + v % VX), p.y, p.x)), 0.f);
-                    tmin = fminf(tmin, t[v]);
-                }
-                const float fb = floorf(tmin);
-                float w[VX * VY][NT];
-#pragma unroll
-                for (int v = 0; v < VX * VY; ++v) {
-                    const float u = t[v] - fb;  // exact
-#pragma unroll
-                    for (int j = 0; j < NT; ++j) w[v][j] = __saturatef(1.f - fabsf(u - (float)j));
-                }
-                const float* p0 = reinterpret_cast<const float*>(slot + (int)fb * kRowBytes);
-#pragma unroll
-                for (int c = 0; c < ZT / 4; ++c) {
-                    float4 T[NT];
-#pragma unroll
-                    for (int j = 0; j < NT; ++j) T[j] = *reinterpret_cast<const float4*>(p0 + j * kZP + 4 * c);
-#pragma unroll
-                    for (int v = 0; v < VX * VY; ++v) {
-                        float a0 = acc[v][4 * c + 0], a1 = acc[v][4 * c + 1];
-                        float a2 = acc[v][4 * c + 2], a3 = acc[v][4 * c + 3];
-#pragma unroll
-                        for (int j = 0; j < NT; ++j) {
-                            a0 = fmaf(T[j].x, w[v][j], a0);
-                            a1 = fmaf(T[j].y, w[v][j], a1);
-                            a2 = fmaf(T[j].z, w[v][j], a2);
-                            a3 = fmaf(T[j].w, w[v][j], a3);
-                        }
-                        acc[v][4 * c + 0] = a0;
-                        acc[v][4 * c + 1] = a1;
-                        acc[v][4 * c + 2] = a2;
-                        acc[v][4 * c + 3] = a3;
-                    }
-                }
+                acc[v][4 * c + 0] = a0;
+                acc[v][4 * c + 1] = a1;
+                acc[v][4 * c + 2] = a2;
+                acc[v][4 * c + 3] = a3;
             }
         }
+    };
+    auto wait_full = [&](int g) {  // first angle of a stage
+        const int it = g / APS;
+        mbar_wait(&full[it % STAGES], (uint32_t)(it / STAGES) & 1u);
+    };
+    auto release = [&](int g) {  // last angle of a stage (or of the launch)
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        if (lane == 0) mbar_arrive(&empty[(g / APS) % STAGES]);
+    };
+
+    if constexpr (!L::PIPE) {
+        for (int g = 0; g < n_ang; ++g) {
+            if (g % APS == 0) wait_full(g);
+            const float* p0;
+            float w[VX * VY][NT];
+            setup(g, p0, w);
+            accumulate(p0, w);
+            if (g % APS == APS - 1 || g == n_ang - 1) release(g);
+        }
+    } else if (n_ang > 0) {
+        wait_full(0);
+        const float* p0;
+        float w[VX * VY][NT];
+        setup(0, p0, w);
+        for (int g = 0; g < n_ang; ++g) {
+            const int gn = g + 1;
+            if (gn < n_ang && gn % APS == 0) wait_full(gn);
+            const float* q0;
+            float wn[VX * VY][NT];
+            setup(min(gn, n_ang - 1), q0, wn);  // independent of this angle's FMAs
+            accumulate(p0, w);
+            if (gn % APS == 0 || gn == n_ang) release(g);
+            p0 = q0;
+#pragma unroll
+            for (int v = 0; v < VX * VY; ++v)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) w[v][j] = wn[v][j];
+        }
     }
 
 #pragma unroll
@@ -345,10 +377,39 @@ PFN_encodeTiled_t encode_fn() {
     return fn;
 }
 
+template <class L>
 int bp_smem_bytes(int slot_bytes) {
-    return STAGES * APS * slot_bytes + STAGES * APS * (int)sizeof(float4) + 2 * STAGES * (int)sizeof(uint64_t);
+    return L::RING * slot_bytes + L::RING * (int)sizeof(float4) + 2 * L::STAGES * (int)sizeof(uint64_t);
 }
 
+}  // namespace
+}  // namespace tf
+
+namespace tf {
+namespace {
+// kernel configurations (VX, VY, taps, rows/thread, stages, angles/stage, pipelined setup, min CTAs/SM)
+using V1Cfg = Layout<1, 1, 2, 32, 4, 4, false, 2>;
+using V4Cfg1 = Layout<2, 2, 4, 16, 4, 4, false, 3>;
+using V4Cfg2 = Layout<2, 2, 4, 16, 8, 2, false, 3>;
+using V4Cfg3 = Layout<2, 2, 4, 16, 8, 2, true, 3>;
+using V4Cfg4 = Layout<2, 2, 4, 16, 8, 2, true, 2>;
+
+int default_v4_variant() {
+    static int v = [] {
+        const char* e = getenv("TF_BP_VARIANT");  // benchmarking knob: 1..4
+        int x = e ? atoi(e) : 0;
+        return (x >= 1 && x <= 4) ? x : 2;
+    }();
+    return v;
+}
+
+template <class L>
+int launch_bp(const CUtensorMap& map, const BPArgs& a, dim3 grid, void* stream) {
+    const int smem = bp_smem_bytes<L>(a.slot_bytes);
+    TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    bp_kernel<L><<<grid, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
+    return TF_OK;
+}
 }  // namespace
 }  // namespace tf
 
@@ -397,7 +458,7 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     p->scale = g->voxel_pitch / g->pixel_pitch;
     // window: max over angles of the tile's channel extent + taps + floor slack
     p->ext = std::sqrt((double)(TX - 1) * (TX - 1) + (double)(TY - 1) * (TY - 1)) * p->scale;
-    if (bp_smem_bytes((kRowBytes * (int)std::ceil(p->ext + 3.0) + 127) / 128 * 128) > 227 * 1024) {
+    if (bp_smem_bytes<V1Cfg>((kRowBytes * (int)std::ceil(p->ext + 3.0) + 127) / 128 * 128) > 227 * 1024) {
         delete p;
         return set_error(TF_ERR_UNSUPPORTED, "voxel/pixel pitch ratio %.3g too large for the tile window",
                          p->scale);
@@ -517,17 +578,17 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     a.R2 = p->R2;
     a.sc2 = p->sc2;
     a.angle_wf = p->angle_wf;
-    const int smem = bp_smem_bytes(a.slot_bytes);
     const int nty = (g.ny + TY - 1) / TY;
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)nzb);
-    if (v4) {
-        using L = Layout<2, 2, 4, 16>;
-        TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<2, 2, 4, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        bp_kernel<2, 2, 4, 16><<<grid, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
-    } else {
-        using L = Layout<1, 1, 2, 32>;
-        TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<1, 1, 2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        bp_kernel<1, 1, 2, 32><<<grid, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
+    int variant = v4 ? default_v4_variant() : 0;
+    int st;
+    switch (variant) {
+        case 0: st = launch_bp<V1Cfg>(map, a, grid, stream); break;
+        case 1: st = launch_bp<V4Cfg1>(map, a, grid, stream); break;
+        case 2: st = launch_bp<V4Cfg2>(map, a, grid, stream); break;
+        case 3: st = launch_bp<V4Cfg3>(map, a, grid, stream); break;
+        default: st = launch_bp<V4Cfg4>(map, a, grid, stream); break;
     }
+    if (st) return st;
     return check_launch("bp_kernel");
 }
