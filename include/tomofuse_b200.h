@@ -145,6 +145,14 @@ TF_API int tf_backproject(const tf_bp_plan* plan, const void* stage, int n_rows,
  * bit-identical to numpy for the same input values. */
 TF_API int tf_quantize(const void* vol, int vol_dtype, uint16_t* out, int64_t n, double lo, double hi, void* stream);
 
+/* ---- host <-> device slab streaming --------------------------------------- */
+/* Strided 2-D async copy (cudaMemcpy2DAsync, direction inferred from UVA):
+ * `height` rows of `width_bytes`, with the given pitches.  Used to move one
+ * z-slab of an angle-major host sinogram (n_proj strided chunks) into HBM and
+ * volume slabs back, overlapped with compute on other streams. */
+TF_API int tf_copy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width_bytes,
+                           size_t height, void* stream);
+
 /* ---- synthetic input: analytic 3-D Shepp-Logan raw counts -------------- */
 /* Writes raw counts i0*exp(-p) (fp32) for angles [a0,a1), rows [r0,r1) into
  * out (a1-a0, r1-r0, n_chan).  Attenuation max `mu_max` (1/um). */

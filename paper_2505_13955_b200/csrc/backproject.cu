@@ -53,8 +53,10 @@ constexpr int TX = 16, TY = 16;           // voxel columns per CTA tile
 //       per-voxel weights are tents sat(1 - |u - j|): exactly {1-f, f} on the
 //       two live taps and 0 elsewhere, so the FMA sequence -- and the result
 //       -- is bit-identical to V1.
-template <int VX, int VY, int NT, int ZT, int STAGES_ = 3, int APS_ = 4, bool PIPE_ = false, int MINB_ = 2>
+template <int VX, int VY, int NT, int ZT, int STAGES_ = 3, int APS_ = 4, bool PIPE_ = false, int MINB_ = 2,
+          int PW_ = 4>
 struct Layout {
+    static constexpr int PW = PW_, PH = 8 / PW_;  // one 8-lane LDS.128 phase = PW x PH blocks
     static constexpr int STAGES = STAGES_, APS = APS_, RING = STAGES_ * APS_;  // smem ring of angle slots
     static constexpr bool PIPE = PIPE_;  // software-pipeline the next angle's setup under this angle's FMAs
     static constexpr int MINB = MINB_;
@@ -188,8 +190,9 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     const int zg = threadIdx.x / L::COLS;
     const int wg = (threadIdx.x % L::COLS) >> 5;
     const int q = lane >> 3, i8 = lane & 7;
-    const int bx = (wg % L::WX) * 8 + (q & 1) * 4 + (i8 & 3);
-    const int by = (wg / L::WX) * 4 + (q >> 1) * 2 + (i8 >> 2);
+    constexpr int QW = 8 / L::PW;  // phases across the warp's 8-block width
+    const int bx = (wg % L::WX) * 8 + (q % QW) * L::PW + (i8 % L::PW);
+    const int by = (wg / L::WX) * 4 + (q / QW) * L::PH + (i8 / L::PW);
     const int dx0 = bx * VX, dy0 = by * VY;
     const size_t plane = (size_t)args.nx * args.ny;
     const int zrow0 = zb * kZB + zg * ZT;                 // first volume row of this thread
@@ -226,6 +229,29 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
             w[0][0] = 1.f - f;
             w[0][1] = f;
             p0 = reinterpret_cast<const float*>(base + (int)fl * kRowBytes);
+        } else if constexpr (NT == 3) {
+            // pair of voxels along x: their rays differ by |cos|*scale <= 1
+            // channel, so taps fb..fb+2 cover both.  Weights are the exact
+            // two-tap {1-f, f} of the 2-tap kernel, placed at o = floor(t)-fb.
+            float t[VX * VY];
+            float tmin = 3.0e38f;
+#pragma unroll
+            for (int v = 0; v < VX * VY; ++v) {
+                t[v] = fmaxf(fmaf((float)(dy0 + v / VX), p.z, fmaf((float)(dx0 + v % VX), p.y, p.x)), 0.f);
+                tmin = fminf(tmin, t[v]);
+            }
+            const float fb = floorf(tmin);
+#pragma unroll
+            for (int v = 0; v < VX * VY; ++v) {
+                const float fl = floorf(t[v]);
+                const float f = t[v] - fl;
+                const float g0 = 1.f - f;
+                const bool hi = fl > fb;  // o == 1
+                w[v][0] = hi ? 0.f : g0;
+                w[v][1] = hi ? g0 : f;
+                w[v][2] = hi ? f : 0.f;
+            }
+            p0 = reinterpret_cast<const float*>(base + (int)fb * kRowBytes);
         } else {
             float t[VX * VY];
             float tmin = 3.0e38f;
@@ -393,12 +419,15 @@ using V4Cfg1 = Layout<2, 2, 4, 16, 4, 4, false, 3>;
 using V4Cfg2 = Layout<2, 2, 4, 16, 8, 2, false, 3>;
 using V4Cfg3 = Layout<2, 2, 4, 16, 8, 2, true, 3>;
 using V4Cfg4 = Layout<2, 2, 4, 16, 8, 2, true, 2>;
+using P3Cfg5 = Layout<2, 1, 3, 32, 4, 4, false, 3, 2>;
+using P3Cfg6 = Layout<2, 1, 3, 32, 8, 2, true, 3, 2>;
+using P3Cfg7 = Layout<2, 1, 3, 32, 8, 2, false, 3, 2>;
 
-int default_v4_variant() {
+int default_variant() {
     static int v = [] {
         const char* e = getenv("TF_BP_VARIANT");  // benchmarking knob: 1..4
         int x = e ? atoi(e) : 0;
-        return (x >= 1 && x <= 4) ? x : 2;
+        return (x >= 1 && x <= 7) ? x : 6;
     }();
     return v;
 }
@@ -538,8 +567,10 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
 
     // kernel variant: the 2x2-block 4-tap gather needs the block's rays to span
     // < 2 channels (sqrt(2) * voxel/pixel pitch ratio); else the 2-tap kernel
-    const bool v4 = !(flags & TF_BP_KERNEL_V1) && p->scale <= 1.4;
-    const int W = (int)std::ceil(p->ext + (v4 ? 4.0 : 3.0));
+    int variant = (flags & TF_BP_KERNEL_V1) ? 0 : default_variant();
+    if (variant >= 5 && p->scale > 1.0) variant = 0;  // x-pairs need |cos|*scale <= 1 (3 taps)
+    if (variant >= 1 && p->scale > 1.4) variant = 0;  // 2x2 blocks need sqrt(2)*scale < 2 (4 taps)
+    const int W = (int)std::ceil(p->ext + (variant == 0 ? 3.0 : 4.0));
 
     PFN_encodeTiled_t enc = encode_fn();
     if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
@@ -580,14 +611,16 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     a.angle_wf = p->angle_wf;
     const int nty = (g.ny + TY - 1) / TY;
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)nzb);
-    int variant = v4 ? default_v4_variant() : 0;
     int st;
     switch (variant) {
         case 0: st = launch_bp<V1Cfg>(map, a, grid, stream); break;
         case 1: st = launch_bp<V4Cfg1>(map, a, grid, stream); break;
         case 2: st = launch_bp<V4Cfg2>(map, a, grid, stream); break;
         case 3: st = launch_bp<V4Cfg3>(map, a, grid, stream); break;
-        default: st = launch_bp<V4Cfg4>(map, a, grid, stream); break;
+        case 4: st = launch_bp<V4Cfg4>(map, a, grid, stream); break;
+        case 5: st = launch_bp<P3Cfg5>(map, a, grid, stream); break;
+        case 6: st = launch_bp<P3Cfg6>(map, a, grid, stream); break;
+        default: st = launch_bp<P3Cfg7>(map, a, grid, stream); break;
     }
     if (st) return st;
     return check_launch("bp_kernel");

@@ -187,3 +187,13 @@ extern "C" int tf_phantom_sinogram(const tf_geometry* g, int a0, int a1, int r0,
     phantom_kernel<<<blocks, 256, 0, as_stream(stream)>>>(p);
     return check_launch("phantom_kernel");
 }
+
+extern "C" int tf_copy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width_bytes,
+                               size_t height, void* stream) {
+    if (width_bytes == 0 || height == 0) return TF_OK;
+    if (!dst || !src || dpitch < width_bytes || spitch < width_bytes)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "invalid 2-D copy");
+    TF_CUDA_TRY(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width_bytes, height, cudaMemcpyDefault,
+                                  as_stream(stream)));
+    return TF_OK;
+}

@@ -109,3 +109,104 @@ def phantom_raw(params: AcquisitionParams, dims: VolumeDims, out, a0=0, a1=None,
     check(lib().tf_phantom_sinogram(ctypes.byref(g), a0, a1, r0, r1, float(i0), float(mu_max),
                                     _ptr(out), ctypes.c_void_p(st.cuda_stream)))
     return out
+
+
+class StreamedReconstructor:
+    """Host-fed FBP: pinned host sinogram in, pinned host volume out, with
+    the copies hidden under compute (the reference's four-stage pipeline of
+    pipeline.py:311-349, realised with CUDA streams instead of a model).
+
+    The volume is processed in z-sub-slabs of `slab_rows` rows.  For slab i:
+      h2d stream : strided 2-D copy of rows [r0, r1) of every angle -> raw[i%2]
+      comp stream: K1 filter -> stage -> K2 back-projection -> vol[i%2]
+      d2h stream : vol[i%2] -> host rows [r0, r1)
+    Events order the double-buffered raw/vol buffers, so slab i+1's H2D and
+    slab i-1's D2H overlap slab i's kernels.  HBM use is bounded by the
+    sub-slab size, so this is also the path for volumes larger than HBM.
+    """
+
+    def __init__(self, params: AcquisitionParams, dims: VolumeDims, spec: FilterSpec | None = None,
+                 i0: float = 1e5, feather_band: int = 32, slab_rows: int = 256, device=None):
+        import torch
+
+        self.torch = torch
+        self.params, self.dims = params, dims
+        self.device = torch.device(device if device is not None else "cuda")
+        self.slab_rows = min(slab_rows, params.n_rows)
+        k = self.slab_rows
+        with torch.cuda.device(self.device):
+            self.eng = SlabReconstructor(params, dims, spec, i0, feather_band, rows=(0, k),
+                                         device=self.device)
+            shape = (params.n_proj, k, params.n_chan)
+            self.raw = [torch.empty(shape, dtype=torch.float32, device=self.device) for _ in range(2)]
+            self.vol = [self.eng.vol, torch.empty_like(self.eng.vol)]
+            self.s_h2d = torch.cuda.Stream(self.device)
+            self.s_comp = torch.cuda.Stream(self.device)
+            self.s_d2h = torch.cuda.Stream(self.device)
+
+    def _copy2d(self, dst, dpitch, src, spitch, width, height, stream):
+        check(lib().tf_copy2d_async(ctypes.c_void_p(dst), dpitch, ctypes.c_void_p(src), spitch, width, height,
+                                    ctypes.c_void_p(stream.cuda_stream)))
+
+    def run(self, raw_host, vol_host, row_range=None, host_row0=0):
+        """raw_host: pinned (n_proj, H, n_chan) fp32 counts holding detector
+        rows [host_row0, host_row0 + H); vol_host: pinned (R, ny, nx) fp32
+        receiving volume rows `row_range` = [r0, r1) (default: all rows).
+        Work is queued on this object's streams (ordered after the current
+        stream); returns the last D2H event."""
+        torch = self.torch
+        p, d = self.params, self.dims
+        R0, R1 = row_range if row_range is not None else (0, p.n_rows)
+        n = p.n_chan
+        line = n * 4
+        plane = d.nx * d.ny * 4
+        cur = torch.cuda.current_stream(self.device)
+        for s in (self.s_h2d, self.s_comp, self.s_d2h):
+            s.wait_stream(cur)
+        raw_free = [None, None]
+        vol_free = [None, None]
+        done = None
+        starts = list(range(R0, R1, self.slab_rows))
+        for i, r0 in enumerate(starts):
+            r1 = min(r0 + self.slab_rows, R1)
+            k = r1 - r0
+            b = i % 2
+            # H2D: rows [r0, r1) of every angle (n_proj strided chunks)
+            if raw_free[b] is not None:
+                self.s_h2d.wait_event(raw_free[b])
+            self._copy2d(self.raw[b].data_ptr(), k * line, raw_host.data_ptr() + (r0 - host_row0) * line,
+                         raw_host.shape[1] * line, k * line, p.n_proj, self.s_h2d)
+            h2d_done = torch.cuda.Event()
+            h2d_done.record(self.s_h2d)
+            # compute
+            self.s_comp.wait_event(h2d_done)
+            src = self.raw[b].view(-1)[: p.n_proj * k * n].view(p.n_proj, k, n)
+            self.eng.filter(src, out=self.eng.filt.view(-1)[: p.n_proj * k * n].view(p.n_proj, k, n),
+                            stream=self.s_comp)
+            ev = torch.cuda.Event()
+            ev.record(self.s_comp)
+            raw_free[b] = ev
+            check(lib().tf_bp_stage(self.eng.bplan.handle, _ptr(self.eng.filt), k, 0, k, _ptr(self.eng.stage),
+                                    ctypes.c_void_p(self.s_comp.cuda_stream)))
+            if vol_free[b] is not None:
+                self.s_comp.wait_event(vol_free[b])
+            check(lib().tf_backproject(self.eng.bplan.handle, _ptr(self.eng.stage), k, _ptr(self.vol[b]), 0,
+                                       p.n_proj, 0, d.nx, 0, d.ny, _lib.TF_BP_FINALIZE,
+                                       ctypes.c_void_p(self.s_comp.cuda_stream)))
+            comp_done = torch.cuda.Event()
+            comp_done.record(self.s_comp)
+            # D2H: contiguous volume slab
+            self.s_d2h.wait_event(comp_done)
+            self._copy2d(vol_host.data_ptr() + (r0 - R0) * plane, plane, self.vol[b].data_ptr(), plane, plane, k,
+                         self.s_d2h)
+            ev = torch.cuda.Event()
+            ev.record(self.s_d2h)
+            vol_free[b] = ev
+            done = ev
+        for s in (self.s_h2d, self.s_comp, self.s_d2h):
+            cur.wait_stream(s)
+        return done
+
+    def updates(self, row_range=None) -> int:
+        r0, r1 = row_range if row_range is not None else (0, self.params.n_rows)
+        return self.params.n_proj * (r1 - r0) * self.dims.nx * self.dims.ny
