@@ -327,7 +327,14 @@ def main():
     exec_upd, active_tiles = executed_updates(d, n_proj, k_rows)
     sm_mhz = clk.get("sm_mhz") or 1965.0
     smem_peak = SMEM_BYTES_PER_CLK * SM_COUNT * sm_mhz * 1e6 / 1e9  # GB/s
-    smem_achieved = exec_upd * 8 / (bp_avg_ms / 1e3) / 1e9
+    import ctypes
+
+    from paper_2505_13955_b200._lib import TF_BP_FINALIZE, lib as _tf_lib
+
+    bpu = ctypes.c_double()
+    _tf_lib().tf_bp_smem_bytes_per_update(slab.bplan.handle, TF_BP_FINALIZE, ctypes.byref(bpu))
+    bytes_per_update = bpu.value
+    smem_achieved = exec_upd * bytes_per_update / (bp_avg_ms / 1e3) / 1e9
     fp32_peak_tflops = 128 * 2 * SM_COUNT * sm_mhz * 1e6 / 1e12
     fp32_achieved = exec_upd * 4 / (bp_avg_ms / 1e3) / 1e12
     slab_updates = n_proj * k_rows * n * n
@@ -455,7 +462,10 @@ def main():
             "traffic": None,
             "peak_source": "derived: 128 B/clk/SM x 148 SMs x measured median SM clock "
                            "(shared-memory data path; no tensor-core or HBM bound applies, SURVEY 8d)",
-            "algorithmic_bytes_per_update": 8,
+            "roof_updates_per_s_e9": round(smem_peak / bytes_per_update, 1),
+            "algorithmic_bytes_per_update": bytes_per_update,
+            "bytes_note": "smem bytes the K2 variant gathers per update: 8 = two fp32 taps; 6 = x-pair "
+                          "kernel (3 taps shared by 2 voxels, taps held in registers)",
             "bp_ms_per_launch": round(bp_avg_ms, 3),
             "executed_updates_per_launch": exec_upd,
             "active_tiles": active_tiles,

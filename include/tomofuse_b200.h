@@ -140,6 +140,11 @@ enum {
 TF_API int tf_backproject(const tf_bp_plan* plan, const void* stage, int n_rows, float* vol, int a0, int a1, int x0,
                    int x1, int y0, int y1, int flags, void* stream);
 
+/* Shared-memory bytes the selected K2 variant gathers per voxel x projection
+ * update for these flags (8 = 2-tap, 6 = x-pair 3-tap, 4 = 2x2 4-tap): the
+ * algorithmic numerator of K2's roofline. */
+TF_API int tf_bp_smem_bytes_per_update(const tf_bp_plan* plan, int flags, double* bytes);
+
 /* ---- quantize (fbp.py:255-259) ------------------------------------------ */
 /* vol is fp32 or fp64 (vol_dtype); arithmetic is fp64, round-half-even,
  * bit-identical to numpy for the same input values. */

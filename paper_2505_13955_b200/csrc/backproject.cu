@@ -432,6 +432,13 @@ int default_variant() {
     return v;
 }
 
+int select_variant(const tf_bp_plan* p, int flags) {
+    int variant = (flags & TF_BP_KERNEL_V1) ? 0 : default_variant();
+    if (variant >= 5 && p->scale > 1.0) variant = 0;  // x-pairs need |cos|*scale <= 1 (3 taps)
+    if (variant >= 1 && p->scale > 1.4) variant = 0;  // 2x2 blocks need sqrt(2)*scale < 2 (4 taps)
+    return variant;
+}
+
 template <class L>
 int launch_bp(const CUtensorMap& map, const BPArgs& a, dim3 grid, void* stream) {
     const int smem = bp_smem_bytes<L>(a.slot_bytes);
@@ -567,9 +574,7 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
 
     // kernel variant: the 2x2-block 4-tap gather needs the block's rays to span
     // < 2 channels (sqrt(2) * voxel/pixel pitch ratio); else the 2-tap kernel
-    int variant = (flags & TF_BP_KERNEL_V1) ? 0 : default_variant();
-    if (variant >= 5 && p->scale > 1.0) variant = 0;  // x-pairs need |cos|*scale <= 1 (3 taps)
-    if (variant >= 1 && p->scale > 1.4) variant = 0;  // 2x2 blocks need sqrt(2)*scale < 2 (4 taps)
+    const int variant = select_variant(p, flags);
     const int W = (int)std::ceil(p->ext + (variant == 0 ? 3.0 : 4.0));
 
     PFN_encodeTiled_t enc = encode_fn();
@@ -624,4 +629,11 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     }
     if (st) return st;
     return check_launch("bp_kernel");
+}
+
+extern "C" int tf_bp_smem_bytes_per_update(const tf_bp_plan* p, int flags, double* bytes) {
+    if (!p || !bytes) return set_error(TF_ERR_INVALID_ARGUMENT, "null argument");
+    const int v = select_variant(p, flags);
+    *bytes = v == 0 ? 8.0 : (v >= 5 ? 6.0 : 4.0);
+    return TF_OK;
 }

@@ -372,3 +372,56 @@ def test_streamed_host_path_equals_device_path(F):
     st.run(h_part, out, row_range=(r0, r1), host_row0=r0)
     torch.cuda.synchronize()
     assert torch.equal(out, ref[r0:r1])
+
+
+def test_filter_slab_map_matches_host_restatement(F):
+    """K1's slab-major output mapping (all-to-all send layout) equals the
+    host restatement distributed.slab_major of its natural-layout output."""
+    import ctypes
+
+    import torch
+
+    from paper_2505_13955_b200._lib import check, lib
+    from paper_2505_13955_b200.distributed import exchange_layout, slab_major
+    from paper_2505_13955_b200.engine import SlabReconstructor
+    from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
+
+    p = AcquisitionParams(n_proj=30, n_rows=22, n_chan=40)
+    d = VolumeDims(40, 40, 22)
+    raw = _phantom_rows(p, d, 0, 22)
+    eng = SlabReconstructor(p, d, i0=1e5)
+    world, rank = 3, 1
+    slabs, chunks, row0, base, ins, outs = exchange_layout(world, rank, 30, 22, 40)
+    a0, a1 = chunks[rank]
+    chunk = raw[a0:a1].contiguous()
+    natural = torch.empty_like(chunk)
+    eng.filter(chunk, out=natural)
+    send = torch.empty(chunk.numel(), device="cuda")
+    r0 = (ctypes.c_int32 * len(row0))(*row0)
+    b0 = (ctypes.c_int64 * len(base))(*base)
+    check(lib().tf_filter(eng.fplan.handle, ctypes.c_void_p(chunk.data_ptr()), ctypes.c_void_p(send.data_ptr()),
+                          chunk.numel() // 40, 1e5, 22, world, r0, b0,
+                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    assert torch.equal(send, slab_major(natural, slabs))
+
+
+def test_multi_gpu_zslab_bitwise(F):
+    """torchrun over all visible GPUs (>= 2): the z-slab NCCL path (both
+    exchanges) reproduces the 1-GPU volume bit for bit."""
+    import os
+    import subprocess
+    import sys
+
+    import torch
+
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for mode in ("alltoall", "allgather"):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+               "--master-addr", "127.0.0.1", "--master-port", str(29500 + (mode == "allgather")),
+               os.path.join(root, "tools", "mgpu_check.py"), "--exchange", mode]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+        print(r.stdout[-2000:], r.stderr[-2000:])
+        assert r.returncode == 0 and "MGPU_OK" in r.stdout
