@@ -246,6 +246,7 @@ def main():
 
     from paper_2505_13955_b200.engine import SlabReconstructor, phantom_raw
 
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
