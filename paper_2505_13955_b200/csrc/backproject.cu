@@ -24,6 +24,7 @@
 // Tiles wholly outside the field of view skip the angle loop.
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -54,8 +55,15 @@ constexpr int TX = 16, TY = 16;           // voxel columns per CTA tile
 //       two live taps and 0 elsewhere, so the FMA sequence -- and the result
 //       -- is bit-identical to V1.
 template <int VX, int VY, int NT, int ZT, int STAGES_ = 3, int APS_ = 4, bool PIPE_ = false, int MINB_ = 2,
-          int PW_ = 4>
+          int PW_ = 4, bool ROLE_ = false>
 struct Layout {
+    // ROLE (2x2, 4 taps): per angle the block voxel with the smallest t is
+    // the "base" (its taps are exactly 0,1); its x-, y- and diagonal
+    // neighbours need taps 0..2, 0..2 and 0..3.  Accumulating each voxel only
+    // over its possible taps costs 12 FMA per 4 updates instead of 16, with
+    // exact {1-f, f} weights (bit-identical to the 2-tap kernel).  The voxel
+    // -> role map depends on the signs of cos/sin (warp-uniform per angle).
+    static constexpr bool ROLE = ROLE_;
     static constexpr int PW = PW_, PH = 8 / PW_;  // one 8-lane LDS.128 phase = PW x PH blocks
     static constexpr int STAGES = STAGES_, APS = APS_, RING = STAGES_ * APS_;  // smem ring of angle slots
     static constexpr bool PIPE = PIPE_;  // software-pipeline the next angle's setup under this angle's FMAs
@@ -88,6 +96,37 @@ __device__ __forceinline__ bool outside_fov(int x, int y, const BPArgs& a) {
     double dx = __dsub_rn((double)x, a.cx), dy = __dsub_rn((double)y, a.cy);
     double rr = __dmul_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), a.sc2);
     return rr > a.R2;
+}
+
+// Role-kernel inner loop for one angle: voxel (C ^ r) plays role r and only
+// touches taps 0..ntap(r)-1 (see Layout::ROLE).
+__host__ __device__ constexpr int role_taps(int r) { return r == 0 ? 2 : (r == 3 ? 4 : 3); }
+
+template <int C, int ZT>
+__device__ __forceinline__ void accumulate_roles(float (&acc)[4][ZT], const float* p0, const float (&w)[4][4]) {
+#pragma unroll
+    for (int c = 0; c < ZT / 4; ++c) {
+        float4 T[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) T[j] = *reinterpret_cast<const float4*>(p0 + j * kZP + 4 * c);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int v = C ^ r;
+            float a0 = acc[v][4 * c + 0], a1 = acc[v][4 * c + 1];
+            float a2 = acc[v][4 * c + 2], a3 = acc[v][4 * c + 3];
+#pragma unroll
+            for (int j = 0; j < role_taps(r); ++j) {
+                a0 = fmaf(T[j].x, w[r][j], a0);
+                a1 = fmaf(T[j].y, w[r][j], a1);
+                a2 = fmaf(T[j].z, w[r][j], a2);
+                a3 = fmaf(T[j].w, w[r][j], a3);
+            }
+            acc[v][4 * c + 0] = a0;
+            acc[v][4 * c + 1] = a1;
+            acc[v][4 * c + 2] = a2;
+            acc[v][4 * c + 3] = a3;
+        }
+    }
 }
 
 template <class L>
@@ -217,11 +256,34 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
 
     // per-angle setup: detector coordinates -> tap row + interpolation weights
     const uint8_t* ring_z = ring + zg * ZT * 4;
-    auto setup = [&](int g, const float*& p0, float (&w)[VX * VY][NT]) {
+    auto setup = [&](int g, const float*& p0, float (&w)[VX * VY][NT], int& cls) {
         const int slot = g & (L::RING - 1);
         const float4 p = prm[slot];
         const uint8_t* base = ring_z + slot * args.slot_bytes;
-        if constexpr (NT == 2) {
+        cls = 0;
+        if constexpr (L::ROLE) {
+            static_assert(VX == 2 && VY == 2 && NT == 4, "role kernel is 2x2 x 4 taps");
+            cls = (p.y < 0.f ? 1 : 0) | (p.z < 0.f ? 2 : 0);  // base voxel index = cls, role r voxel = cls ^ r
+            float t[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int v = cls ^ r;
+                t[r] = fmaxf(fmaf((float)(dy0 + (v >> 1)), p.z, fmaf((float)(dx0 + (v & 1)), p.y, p.x)), 0.f);
+            }
+            const float fb = floorf(t[0]);  // the base voxel has the smallest t (monotone rounding)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const float fl = floorf(t[r]);
+                const float f = t[r] - fl;
+                const float g0 = 1.f - f;
+                const float o = fl - fb;  // 0 (base), 0..1 (x / y neighbour), 0..2 (diagonal)
+                w[r][0] = o == 0.f ? g0 : 0.f;
+                w[r][1] = o == 0.f ? f : (o == 1.f ? g0 : 0.f);
+                w[r][2] = o == 1.f ? f : (o == 2.f ? g0 : 0.f);
+                w[r][3] = o == 2.f ? f : 0.f;
+            }
+            p0 = reinterpret_cast<const float*>(base + (int)fb * kRowBytes);
+        } else if constexpr (NT == 2) {
             float t = fmaf((float)dy0, p.z, fmaf((float)dx0, p.y, p.x));
             t = fmaxf(t, 0.f);
             const float fl = floorf(t);
@@ -270,7 +332,16 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
             p0 = reinterpret_cast<const float*>(base + (int)fb * kRowBytes);
         }
     };
-    auto accumulate = [&](const float* p0, const float (&w)[VX * VY][NT]) {
+    auto accumulate = [&](const float* p0, const float (&w)[VX * VY][NT], int cls) {
+        if constexpr (L::ROLE) {
+            switch (cls) {  // warp-uniform: depends on the angle only
+                case 0: accumulate_roles<0, ZT>(acc, p0, w); break;
+                case 1: accumulate_roles<1, ZT>(acc, p0, w); break;
+                case 2: accumulate_roles<2, ZT>(acc, p0, w); break;
+                default: accumulate_roles<3, ZT>(acc, p0, w); break;
+            }
+            return;
+        }
 #pragma unroll
         for (int c = 0; c < ZT / 4; ++c) {
             float4 T[NT];
@@ -308,24 +379,28 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
             if (g % APS == 0) wait_full(g);
             const float* p0;
             float w[VX * VY][NT];
-            setup(g, p0, w);
-            accumulate(p0, w);
+            int cls;
+            setup(g, p0, w, cls);
+            accumulate(p0, w, cls);
             if (g % APS == APS - 1 || g == n_ang - 1) release(g);
         }
     } else if (n_ang > 0) {
         wait_full(0);
         const float* p0;
         float w[VX * VY][NT];
-        setup(0, p0, w);
+        int cls;
+        setup(0, p0, w, cls);
         for (int g = 0; g < n_ang; ++g) {
             const int gn = g + 1;
             if (gn < n_ang && gn % APS == 0) wait_full(gn);
             const float* q0;
             float wn[VX * VY][NT];
-            setup(min(gn, n_ang - 1), q0, wn);  // independent of this angle's FMAs
-            accumulate(p0, w);
+            int clsn;
+            setup(min(gn, n_ang - 1), q0, wn, clsn);  // independent of this angle's FMAs
+            accumulate(p0, w, cls);
             if (gn % APS == 0 || gn == n_ang) release(g);
             p0 = q0;
+            cls = clsn;
 #pragma unroll
             for (int v = 0; v < VX * VY; ++v)
 #pragma unroll
@@ -422,19 +497,21 @@ using V4Cfg4 = Layout<2, 2, 4, 16, 8, 2, true, 2>;
 using P3Cfg5 = Layout<2, 1, 3, 32, 4, 4, false, 3, 2>;
 using P3Cfg6 = Layout<2, 1, 3, 32, 8, 2, true, 3, 2>;
 using P3Cfg7 = Layout<2, 1, 3, 32, 8, 2, false, 3, 2>;
+using Q4Cfg8 = Layout<2, 2, 4, 16, 8, 2, true, 3, 2, true>;
+using Q4Cfg9 = Layout<2, 2, 4, 16, 8, 2, false, 3, 2, true>;
 
 int default_variant() {
     static int v = [] {
         const char* e = getenv("TF_BP_VARIANT");  // benchmarking knob: 1..4
         int x = e ? atoi(e) : 0;
-        return (x >= 1 && x <= 7) ? x : 6;
+        return (x >= 1 && x <= 9) ? x : 6;
     }();
     return v;
 }
 
 int select_variant(const tf_bp_plan* p, int flags) {
     int variant = (flags & TF_BP_KERNEL_V1) ? 0 : default_variant();
-    if (variant >= 5 && p->scale > 1.0) variant = 0;  // x-pairs need |cos|*scale <= 1 (3 taps)
+    if (variant >= 5 && variant <= 7 && p->scale > 1.0) variant = 0;  // x-pairs need |cos|*scale <= 1 (3 taps)
     if (variant >= 1 && p->scale > 1.4) variant = 0;  // 2x2 blocks need sqrt(2)*scale < 2 (4 taps)
     return variant;
 }
@@ -625,7 +702,9 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
         case 4: st = launch_bp<V4Cfg4>(map, a, grid, stream); break;
         case 5: st = launch_bp<P3Cfg5>(map, a, grid, stream); break;
         case 6: st = launch_bp<P3Cfg6>(map, a, grid, stream); break;
-        default: st = launch_bp<P3Cfg7>(map, a, grid, stream); break;
+        case 7: st = launch_bp<P3Cfg7>(map, a, grid, stream); break;
+        case 8: st = launch_bp<Q4Cfg8>(map, a, grid, stream); break;
+        default: st = launch_bp<Q4Cfg9>(map, a, grid, stream); break;
     }
     if (st) return st;
     return check_launch("bp_kernel");
@@ -634,6 +713,6 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
 extern "C" int tf_bp_smem_bytes_per_update(const tf_bp_plan* p, int flags, double* bytes) {
     if (!p || !bytes) return set_error(TF_ERR_INVALID_ARGUMENT, "null argument");
     const int v = select_variant(p, flags);
-    *bytes = v == 0 ? 8.0 : (v >= 5 ? 6.0 : 4.0);
+    *bytes = v == 0 ? 8.0 : ((v >= 5 && v <= 7) ? 6.0 : 4.0);
     return TF_OK;
 }
