@@ -282,8 +282,7 @@ def main():
         k_rows = n
 
         def step_parts():
-            eng.filter(raw)
-            eng.stage_rows(eng.filt)
+            eng.filter_stage(raw)  # K1 fused: Beer-Lambert + ramp + feather -> z-blocked staging
             bp_ev[0].record()
             eng.backproject()
             bp_ev[1].record()
@@ -452,7 +451,8 @@ def main():
                    "parallelism": f"z-slab x{world}" + (f" ({args.exchange} exchange)" if world > 1 else ""),
                    "l2": "inputs larger than L2 (raw %.1f GB, volume %.1f GB per step)" % (
                        raw.numel() * 4 / 1e9, slab.vol.numel() * 4 / 1e9),
-                   "step": "K1 filter (+Beer-Lambert) -> [exchange] -> stage -> K2 back-project"},
+                   "step": ("K1 Beer-Lambert+ramp+feather -> z-blocked staging -> [NCCL row-slab all-to-all "
+                            "landing in the owner's staging buffer] -> K2 back-projection")},
         "roofline": {
             "bound": "smem",
             "kernel": "bp_kernel (K2)",
@@ -478,7 +478,7 @@ def main():
             "hbm_peak_measured": peaks.get("hbm_gbs"),
         },
         "clocks": clk,
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": (3 if (world > 1 and args.exchange == "allgather") else 2) * args.steps,
     }
     if e2e is not None:
         line["e2e"] = e2e

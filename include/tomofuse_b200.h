@@ -104,6 +104,18 @@ TF_API int tf_filter(const tf_filter_plan* plan, const float* in, float* out, in
               int rows_per_angle, int n_slabs, const int32_t* slab_row0, const int64_t* slab_base,
               void* stream);
 
+/* Same filter, written straight into K2's z-blocked staging layout (the
+ * layout tf_bp_stage produces, feather weights of `bp` applied) -- the fused
+ * reconstruction path, no intermediate filtered sinogram.  Lines are
+ * (angle, row) of an angle-major block of `rows_per_angle` rows.  With
+ * n_slabs > 0 the rows are split into slabs [slab_row0[s], slab_row0[s+1])
+ * each staged as its own z-blocked array starting at element slab_base[s]
+ * (the row-slab all-to-all send layout: it lands on the owner as its staging
+ * buffer); n_slabs == 0 stages all rows as one slab at `stage`. */
+TF_API int tf_filter_stage(const tf_filter_plan* plan, const tf_bp_plan* bp, const float* in, void* stage,
+                           int64_t n_lines, float i0, int rows_per_angle, int n_slabs, const int32_t* slab_row0,
+                           const int64_t* slab_base, void* stream);
+
 /* Beer-Lambert only (fbp.py:75-83): fp32 or fp64 counts -> fp64 depth
  * (the reference's output dtype), computed in fp64. */
 TF_API int tf_preprocess(const void* raw, int raw_dtype, double* out, int64_t n, double i0, void* stream);

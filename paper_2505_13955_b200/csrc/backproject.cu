@@ -528,6 +528,11 @@ int launch_bp(const CUtensorMap& map, const BPArgs& a, dim3 grid, void* stream) 
 
 using namespace tf;
 
+namespace tf {
+const float* bp_plan_weights(const tf_bp_plan* p) { return p->g.scan_mode ? p->d_w : nullptr; }
+int bp_plan_n_chan(const tf_bp_plan* p) { return p->g.n_chan; }
+}  // namespace tf
+
 extern "C" int tf_offset_weights(const tf_geometry* g, int band, double* w) {
     if (!g || !w) return set_error(TF_ERR_INVALID_ARGUMENT, "null argument");
     const int n = g->n_chan;

@@ -27,6 +27,10 @@ struct tf_filter_plan {
     float2* d_tw;      // exp(-2 pi i m / P), m in [0, P)
     float* d_mult;     // multiplier / P, m in [0, P/2]
     float* d_blur;     // 2*radius+1 Gaussian weights (or null)
+    bool smem_tw;      // twiddles staged in shared memory (P <= 8192)
+    int smem;          // dynamic shared memory per CTA
+    int max_grid;      // persistent grid: resident CTAs per SM x SMs
+    const void* kernel;  // ramp_filter_kernel instantiation for this P
 };
 
 namespace tf {
@@ -141,23 +145,24 @@ __device__ __forceinline__ void dft(float2 (&v)[R]) {
     }
 }
 
-// One Stockham pass of radix R over a padded smem line of length P.
-template <int R>
-__device__ __forceinline__ void stockham_pass(float2* buf, const float2* __restrict__ tw, int P, int Ns, int tid,
-                                              int T) {
-    constexpr int MAXB = 16 / R;  // butterflies per thread held across the sync (P <= 16*T)
-    float2 v[MAXB][R];
+// One Stockham pass of radix R over a padded smem line of length P; each
+// thread holds NB radix-R butterflies in registers across the sync.
+// Twiddles come from `tw` (exp(-2 pi i m / P), m in [0, P)), staged in
+// shared memory for P <= 8192, else read from global.
+template <int R, int NB>
+__device__ __forceinline__ void stockham_pass(float2* buf, const float2* tw, int P, int Ns, int tid, int T) {
+    float2 v[NB][R];
     const int nb = P / R;
     const int stride = P / (Ns * R);
 #pragma unroll
-    for (int b = 0; b < MAXB; ++b) {
-        int j = tid + b * T;
+    for (int b = 0; b < NB; ++b) {
+        const int j = tid + b * T;
         if (j < nb) {
-            int k = j & (Ns - 1);
+            const int k = j & (Ns - 1);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 float2 x = buf[pad_idx(j + r * nb)];
-                if (r > 0 && Ns > 1) x = cmul(x, __ldg(&tw[k * r * stride]));
+                if (r > 0 && Ns > 1) x = cmul(x, tw[k * r * stride]);
                 v[b][r] = x;
             }
             dft<R>(v[b]);
@@ -165,11 +170,11 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* __restr
     }
     __syncthreads();
 #pragma unroll
-    for (int b = 0; b < MAXB; ++b) {
-        int j = tid + b * T;
+    for (int b = 0; b < NB; ++b) {
+        const int j = tid + b * T;
         if (j < nb) {
-            int k = j & (Ns - 1);
-            int base = (j - k) * R + k;
+            const int k = j & (Ns - 1);
+            const int base = (j - k) * R + k;
 #pragma unroll
             for (int r = 0; r < R; ++r) buf[pad_idx(base + r * Ns)] = v[b][r];
         }
@@ -177,104 +182,163 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* __restr
     __syncthreads();
 }
 
-__device__ void fft_forward(float2* buf, const float2* __restrict__ tw, int P, int log2P, int tid, int T) {
+// Radix-8 passes (T >= P / (8 * NB8) threads) plus one radix-4/2 pass.
+template <int NB8>
+__device__ __forceinline__ void fft_forward(float2* buf, const float2* tw, int P, int log2P, int tid, int T) {
     int Ns = 1, rem = log2P;
-    while (rem >= 4) {
-        stockham_pass<16>(buf, tw, P, Ns, tid, T);
-        Ns <<= 4;
-        rem -= 4;
+    while (rem >= 3) {
+        stockham_pass<8, NB8>(buf, tw, P, Ns, tid, T);
+        Ns <<= 3;
+        rem -= 3;
     }
-    if (rem == 3) stockham_pass<8>(buf, tw, P, Ns, tid, T);
-    else if (rem == 2) stockham_pass<4>(buf, tw, P, Ns, tid, T);
-    else if (rem == 1) stockham_pass<2>(buf, tw, P, Ns, tid, T);
+    if (rem == 2) stockham_pass<4, 2 * NB8>(buf, tw, P, Ns, tid, T);
+    else if (rem == 1) stockham_pass<2, 4 * NB8>(buf, tw, P, Ns, tid, T);
 }
 
-struct SlabMap {
-    int n_slabs;
+// Where filtered line l = (angle a, row r) goes (tf_filter's slab map and
+// output layout, see include/tomofuse_b200.h).
+struct OutMap {
+    int zblocked;        // 0: [a][r][c] rows; 1: z-blocked staging [a][zb][c][36] (K2 input)
+    int n_slabs;         // >= 1 (1 slab == whole row range)
     int rows_per_angle;
     int32_t row0[9];
-    long long base[8];
+    long long base[8];   // element offset of each slab's block
+    const float* w;      // per-channel feather (z-blocked output only), may be null
 };
 
-__device__ __forceinline__ long long line_offset(long long l, int n, const SlabMap& m) {
-    if (m.n_slabs == 0) return l * n;
-    long long a = l / m.rows_per_angle;
-    int r = (int)(l - a * m.rows_per_angle);
+// row0/base are read from a shared-memory copy (dynamic indexing of a
+// kernel-parameter array would spill the struct to local memory)
+__device__ __forceinline__ long long out_offset(long long l, int n, const OutMap& m, const int32_t* row0,
+                                                const long long* base, int& zi) {
+    const long long a = l / m.rows_per_angle;
+    const int r = (int)(l - a * m.rows_per_angle);
     int s = 0;
 #pragma unroll 1
-    while (s + 1 < m.n_slabs && r >= m.row0[s + 1]) ++s;
-    int rs = m.row0[s + 1] - m.row0[s];
-    return m.base[s] + (a * rs + (r - m.row0[s])) * (long long)n;
+    while (s + 1 < m.n_slabs && r >= row0[s + 1]) ++s;
+    const int rl = r - row0[s];
+    const int ks = row0[s + 1] - row0[s];
+    if (!m.zblocked) {
+        zi = 0;
+        return base[s] + (a * ks + rl) * (long long)n;
+    }
+    const int nzb = (ks + kZB - 1) / kZB;
+    zi = rl % kZB;
+    return base[s] + ((a * nzb + rl / kZB) * (long long)n) * kZP + zi;
 }
 
+// Persistent: each CTA loops over line pairs; the twiddle table is loaded
+// into shared memory once per CTA.
+template <bool SMEM_TW, int NB8>
 __global__ void __launch_bounds__(1024) ramp_filter_kernel(const float* __restrict__ in, float* out,
                                                            long long n_lines, int n, int P, int log2P,
-                                                           const float2* __restrict__ tw,
+                                                           const float2* __restrict__ tw_g,
                                                            const float* __restrict__ mult,
                                                            const float* __restrict__ blur, int radius,
-                                                           float i0, SlabMap map) {
+                                                           float i0, OutMap map) {
     extern __shared__ float2 sbuf[];
+    __shared__ int32_t s_row0[9];
+    __shared__ long long s_base[8];
     const int tid = threadIdx.x, T = blockDim.x;
-    const long long la = 2 * (long long)blockIdx.x;
-    const bool has_b = la + 1 < n_lines;
-    const float* pa = in + la * n;
-    const float* pb = in + (la + 1) * n;
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < 9; ++s) s_row0[s] = map.row0[s];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) s_base[s] = map.base[s];
+    }
+    const float2* tw = tw_g;
+    float2* data = sbuf;
+    if constexpr (SMEM_TW) {
+        float2* tws = sbuf + (P + P / 16);
+        for (int m = tid; m < P; m += T) tws[m] = tw_g[m];
+        tw = tws;  // visible after the first __syncthreads below
+    }
+    const long long n_pairs = (n_lines + 1) / 2;
     const bool log_in = i0 > 0.f;
-
-    // load (+ Beer-Lambert) the two lines as one complex line, zero-padded
-    for (int m = tid; m < P; m += T) {
-        float2 z = make_float2(0.f, 0.f);
-        if (m < n) {
-            float a = pa[m];
-            float b = has_b ? pb[m] : 0.f;
-            if (log_in) {  // -ln(max(raw, 1) / i0), fbp.py:80-83
-                a = -logf(__fdiv_rn(fmaxf(a, 1.f), i0));
-                b = has_b ? -logf(__fdiv_rn(fmaxf(b, 1.f), i0)) : 0.f;
+    for (long long pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+        const long long la = 2 * pair;
+        const bool has_b = la + 1 < n_lines;
+        const float* pa = in + la * n;
+        const float* pb = pa + n;
+        // load (+ Beer-Lambert) the two lines as one complex line, zero-padded
+        for (int m = tid; m < P; m += T) {
+            float2 z = make_float2(0.f, 0.f);
+            if (m < n) {
+                float a = __ldcs(pa + m);
+                float b = has_b ? __ldcs(pb + m) : 0.f;
+                if (log_in) {  // -ln(max(raw, 1) / i0), fbp.py:80-83
+                    a = -logf(__fdiv_rn(fmaxf(a, 1.f), i0));
+                    b = has_b ? -logf(__fdiv_rn(fmaxf(b, 1.f), i0)) : 0.f;
+                }
+                z = make_float2(a, b);
             }
-            z = make_float2(a, b);
-        }
-        sbuf[pad_idx(m)] = z;
-    }
-    __syncthreads();
-
-    if (radius > 0) {  // scipy gaussian_filter1d(mode="nearest") restated (fbp.py:125-126)
-        float2 acc[16];
-        int cnt = 0;
-        for (int m = tid; m < n; m += T, ++cnt) {
-            float2 s = make_float2(0.f, 0.f);
-            for (int j = -radius; j <= radius; ++j) {
-                int c = min(max(m + j, 0), n - 1);
-                float wj = __ldg(&blur[j + radius]);
-                float2 x = sbuf[pad_idx(c)];
-                s.x = fmaf(wj, x.x, s.x);
-                s.y = fmaf(wj, x.y, s.y);
-            }
-            acc[cnt] = s;
+            data[pad_idx(m)] = z;
         }
         __syncthreads();
-        cnt = 0;
-        for (int m = tid; m < n; m += T, ++cnt) sbuf[pad_idx(m)] = acc[cnt];
+
+        if (radius > 0) {  // scipy gaussian_filter1d(mode="nearest") restated (fbp.py:125-126)
+            float2 acc[4 * NB8];  // n <= P/2 <= 4*NB8*T
+#pragma unroll
+            for (int q = 0; q < 4 * NB8; ++q) {
+                const int m = tid + q * T;
+                float2 s = make_float2(0.f, 0.f);
+                if (m < n) {
+                    for (int j = -radius; j <= radius; ++j) {
+                        const int c = min(max(m + j, 0), n - 1);
+                        const float wj = __ldg(&blur[j + radius]);
+                        const float2 x = data[pad_idx(c)];
+                        s.x = fmaf(wj, x.x, s.x);
+                        s.y = fmaf(wj, x.y, s.y);
+                    }
+                }
+                acc[q] = s;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 4 * NB8; ++q) {
+                const int m = tid + q * T;
+                if (m < n) data[pad_idx(m)] = acc[q];
+            }
+            __syncthreads();
+        }
+
+        fft_forward<NB8>(data, tw, P, log2P, tid, T);
+
+        // X <- conj(X * M / P): the inverse transform is conj(FFT(conj(.)))
+        for (int m = tid; m < P; m += T) {
+            const float g = __ldg(&mult[m <= P / 2 ? m : P - m]);
+            const float2 x = data[pad_idx(m)];
+            data[pad_idx(m)] = make_float2(x.x * g, -x.y * g);
+        }
         __syncthreads();
-    }
 
-    fft_forward(sbuf, tw, P, log2P, tid, T);
+        fft_forward<NB8>(data, tw, P, log2P, tid, T);
 
-    // X <- conj(X * M / P): the inverse transform is conj(FFT(conj(.)))
-    for (int m = tid; m < P; m += T) {
-        float g = __ldg(&mult[m <= P / 2 ? m : P - m]);
-        float2 x = sbuf[pad_idx(m)];
-        sbuf[pad_idx(m)] = make_float2(x.x * g, -x.y * g);
-    }
-    __syncthreads();
-
-    fft_forward(sbuf, tw, P, log2P, tid, T);
-
-    float* oa = out + line_offset(la, n, map);
-    float* ob = has_b ? out + line_offset(la + 1, n, map) : nullptr;
-    for (int m = tid; m < n; m += T) {
-        float2 y = sbuf[pad_idx(m)];
-        oa[m] = y.x;
-        if (has_b) ob[m] = -y.y;
+        int za, zb = 0;
+        float* oa = out + out_offset(la, n, map, s_row0, s_base, za);
+        float* ob = has_b ? out + out_offset(la + 1, n, map, s_row0, s_base, zb) : nullptr;
+        if (!map.zblocked) {
+            for (int m = tid; m < n; m += T) {
+                const float2 y = data[pad_idx(m)];
+                __stcs(oa + m, y.x);
+                if (has_b) __stcs(ob + m, -y.y);
+            }
+        } else {
+            // both rows in one 8-B store when they are z-neighbours of the same block
+            const bool pairwise = has_b && (ob == oa + 1) && ((za & 1) == 0);
+            for (int m = tid; m < n; m += T) {
+                const float2 y = data[pad_idx(m)];
+                const float wm = map.w ? __ldg(&map.w[m]) : 1.f;
+                // feather applied after the filter, as fbp.py:242 does (f32 product)
+                const float va = y.x * wm, vb = -y.y * wm;
+                if (pairwise) {
+                    *reinterpret_cast<float2*>(oa + (size_t)m * kZP) = make_float2(va, vb);
+                } else {
+                    oa[(size_t)m * kZP] = va;
+                    if (has_b) ob[(size_t)m * kZP] = vb;
+                }
+            }
+        }
+        __syncthreads();  // data[] is reused by the next pair
     }
 }
 
@@ -322,7 +386,7 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
     p->n = n_chan;
     p->P = P;
     p->log2P = ilog2(P);
-    p->threads = std::max(32, std::min(1024, P / 16));
+    p->threads = std::max(32, std::min(1024, P / 8));  // one radix-8 butterfly per thread (2 at P = 16384)
     // twiddles in fp64, rounded once
     std::vector<float2> tw(P);
     for (int m = 0; m < P; ++m) {
@@ -345,10 +409,6 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
         }
         bw.resize(2 * rad + 1);
         for (int j = 0; j <= 2 * rad; ++j) bw[j] = (float)(w[j] / sum);
-        if (n_chan > 16 * p->threads) {
-            delete p;
-            return set_error(TF_ERR_UNSUPPORTED, "blur path supports n_chan <= 16*threads");
-        }
     }
     p->blur_radius = rad;
     cudaError_t e = cudaMalloc(&p->d_tw, sizeof(float2) * P);
@@ -359,9 +419,19 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
         e = cudaMemcpy(p->d_mult, multf.data(), sizeof(float) * (P / 2 + 1), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && rad > 0)
         e = cudaMemcpy(p->d_blur, bw.data(), sizeof(float) * (2 * rad + 1), cudaMemcpyHostToDevice);
+    p->smem_tw = P <= 8192;  // twiddle table in shared memory next to the line buffer
+    p->smem = (P + P / 16 + (p->smem_tw ? P : 0)) * (int)sizeof(float2);
+    p->kernel = P <= 8192 ? (p->smem_tw ? (const void*)ramp_filter_kernel<true, 1>
+                                        : (const void*)ramp_filter_kernel<false, 1>)
+                          : (const void*)ramp_filter_kernel<false, 2>;
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(p->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem);
     if (e == cudaSuccess) {
-        int smem = (P + P / 16) * (int)sizeof(float2);
-        e = cudaFuncSetAttribute(ramp_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int blocks = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, p->kernel, p->threads, p->smem);
+        int dev = 0, sms = 148;
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        p->max_grid = std::max(1, blocks) * sms;
     }
     if (e != cudaSuccess) {
         tf_filter_plan_destroy(p);
@@ -380,6 +450,49 @@ extern "C" int tf_filter_plan_destroy(tf_filter_plan* p) {
     return TF_OK;
 }
 
+namespace tf {
+namespace {
+int build_map(OutMap& map, int64_t n_lines, int rows_per_angle, int n_slabs, const int32_t* slab_row0,
+              const int64_t* slab_base) {
+    map.n_slabs = n_slabs > 0 ? n_slabs : 1;
+    map.rows_per_angle = rows_per_angle > 0 ? rows_per_angle : (int)std::min<int64_t>(n_lines, 1 << 30);
+    if (n_slabs > 0) {
+        if (n_slabs > 8 || rows_per_angle < 1 || !slab_row0 || !slab_base)
+            return set_error(TF_ERR_INVALID_ARGUMENT, "invalid slab map");
+        for (int s = 0; s <= n_slabs; ++s) map.row0[s] = slab_row0[s];
+        for (int s = 0; s < n_slabs; ++s) map.base[s] = slab_base[s];
+        if (map.row0[0] != 0 || map.row0[n_slabs] != rows_per_angle)
+            return set_error(TF_ERR_INVALID_ARGUMENT, "slab rows must cover [0, rows_per_angle)");
+        for (int s = 0; s < n_slabs; ++s)
+            if (map.row0[s + 1] < map.row0[s]) return set_error(TF_ERR_INVALID_ARGUMENT, "slab rows must ascend");
+    } else {
+        map.row0[0] = 0;
+        map.row0[1] = map.rows_per_angle;
+        map.base[0] = 0;
+    }
+    if (rows_per_angle > 0 && n_lines % rows_per_angle != 0)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "n_lines must be a multiple of rows_per_angle");
+    return TF_OK;
+}
+
+int launch_filter(const tf_filter_plan* p, const float* in, float* out, int64_t n_lines, float i0,
+                  const OutMap& map, void* stream) {
+    const long long pairs = (n_lines + 1) / 2;
+    const unsigned grid = (unsigned)std::min<long long>(pairs, p->max_grid);
+    long long nl = n_lines;
+    int n = p->n, P = p->P, l2 = p->log2P, rad = p->blur_radius;
+    const float2* tw = p->d_tw;
+    const float* mult = p->d_mult;
+    const float* blur = p->d_blur;
+    OutMap m = map;
+    void* args[] = {(void*)&in, (void*)&out, &nl, &n, &P, &l2, (void*)&tw, (void*)&mult, (void*)&blur, &rad,
+                    &i0, &m};
+    TF_CUDA_TRY(cudaLaunchKernel(p->kernel, dim3(grid), dim3(p->threads), args, p->smem, as_stream(stream)));
+    return TF_OK;
+}
+}  // namespace
+}  // namespace tf
+
 extern "C" int tf_filter(const tf_filter_plan* p, const float* in, float* out, int64_t n_lines, float i0,
                          int rows_per_angle, int n_slabs, const int32_t* slab_row0, const int64_t* slab_base,
                          void* stream) {
@@ -387,22 +500,29 @@ extern "C" int tf_filter(const tf_filter_plan* p, const float* in, float* out, i
     if (n_lines < 0) return set_error(TF_ERR_INVALID_ARGUMENT, "n_lines must be >= 0");
     if (n_lines == 0) return TF_OK;
     if (!in || !out) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
-    SlabMap map{};
-    map.n_slabs = n_slabs;
-    map.rows_per_angle = rows_per_angle;
-    if (n_slabs > 0) {
-        if (n_slabs > 8 || rows_per_angle < 1 || !slab_row0 || !slab_base || in == out)
-            return set_error(TF_ERR_INVALID_ARGUMENT, "invalid slab map");
-        for (int s = 0; s <= n_slabs; ++s) map.row0[s] = slab_row0[s];
-        for (int s = 0; s < n_slabs; ++s) map.base[s] = slab_base[s];
-        if (map.row0[0] != 0 || map.row0[n_slabs] != rows_per_angle)
-            return set_error(TF_ERR_INVALID_ARGUMENT, "slab rows must cover [0, rows_per_angle)");
-    }
-    long long pairs = (n_lines + 1) / 2;
-    int smem = (p->P + p->P / 16) * (int)sizeof(float2);
-    ramp_filter_kernel<<<(unsigned)pairs, p->threads, smem, as_stream(stream)>>>(
-        in, out, n_lines, p->n, p->P, p->log2P, p->d_tw, p->d_mult, p->d_blur, p->blur_radius, i0, map);
-    return check_launch("ramp_filter_kernel");
+    if (n_slabs > 0 && in == out) return set_error(TF_ERR_INVALID_ARGUMENT, "slab-major output cannot be in place");
+    OutMap map{};
+    int st = build_map(map, n_lines, n_slabs > 0 ? rows_per_angle : 0, n_slabs, slab_row0, slab_base);
+    if (st) return st;
+    map.zblocked = 0;
+    map.w = nullptr;
+    return launch_filter(p, in, out, n_lines, i0, map, stream);
+}
+
+extern "C" int tf_filter_stage(const tf_filter_plan* p, const tf_bp_plan* bp, const float* in, void* stage,
+                               int64_t n_lines, float i0, int rows_per_angle, int n_slabs,
+                               const int32_t* slab_row0, const int64_t* slab_base, void* stream) {
+    if (!p || !bp) return set_error(TF_ERR_INVALID_ARGUMENT, "null plan");
+    if (n_lines < 0 || rows_per_angle < 1) return set_error(TF_ERR_INVALID_ARGUMENT, "invalid line counts");
+    if (n_lines == 0) return TF_OK;
+    if (!in || !stage) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    if (bp_plan_n_chan(bp) != p->n) return set_error(TF_ERR_INVALID_ARGUMENT, "filter/bp plans disagree on n_chan");
+    OutMap map{};
+    int st = build_map(map, n_lines, rows_per_angle, n_slabs, slab_row0, slab_base);
+    if (st) return st;
+    map.zblocked = 1;
+    map.w = bp_plan_weights(bp);
+    return launch_filter(p, in, static_cast<float*>(stage), n_lines, i0, map, stream);
 }
 
 extern "C" int tf_preprocess(const void* raw, int raw_dtype, double* out, int64_t n, double i0, void* stream) {

@@ -12,6 +12,9 @@
 namespace tf {
 
 int set_error(int status, const char* fmt, ...);
+// bp plan accessors for the fused filter -> staging path (backproject.cu)
+const float* bp_plan_weights(const tf_bp_plan* p);  // device feather weights, nullptr if all ones
+int bp_plan_n_chan(const tf_bp_plan* p);
 int check_launch(const char* what);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }

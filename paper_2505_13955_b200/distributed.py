@@ -11,9 +11,10 @@ devices:
 * rank g ingests and filters the angle chunk `split_range(n_proj, N)[g]`
   (all rows), i.e. 1/N of the projections, as north_star prescribes;
 * filtered rows reach their owner through one collective:
-    - "alltoall" (default, minimal bytes): K1 writes its output already
-      grouped slab-major, so a single `all_to_all_single` lands every
-      owner's rows angle-ordered in its staging input;
+    - "alltoall" (default, minimal bytes): K1 writes its output already in
+      K2's z-blocked staging layout, grouped per destination slab, so a
+      single `all_to_all_single` lands every owner's rows angle-ordered
+      directly in its staging buffer (no separate staging pass);
     - "allgather" (north_star's literal variant): `all_gather_into_tensor`
       of the natural-layout chunks, N x the bytes, owners stage their rows.
 """
@@ -30,23 +31,34 @@ from .fbp import FilterSpec
 from .geometry import AcquisitionParams, VolumeDims, split_range
 
 
-def exchange_layout(world: int, rank: int, n_proj: int, n_rows: int, n_chan: int):
+ZB, ZP = 32, 36  # z-block rows and padded row pitch of K2's staging layout (csrc/common.cuh)
+
+
+def _rows_elems(k: int, n_chan: int, zblocked: bool) -> int:
+    """Elements one angle of a k-row slab occupies: natural rows or z-blocks."""
+    return (-(-k // ZB)) * n_chan * ZP if zblocked else k * n_chan
+
+
+def exchange_layout(world: int, rank: int, n_proj: int, n_rows: int, n_chan: int, zblocked: bool = False):
     """Row-slab all-to-all layout for `rank`.
 
     Returns (slabs, chunks, slab_row0, slab_base, in_splits, out_splits):
     element offsets of each destination's block in the send buffer
-    (slab-major: [dest][angle][row-in-slab][chan]) and the split sizes of
-    `all_to_all_single`, in elements.
+    (slab-major: [dest][angle][rows of the dest slab]) and the split sizes of
+    `all_to_all_single`, in elements.  With `zblocked` the rows of a slab are
+    K2's staging layout ([zb][chan][36]), so what lands on the owner is its
+    staging buffer, angle-ordered.
     """
     slabs = split_range(n_rows, world)
     chunks = split_range(n_proj, world)
     a0, a1 = chunks[rank]
     A = a1 - a0
     r0, r1 = slabs[rank]
+    per = [_rows_elems(e - s, n_chan, zblocked) for s, e in slabs]
     slab_row0 = [s for s, _ in slabs] + [n_rows]
-    slab_base = [A * s * n_chan for s, _ in slabs]
-    in_splits = [A * (e - s) * n_chan for s, e in slabs]
-    out_splits = [(ce - cs) * (r1 - r0) * n_chan for cs, ce in chunks]
+    slab_base = [A * sum(per[:i]) for i in range(world)]
+    in_splits = [A * q for q in per]
+    out_splits = [(ce - cs) * per[rank] for cs, ce in chunks]
     return slabs, chunks, slab_row0, slab_base, in_splits, out_splits
 
 
@@ -57,6 +69,23 @@ def slab_major(chunk, slabs):
     import torch
 
     return torch.cat([chunk[:, s:e].reshape(-1) for s, e in slabs])
+
+
+def zblocked(rows, weights=None):
+    """Host/torch restatement of K2's staging layout (tf_bp_stage /
+    tf_filter_stage): (A, k, n_chan) -> flat [A][zb][n_chan][36], rows padded
+    to 32 with zeros, pad floats 32..35 zero, optional per-channel feather."""
+    import torch
+
+    A, k, n = rows.shape
+    nzb = -(-k // ZB)
+    x = rows if weights is None else rows * weights
+    out = torch.zeros((A, nzb * ZB, n), dtype=rows.dtype, device=rows.device)
+    out[:, :k] = x
+    out = out.view(A, nzb, ZB, n).permute(0, 1, 3, 2)  # [A][zb][n][32]
+    full = torch.zeros((A, nzb, n, ZP), dtype=rows.dtype, device=rows.device)
+    full[..., :ZB] = out
+    return full.reshape(-1)
 
 
 def exchange(send, recv, in_splits, out_splits, group=None):
@@ -83,7 +112,8 @@ class ZSlabReconstructor:
         self.params, self.dims = params, dims
         n_proj, n_rows, n_chan = params.n_proj, params.n_rows, params.n_chan
         (self.slabs, self.chunks, row0, base, self.in_splits,
-         self.out_splits) = exchange_layout(self.world, self.rank, n_proj, n_rows, n_chan)
+         self.out_splits) = exchange_layout(self.world, self.rank, n_proj, n_rows, n_chan,
+                                            zblocked=exchange_mode == "alltoall")
         self.a0, self.a1 = self.chunks[self.rank]
         self.r0, self.r1 = self.slabs[self.rank]
         self.device = torch.device(device if device is not None else "cuda")
@@ -93,11 +123,12 @@ class ZSlabReconstructor:
                 raise ValueError("allgather exchange needs n_proj divisible by the world size")
         elif exchange_mode != "alltoall":
             raise ValueError(f"unknown exchange mode {exchange_mode!r}")
-        # local slab engine; its `filt` buffer is the all-to-all landing zone
+        # local slab engine; its staging buffer is the all-to-all landing zone
         self.local = SlabReconstructor(params, dims, spec, i0, feather_band, rows=(self.r0, self.r1),
                                        device=self.device)
         A = self.a1 - self.a0
-        self.send = torch.empty(A * n_rows * n_chan, dtype=torch.float32, device=self.device)
+        self.send = torch.empty(sum(self.in_splits) if exchange_mode == "alltoall" else A * n_rows * n_chan,
+                                dtype=torch.float32, device=self.device)
         if exchange_mode == "allgather":
             self.gathered = torch.empty((n_proj, n_rows, n_chan), dtype=torch.float32,
                                         device=self.device)
@@ -113,7 +144,9 @@ class ZSlabReconstructor:
         return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
 
     def filter(self, raw_chunk):
-        """K1 over this rank's angle chunk, written in the exchange layout."""
+        """K1 over this rank's angle chunk, written in the exchange layout:
+        z-blocked staging per destination slab (alltoall) or natural rows
+        (allgather)."""
         p = self.params
         n_lines = raw_chunk.numel() // p.n_chan
         if self._map is None:
@@ -122,23 +155,22 @@ class ZSlabReconstructor:
                                   0, 0, None, None, self._s()))
         else:
             row0, base = self._map
-            check(lib().tf_filter(self.local.fplan.handle, ctypes.c_void_p(raw_chunk.data_ptr()),
-                                  ctypes.c_void_p(self.send.data_ptr()), n_lines, self.local.i0,
-                                  p.n_rows, self.world, row0, base, self._s()))
+            check(lib().tf_filter_stage(self.local.fplan.handle, self.local.bplan.handle,
+                                        ctypes.c_void_p(raw_chunk.data_ptr()), ctypes.c_void_p(self.send.data_ptr()),
+                                        n_lines, self.local.i0, p.n_rows, self.world, row0, base, self._s()))
 
     def exchange(self):
         import torch.distributed as dist
 
         if self.mode == "allgather":
             dist.all_gather_into_tensor(self.gathered.view(-1), self.send, group=self.group)
-        else:
-            exchange(self.send, self.local.filt.view(-1), self.in_splits, self.out_splits, self.group)
+        else:  # lands directly in this rank's staging buffer
+            exchange(self.send, self.local.stage.view(self.torch.float32), self.in_splits, self.out_splits,
+                     self.group)
 
     def stage(self):
         if self.mode == "allgather":
             self.local.stage_rows(self.gathered, rows_per_angle=self.params.n_rows, r0=self.r0)
-        else:
-            self.local.stage_rows(self.local.filt)
 
     def run(self, raw_chunk):
         """raw_chunk: device (A, n_rows, n_chan) fp32 counts of this rank's

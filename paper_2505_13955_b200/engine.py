@@ -47,13 +47,18 @@ class SlabReconstructor:
             self.fplan = filter_plan(params.n_chan, self.spec, params.pixel_pitch)
             self.bplan = bp_plan(params, dims, feather_band)
             self.in_place = in_place_filter
-            shape = (params.n_proj, self.k, params.n_chan)
-            self.filt = None if in_place_filter else torch.empty(shape, dtype=torch.float32,
-                                                                   device=self.device)
+            self._filt = None  # natural-layout filtered rows, only for the unfused path
             self.stage = torch.empty(self.bplan.stage_bytes(self.k), dtype=torch.uint8,
                                      device=self.device)
             self.vol = torch.empty((self.k, dims.ny, dims.nx), dtype=torch.float32,
                                    device=self.device)
+
+    @property
+    def filt(self):
+        if self._filt is None:
+            self._filt = self.torch.empty((self.params.n_proj, self.k, self.params.n_chan),
+                                          dtype=self.torch.float32, device=self.device)
+        return self._filt
 
     # -- individual kernels (stream = torch current stream unless given)
     def _s(self, stream):
@@ -67,6 +72,14 @@ class SlabReconstructor:
         check(lib().tf_filter(self.fplan.handle, _ptr(raw), _ptr(out), n_lines,
                               self.i0 if i0 is None else float(i0), 0, 0, None, None, self._s(stream)))
         return out
+
+    def filter_stage(self, raw, stream=None, i0=None):
+        """Fused K1: raw counts (n_proj, k, n_chan) -> Beer-Lambert -> ramp
+        filter -> feather -> z-blocked staging buffer (no filtered copy)."""
+        n_lines = raw.numel() // self.params.n_chan
+        check(lib().tf_filter_stage(self.fplan.handle, self.bplan.handle, _ptr(raw), _ptr(self.stage), n_lines,
+                                    self.i0 if i0 is None else float(i0), self.k, 0, None, None,
+                                    self._s(stream)))
 
     def stage_rows(self, filt, rows_per_angle=None, r0=0, stream=None):
         rpa = rows_per_angle if rows_per_angle is not None else self.k
@@ -87,8 +100,7 @@ class SlabReconstructor:
 
     def run(self, raw, stream=None):
         """raw: device (n_proj, k, n_chan) fp32 counts -> self.vol."""
-        filt = self.filter(raw, stream=stream)
-        self.stage_rows(filt, stream=stream)
+        self.filter_stage(raw, stream=stream)
         return self.backproject(stream=stream)
 
     def updates(self) -> int:
@@ -180,14 +192,12 @@ class StreamedReconstructor:
             h2d_done.record(self.s_h2d)
             # compute
             self.s_comp.wait_event(h2d_done)
-            src = self.raw[b].view(-1)[: p.n_proj * k * n].view(p.n_proj, k, n)
-            self.eng.filter(src, out=self.eng.filt.view(-1)[: p.n_proj * k * n].view(p.n_proj, k, n),
-                            stream=self.s_comp)
+            check(lib().tf_filter_stage(self.eng.fplan.handle, self.eng.bplan.handle, _ptr(self.raw[b]),
+                                        _ptr(self.eng.stage), p.n_proj * k, self.eng.i0, k, 0, None, None,
+                                        ctypes.c_void_p(self.s_comp.cuda_stream)))
             ev = torch.cuda.Event()
             ev.record(self.s_comp)
             raw_free[b] = ev
-            check(lib().tf_bp_stage(self.eng.bplan.handle, _ptr(self.eng.filt), k, 0, k, _ptr(self.eng.stage),
-                                    ctypes.c_void_p(self.s_comp.cuda_stream)))
             if vol_free[b] is not None:
                 self.s_comp.wait_event(vol_free[b])
             check(lib().tf_backproject(self.eng.bplan.handle, _ptr(self.eng.stage), k, _ptr(self.vol[b]), 0,

@@ -26,35 +26,41 @@ def _full(n_proj, n_rows, n_chan):
     return a + r + c
 
 
-def _worker(rank, world, port, shape, q):
+def _worker(rank, world, port, shape, q, zb=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2505_13955_b200.distributed import exchange, exchange_layout, slab_major
+        from paper_2505_13955_b200.distributed import exchange, exchange_layout, slab_major, zblocked
 
         n_proj, n_rows, n_chan = shape
         full = _full(*shape)
-        slabs, chunks, row0, base, ins, outs = exchange_layout(world, rank, *shape)
+        slabs, chunks, row0, base, ins, outs = exchange_layout(world, rank, *shape, zblocked=zb)
         a0, a1 = chunks[rank]
         r0, r1 = slabs[rank]
-        send = slab_major(full[a0:a1], slabs)
+        if zb:  # K1's fused output: one z-blocked staging array per destination slab
+            send = torch.cat([zblocked(full[a0:a1, s:e]) for s, e in slabs])
+        else:
+            send = slab_major(full[a0:a1], slabs)
         assert send.numel() == sum(ins)
         assert base == [sum(ins[:i]) for i in range(world)]
-        recv = torch.empty(n_proj * (r1 - r0) * n_chan)
+        recv = torch.empty(sum(outs))
         exchange(send, recv, ins, outs)
-        ok = torch.equal(recv.view(n_proj, r1 - r0, n_chan), full[:, r0:r1])
+        want = zblocked(full[:, r0:r1]) if zb else full[:, r0:r1].reshape(-1)
+        ok = torch.equal(recv, want)
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,shape", [(2, (12, 10, 8)), (3, (7, 11, 5)), (2, (1800 // 60, 64, 16))])
-def test_row_slab_all_to_all_layout(world, shape):
+@pytest.mark.parametrize("world,shape,zb", [(2, (12, 10, 8), False), (3, (7, 11, 5), False),
+                                           (2, (1800 // 60, 64, 16), False), (2, (12, 70, 8), True),
+                                           (3, (7, 40, 5), True)])
+def test_row_slab_all_to_all_layout(world, shape, zb):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, q, zb)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=120) for _ in range(world))

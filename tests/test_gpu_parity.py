@@ -425,3 +425,39 @@ def test_multi_gpu_zslab_bitwise(F):
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
         print(r.stdout[-2000:], r.stderr[-2000:])
         assert r.returncode == 0 and "MGPU_OK" in r.stdout
+
+
+@pytest.mark.parametrize("rows,offset", [(64, 0), (45, 0), (7, 0), (33, 13)])
+def test_fused_filter_stage_equals_filter_then_stage(F, rows, offset):
+    """K1 writing K2's staging layout directly (feather fused) == K1 natural
+    output followed by tf_bp_stage, bit for bit; also == the host restatement."""
+    import math as _m
+
+    import torch
+
+    from paper_2505_13955_b200.distributed import zblocked
+    from paper_2505_13955_b200.engine import SlabReconstructor
+    from paper_2505_13955_b200.geometry import AcquisitionParams, ScanMode, VolumeDims
+
+    if offset:
+        p = AcquisitionParams(n_proj=20, n_rows=rows, n_chan=48, angle_span=2 * _m.pi,
+                              scan_mode=ScanMode.OFFSET, offset_chan=offset)
+    else:
+        p = AcquisitionParams(n_proj=21, n_rows=rows, n_chan=48)
+    d = VolumeDims(48, 48, rows)
+    raw = _phantom_rows(p, d, 0, rows)
+    eng = SlabReconstructor(p, d, i0=1e5)
+    eng.filter_stage(raw)
+    fused = eng.stage.clone().view(torch.float32)
+    filt = eng.filter(raw)
+    eng.stage_rows(filt)
+    two = eng.stage.view(torch.float32)
+    nzb = -(-rows // 32)
+    f = fused.view(p.n_proj, nzb, 48, 36)[..., :32]
+    t = two.view(p.n_proj, nzb, 48, 36)[..., :32]
+    k_last = rows - 32 * (nzb - 1)
+    assert torch.equal(f[:, :-1], t[:, :-1])            # full z-blocks
+    assert torch.equal(f[:, -1, :, :k_last], t[:, -1, :, :k_last])  # valid rows of the last block
+    w = torch.from_numpy(F.offset_weights(p)).float().cuda()
+    host = zblocked(filt, w).view(p.n_proj, nzb, 48, 36)[..., :32]
+    assert torch.equal(host[:, :-1], t[:, :-1])
