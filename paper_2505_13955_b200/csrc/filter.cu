@@ -182,17 +182,19 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* tw, int
     __syncthreads();
 }
 
-// Radix-8 passes (T >= P / (8 * NB8) threads) plus one radix-4/2 pass.
-template <int NB8>
+// Radix-16 passes (one butterfly per thread, T >= P/16) plus one radix-8/4/2
+// pass.  With the 1-in-16 padding of pad_idx, every radix-16 pass reads and
+// writes shared memory without bank conflicts.
 __device__ __forceinline__ void fft_forward(float2* buf, const float2* tw, int P, int log2P, int tid, int T) {
     int Ns = 1, rem = log2P;
-    while (rem >= 3) {
-        stockham_pass<8, NB8>(buf, tw, P, Ns, tid, T);
-        Ns <<= 3;
-        rem -= 3;
+    while (rem >= 4) {
+        stockham_pass<16, 1>(buf, tw, P, Ns, tid, T);
+        Ns <<= 4;
+        rem -= 4;
     }
-    if (rem == 2) stockham_pass<4, 2 * NB8>(buf, tw, P, Ns, tid, T);
-    else if (rem == 1) stockham_pass<2, 4 * NB8>(buf, tw, P, Ns, tid, T);
+    if (rem == 3) stockham_pass<8, 2>(buf, tw, P, Ns, tid, T);
+    else if (rem == 2) stockham_pass<4, 4>(buf, tw, P, Ns, tid, T);
+    else if (rem == 1) stockham_pass<2, 8>(buf, tw, P, Ns, tid, T);
 }
 
 // Where filtered line l = (angle a, row r) goes (tf_filter's slab map and
@@ -228,8 +230,8 @@ __device__ __forceinline__ long long out_offset(long long l, int n, const OutMap
 
 // Persistent: each CTA loops over line pairs; the twiddle table is loaded
 // into shared memory once per CTA.
-template <bool SMEM_TW, int NB8>
-__global__ void __launch_bounds__(1024) ramp_filter_kernel(const float* __restrict__ in, float* out,
+template <bool SMEM_TW, int MAXT>
+__global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kernel(const float* __restrict__ in, float* out,
                                                            long long n_lines, int n, int P, int log2P,
                                                            const float2* __restrict__ tw_g,
                                                            const float* __restrict__ mult,
@@ -276,9 +278,9 @@ __global__ void __launch_bounds__(1024) ramp_filter_kernel(const float* __restri
         __syncthreads();
 
         if (radius > 0) {  // scipy gaussian_filter1d(mode="nearest") restated (fbp.py:125-126)
-            float2 acc[4 * NB8];  // n <= P/2 <= 4*NB8*T
+            float2 acc[8];  // n <= P/2 <= 8*T
 #pragma unroll
-            for (int q = 0; q < 4 * NB8; ++q) {
+            for (int q = 0; q < 8; ++q) {
                 const int m = tid + q * T;
                 float2 s = make_float2(0.f, 0.f);
                 if (m < n) {
@@ -294,14 +296,14 @@ __global__ void __launch_bounds__(1024) ramp_filter_kernel(const float* __restri
             }
             __syncthreads();
 #pragma unroll
-            for (int q = 0; q < 4 * NB8; ++q) {
+            for (int q = 0; q < 8; ++q) {
                 const int m = tid + q * T;
                 if (m < n) data[pad_idx(m)] = acc[q];
             }
             __syncthreads();
         }
 
-        fft_forward<NB8>(data, tw, P, log2P, tid, T);
+        fft_forward(data, tw, P, log2P, tid, T);
 
         // X <- conj(X * M / P): the inverse transform is conj(FFT(conj(.)))
         for (int m = tid; m < P; m += T) {
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(1024) ramp_filter_kernel(const float* __restri
         }
         __syncthreads();
 
-        fft_forward<NB8>(data, tw, P, log2P, tid, T);
+        fft_forward(data, tw, P, log2P, tid, T);
 
         int za, zb = 0;
         float* oa = out + out_offset(la, n, map, s_row0, s_base, za);
@@ -386,7 +388,7 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
     p->n = n_chan;
     p->P = P;
     p->log2P = ilog2(P);
-    p->threads = std::max(32, std::min(1024, P / 8));  // one radix-8 butterfly per thread (2 at P = 16384)
+    p->threads = std::max(32, P / 16);  // one radix-16 butterfly per thread (P <= 16384 -> <= 1024)
     // twiddles in fp64, rounded once
     std::vector<float2> tw(P);
     for (int m = 0; m < P; ++m) {
@@ -421,9 +423,9 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
         e = cudaMemcpy(p->d_blur, bw.data(), sizeof(float) * (2 * rad + 1), cudaMemcpyHostToDevice);
     p->smem_tw = P <= 8192;  // twiddle table in shared memory next to the line buffer
     p->smem = (P + P / 16 + (p->smem_tw ? P : 0)) * (int)sizeof(float2);
-    p->kernel = P <= 8192 ? (p->smem_tw ? (const void*)ramp_filter_kernel<true, 1>
-                                        : (const void*)ramp_filter_kernel<false, 1>)
-                          : (const void*)ramp_filter_kernel<false, 2>;
+    p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256>
+                : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512>
+                                    : (const void*)ramp_filter_kernel<false, 1024>;
     if (e == cudaSuccess) e = cudaFuncSetAttribute(p->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem);
     if (e == cudaSuccess) {
         int blocks = 0;
