@@ -24,7 +24,8 @@ struct tf_filter_plan {
     int log2P;
     int threads;
     int blur_radius;
-    float2* d_tw;      // exp(-2 pi i m / P), m in [0, P)
+    float2* d_tw;      // per-pass twiddle tables (twiddle_tables)
+    int n_tw;          // entries
     float* d_mult;     // multiplier / P, m in [0, P/2]
     float* d_blur;     // 2*radius+1 Gaussian weights (or null)
     bool smem_tw;      // twiddles staged in shared memory (P <= 8192)
@@ -153,7 +154,6 @@ template <int R, int NB>
 __device__ __forceinline__ void stockham_pass(float2* buf, const float2* tw, int P, int Ns, int tid, int T) {
     float2 v[NB][R];
     const int nb = P / R;
-    const int stride = P / (Ns * R);
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
         const int j = tid + b * T;
@@ -162,7 +162,9 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* tw, int
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 float2 x = buf[pad_idx(j + r * nb)];
-                if (r > 0 && Ns > 1) x = cmul(x, tw[k * r * stride]);
+                // pass table [r][k] = exp(-2 pi i k r / (Ns R)): consecutive lanes
+                // read consecutive entries (no bank conflicts)
+                if (r > 0 && Ns > 1) x = cmul(x, tw[r * Ns + k]);
                 v[b][r] = x;
             }
             dft<R>(v[b]);
@@ -184,17 +186,42 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* tw, int
 
 // Radix-16 passes (one butterfly per thread, T >= P/16) plus one radix-8/4/2
 // pass.  With the 1-in-16 padding of pad_idx, every radix-16 pass reads and
-// writes shared memory without bank conflicts.
+// writes shared memory without bank conflicts.  `tw` holds the per-pass
+// twiddle tables back to back (twiddle_tables() on the host).
 __device__ __forceinline__ void fft_forward(float2* buf, const float2* tw, int P, int log2P, int tid, int T) {
     int Ns = 1, rem = log2P;
     while (rem >= 4) {
         stockham_pass<16, 1>(buf, tw, P, Ns, tid, T);
+        if (Ns > 1) tw += 16 * Ns;
         Ns <<= 4;
         rem -= 4;
     }
     if (rem == 3) stockham_pass<8, 2>(buf, tw, P, Ns, tid, T);
     else if (rem == 2) stockham_pass<4, 4>(buf, tw, P, Ns, tid, T);
     else if (rem == 1) stockham_pass<2, 8>(buf, tw, P, Ns, tid, T);
+}
+
+// Per-pass twiddle tables, same pass sequence as fft_forward: for each pass
+// with Ns > 1, R*Ns entries [r][k] = exp(-2 pi i k r / (Ns R)) (fp64, rounded once).
+std::vector<float2> twiddle_tables(int P, int log2P) {
+    std::vector<float2> t;
+    auto add = [&](int R, int Ns) {
+        if (Ns == 1) return;
+        for (int r = 0; r < R; ++r)
+            for (int k = 0; k < Ns; ++k) {
+                const double a = -2.0 * M_PI * (double)k * (double)r / ((double)Ns * (double)R);
+                t.push_back(make_float2((float)cos(a), (float)sin(a)));
+            }
+    };
+    int Ns = 1, rem = log2P;
+    while (rem >= 4) {
+        add(16, Ns);
+        Ns <<= 4;
+        rem -= 4;
+    }
+    if (rem > 0) add(1 << rem, Ns);
+    if (t.empty()) t.push_back(make_float2(1.f, 0.f));
+    return t;
 }
 
 // Where filtered line l = (angle a, row r) goes (tf_filter's slab map and
@@ -236,7 +263,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kerne
                                                            const float2* __restrict__ tw_g,
                                                            const float* __restrict__ mult,
                                                            const float* __restrict__ blur, int radius,
-                                                           float i0, OutMap map) {
+                                                           float i0, OutMap map, int n_tw) {
     extern __shared__ float2 sbuf[];
     __shared__ int32_t s_row0[9];
     __shared__ long long s_base[8];
@@ -251,7 +278,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kerne
     float2* data = sbuf;
     if constexpr (SMEM_TW) {
         float2* tws = sbuf + (P + P / 16);
-        for (int m = tid; m < P; m += T) tws[m] = tw_g[m];
+        for (int m = tid; m < n_tw; m += T) tws[m] = tw_g[m];
         tw = tws;  // visible after the first __syncthreads below
     }
     const long long n_pairs = (n_lines + 1) / 2;
@@ -389,12 +416,8 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
     p->P = P;
     p->log2P = ilog2(P);
     p->threads = std::max(32, P / 16);  // one radix-16 butterfly per thread (P <= 16384 -> <= 1024)
-    // twiddles in fp64, rounded once
-    std::vector<float2> tw(P);
-    for (int m = 0; m < P; ++m) {
-        double a = -2.0 * M_PI * (double)m / (double)P;
-        tw[m] = make_float2((float)cos(a), (float)sin(a));
-    }
+    std::vector<float2> tw = twiddle_tables(P, p->log2P);
+    p->n_tw = (int)tw.size();
     std::vector<double> mult(P / 2 + 1);
     multiplier_fp64(kind, P, pixel_pitch, mult.data());
     std::vector<float> multf(P / 2 + 1);
@@ -413,16 +436,16 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
         for (int j = 0; j <= 2 * rad; ++j) bw[j] = (float)(w[j] / sum);
     }
     p->blur_radius = rad;
-    cudaError_t e = cudaMalloc(&p->d_tw, sizeof(float2) * P);
+    cudaError_t e = cudaMalloc(&p->d_tw, sizeof(float2) * p->n_tw);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_mult, sizeof(float) * (P / 2 + 1));
     if (e == cudaSuccess && rad > 0) e = cudaMalloc(&p->d_blur, sizeof(float) * (2 * rad + 1));
-    if (e == cudaSuccess) e = cudaMemcpy(p->d_tw, tw.data(), sizeof(float2) * P, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_tw, tw.data(), sizeof(float2) * p->n_tw, cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
         e = cudaMemcpy(p->d_mult, multf.data(), sizeof(float) * (P / 2 + 1), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && rad > 0)
         e = cudaMemcpy(p->d_blur, bw.data(), sizeof(float) * (2 * rad + 1), cudaMemcpyHostToDevice);
     p->smem_tw = P <= 8192;  // twiddle table in shared memory next to the line buffer
-    p->smem = (P + P / 16 + (p->smem_tw ? P : 0)) * (int)sizeof(float2);
+    p->smem = (P + P / 16 + (p->smem_tw ? p->n_tw : 0)) * (int)sizeof(float2);
     p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256>
                 : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512>
                                     : (const void*)ramp_filter_kernel<false, 1024>;
@@ -487,8 +510,9 @@ int launch_filter(const tf_filter_plan* p, const float* in, float* out, int64_t 
     const float* mult = p->d_mult;
     const float* blur = p->d_blur;
     OutMap m = map;
+    int ntw = p->n_tw;
     void* args[] = {(void*)&in, (void*)&out, &nl, &n, &P, &l2, (void*)&tw, (void*)&mult, (void*)&blur, &rad,
-                    &i0, &m};
+                    &i0, &m, &ntw};
     TF_CUDA_TRY(cudaLaunchKernel(p->kernel, dim3(grid), dim3(p->threads), args, p->smem, as_stream(stream)));
     return TF_OK;
 }
