@@ -146,6 +146,28 @@ def main():
     g["e2eoff_f64"] = fbp.back_project(filt, d, p, dtype=np.float64)
     meta["cases"]["e2eoff"] = geom_record(p, d)
 
+    # --- pipeline.run (pipeline.py:119-324), the caller the shim rebinds:
+    # 2x2x1 simulated ranks (row slabs x angle chunks), float32 volumes + uint16
+    from tomofuse import pipeline
+    from tomofuse.fabric import Fabric, StorageModel
+    from tomofuse.geometry import Specimen, SpecimenSet
+    from tomofuse.partition import RankGrid
+
+    n, n_proj = 40, 36
+    p = params(n_proj, n, n)
+    d = VolumeDims(n, n, n)
+    micro = phantom.generate_microstructure(d, 0.25, 0.03, seed=3)
+    counts = phantom.intensity_sinogram(
+        micro, p, phantom.DegradationSpec(poisson_flux=1e5, seed=3, poisson_enabled=False))
+    counts = counts.astype(np.float32)
+    sset = SpecimenSet(specimens=(Specimen(params=p, dims=d, specimen_id="s0"),))
+    cfg = pipeline.PipelineConfig(grid=RankGrid(2, 2, 1), i0=1e5, hu_window=HuWindow(0.0, 4e-4))
+    res = pipeline.run(sset, {"s0": counts}, cfg, Fabric(n_ranks=cfg.grid.total), StorageModel())
+    g["pipe_raw"] = counts
+    g["pipe_vol"] = res.volumes["s0"]
+    g["pipe_q"] = res.quantized["s0"]
+    meta["cases"]["pipe"] = dict(geom_record(p, d), grid=[2, 2, 1])
+
     g["meta_json"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT}: {len(g)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")

@@ -269,3 +269,42 @@ def test_product_package_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_shim_rebinds_reference_surface():
+    """shim.install() rebinds tomofuse.fbp.* and the names pipeline.py:30
+    imported, and uninstall() restores them (fake modules: no reference
+    needed at run time)."""
+    import types
+
+    from paper_2505_13955_b200 import fbp as gpu
+    from paper_2505_13955_b200 import shim
+
+    def orig(*a, **k):
+        return "cpu"
+
+    fbp_mod = types.ModuleType("tomofuse.fbp")
+    pipe_mod = types.ModuleType("tomofuse.pipeline")
+    for name in ("preprocess", "ramp_filter", "back_project", "quantize", "reconstruct",
+                 "filter_multiplier", "offset_weights"):
+        setattr(fbp_mod, name, orig)
+    for name in ("preprocess", "ramp_filter", "back_project", "quantize"):
+        setattr(pipe_mod, name, orig)
+    mods = {"tomofuse.fbp": fbp_mod, "tomofuse.pipeline": pipe_mod}
+    done = shim.install(mods)
+    assert "tomofuse.pipeline.back_project" in done and "tomofuse.fbp.reconstruct" in done
+    assert pipe_mod.back_project is gpu.back_project and fbp_mod.quantize is gpu.quantize
+    shim.uninstall(mods)
+    assert pipe_mod.back_project is orig and fbp_mod.reconstruct is orig
+
+
+def test_oracle_matches_reference_pipeline_run(golden):
+    """pipeline.run over a 2x2 simulated grid == the serial float32 chain
+    (pkg/tests/test_pipeline.py:102-112 tolerance 1e-5), through the oracle."""
+    from oracle import fbp_oracle as O
+
+    g, meta = golden
+    geom = oracle_geom(meta["cases"]["pipe"])
+    serial = O.fbp_rows(g["pipe_raw"], geom, dtype=np.float32)
+    scale = np.abs(serial).max()
+    assert np.abs(serial - g["pipe_vol"]).max() <= 1e-5 * scale
