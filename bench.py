@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "allgather"])
+    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "allgather", "p2p"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--slab-rows", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")

@@ -116,6 +116,16 @@ TF_API int tf_filter_stage(const tf_filter_plan* plan, const tf_bp_plan* bp, con
                            int64_t n_lines, float i0, int rows_per_angle, int n_slabs, const int32_t* slab_row0,
                            const int64_t* slab_base, void* stream);
 
+/* Fused filter + exchange: like tf_filter_stage with n_slabs > 0, but slab s
+ * is written straight to the device pointer slab_dst[s] -- typically the
+ * owner GPU's staging buffer mapped over NVLink (CUDA IPC / symmetric
+ * memory), already offset to this rank's first angle.  The K1 epilogue's
+ * stores ARE the row-slab all-to-all; the caller orders them with a
+ * cross-GPU barrier before the owners' back-projection. */
+TF_API int tf_filter_stage_peers(const tf_filter_plan* plan, const tf_bp_plan* bp, const float* in, int64_t n_lines,
+                                 float i0, int rows_per_angle, int n_slabs, const int32_t* slab_row0,
+                                 void* const* slab_dst, void* stream);
+
 /* Beer-Lambert only (fbp.py:75-83): fp32 or fp64 counts -> fp64 depth
  * (the reference's output dtype), computed in fp64. */
 TF_API int tf_preprocess(const void* raw, int raw_dtype, double* out, int64_t n, double i0, void* stream);

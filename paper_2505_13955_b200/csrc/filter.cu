@@ -231,14 +231,14 @@ struct OutMap {
     int n_slabs;         // >= 1 (1 slab == whole row range)
     int rows_per_angle;
     int32_t row0[9];
-    long long base[8];   // element offset of each slab's block
+    float* dst[8];       // start of each slab's block (may be a peer GPU's buffer over NVLink)
     const float* w;      // per-channel feather (z-blocked output only), may be null
 };
 
 // row0/base are read from a shared-memory copy (dynamic indexing of a
 // kernel-parameter array would spill the struct to local memory)
-__device__ __forceinline__ long long out_offset(long long l, int n, const OutMap& m, const int32_t* row0,
-                                                const long long* base, int& zi) {
+__device__ __forceinline__ float* out_ptr(long long l, int n, const OutMap& m, const int32_t* row0,
+                                          float* const* dst, int& zi) {
     const long long a = l / m.rows_per_angle;
     const int r = (int)(l - a * m.rows_per_angle);
     int s = 0;
@@ -248,11 +248,11 @@ __device__ __forceinline__ long long out_offset(long long l, int n, const OutMap
     const int ks = row0[s + 1] - row0[s];
     if (!m.zblocked) {
         zi = 0;
-        return base[s] + (a * ks + rl) * (long long)n;
+        return dst[s] + (a * ks + rl) * (long long)n;
     }
     const int nzb = (ks + kZB - 1) / kZB;
     zi = rl % kZB;
-    return base[s] + ((a * nzb + rl / kZB) * (long long)n) * kZP + zi;
+    return dst[s] + ((a * nzb + rl / kZB) * (long long)n) * kZP + zi;
 }
 
 // Persistent: each CTA loops over line pairs; the twiddle table is loaded
@@ -266,13 +266,13 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kerne
                                                            float i0, OutMap map, int n_tw) {
     extern __shared__ float2 sbuf[];
     __shared__ int32_t s_row0[9];
-    __shared__ long long s_base[8];
+    __shared__ float* s_dst[8];
     const int tid = threadIdx.x, T = blockDim.x;
     if (tid == 0) {
 #pragma unroll
         for (int s = 0; s < 9; ++s) s_row0[s] = map.row0[s];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) s_base[s] = map.base[s];
+        for (int s = 0; s < 8; ++s) s_dst[s] = map.dst[s];
     }
     const float2* tw = tw_g;
     float2* data = sbuf;
@@ -343,8 +343,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kerne
         fft_forward(data, tw, P, log2P, tid, T);
 
         int za, zb = 0;
-        float* oa = out + out_offset(la, n, map, s_row0, s_base, za);
-        float* ob = has_b ? out + out_offset(la + 1, n, map, s_row0, s_base, zb) : nullptr;
+        float* oa = out_ptr(la, n, map, s_row0, s_dst, za);
+        float* ob = has_b ? out_ptr(la + 1, n, map, s_row0, s_dst, zb) : nullptr;
         if (!map.zblocked) {
             for (int m = tid; m < n; m += T) {
                 const float2 y = data[pad_idx(m)];
@@ -477,15 +477,18 @@ extern "C" int tf_filter_plan_destroy(tf_filter_plan* p) {
 
 namespace tf {
 namespace {
-int build_map(OutMap& map, int64_t n_lines, int rows_per_angle, int n_slabs, const int32_t* slab_row0,
-              const int64_t* slab_base) {
+int build_map(OutMap& map, float* out, int64_t n_lines, int rows_per_angle, int n_slabs, const int32_t* slab_row0,
+              const int64_t* slab_base, void* const* slab_dst = nullptr) {
     map.n_slabs = n_slabs > 0 ? n_slabs : 1;
     map.rows_per_angle = rows_per_angle > 0 ? rows_per_angle : (int)std::min<int64_t>(n_lines, 1 << 30);
     if (n_slabs > 0) {
-        if (n_slabs > 8 || rows_per_angle < 1 || !slab_row0 || !slab_base)
+        if (n_slabs > 8 || rows_per_angle < 1 || !slab_row0 || (!slab_base && !slab_dst))
             return set_error(TF_ERR_INVALID_ARGUMENT, "invalid slab map");
         for (int s = 0; s <= n_slabs; ++s) map.row0[s] = slab_row0[s];
-        for (int s = 0; s < n_slabs; ++s) map.base[s] = slab_base[s];
+        for (int s = 0; s < n_slabs; ++s) {
+            map.dst[s] = slab_dst ? static_cast<float*>(slab_dst[s]) : out + slab_base[s];
+            if (!map.dst[s]) return set_error(TF_ERR_INVALID_ARGUMENT, "null slab destination");
+        }
         if (map.row0[0] != 0 || map.row0[n_slabs] != rows_per_angle)
             return set_error(TF_ERR_INVALID_ARGUMENT, "slab rows must cover [0, rows_per_angle)");
         for (int s = 0; s < n_slabs; ++s)
@@ -493,7 +496,7 @@ int build_map(OutMap& map, int64_t n_lines, int rows_per_angle, int n_slabs, con
     } else {
         map.row0[0] = 0;
         map.row0[1] = map.rows_per_angle;
-        map.base[0] = 0;
+        map.dst[0] = out;
     }
     if (rows_per_angle > 0 && n_lines % rows_per_angle != 0)
         return set_error(TF_ERR_INVALID_ARGUMENT, "n_lines must be a multiple of rows_per_angle");
@@ -528,7 +531,7 @@ extern "C" int tf_filter(const tf_filter_plan* p, const float* in, float* out, i
     if (!in || !out) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
     if (n_slabs > 0 && in == out) return set_error(TF_ERR_INVALID_ARGUMENT, "slab-major output cannot be in place");
     OutMap map{};
-    int st = build_map(map, n_lines, n_slabs > 0 ? rows_per_angle : 0, n_slabs, slab_row0, slab_base);
+    int st = build_map(map, out, n_lines, n_slabs > 0 ? rows_per_angle : 0, n_slabs, slab_row0, slab_base);
     if (st) return st;
     map.zblocked = 0;
     map.w = nullptr;
@@ -544,11 +547,27 @@ extern "C" int tf_filter_stage(const tf_filter_plan* p, const tf_bp_plan* bp, co
     if (!in || !stage) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
     if (bp_plan_n_chan(bp) != p->n) return set_error(TF_ERR_INVALID_ARGUMENT, "filter/bp plans disagree on n_chan");
     OutMap map{};
-    int st = build_map(map, n_lines, rows_per_angle, n_slabs, slab_row0, slab_base);
+    int st = build_map(map, static_cast<float*>(stage), n_lines, rows_per_angle, n_slabs, slab_row0, slab_base);
     if (st) return st;
     map.zblocked = 1;
     map.w = bp_plan_weights(bp);
     return launch_filter(p, in, static_cast<float*>(stage), n_lines, i0, map, stream);
+}
+
+extern "C" int tf_filter_stage_peers(const tf_filter_plan* p, const tf_bp_plan* bp, const float* in,
+                                     int64_t n_lines, float i0, int rows_per_angle, int n_slabs,
+                                     const int32_t* slab_row0, void* const* slab_dst, void* stream) {
+    if (!p || !bp) return set_error(TF_ERR_INVALID_ARGUMENT, "null plan");
+    if (n_lines < 0 || rows_per_angle < 1 || n_slabs < 1) return set_error(TF_ERR_INVALID_ARGUMENT, "invalid line counts");
+    if (n_lines == 0) return TF_OK;
+    if (!in || !slab_dst) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    if (bp_plan_n_chan(bp) != p->n) return set_error(TF_ERR_INVALID_ARGUMENT, "filter/bp plans disagree on n_chan");
+    OutMap map{};
+    int st = build_map(map, nullptr, n_lines, rows_per_angle, n_slabs, slab_row0, nullptr, slab_dst);
+    if (st) return st;
+    map.zblocked = 1;
+    map.w = bp_plan_weights(bp);
+    return launch_filter(p, in, map.dst[0], n_lines, i0, map, stream);
 }
 
 extern "C" int tf_preprocess(const void* raw, int raw_dtype, double* out, int64_t n, double i0, void* stream) {

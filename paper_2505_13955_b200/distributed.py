@@ -15,6 +15,12 @@ devices:
       K2's z-blocked staging layout, grouped per destination slab, so a
       single `all_to_all_single` lands every owner's rows angle-ordered
       directly in its staging buffer (no separate staging pass);
+    - "p2p" (fused compute + exchange): every rank's staging buffer is
+      symmetric memory mapped over NVLink; K1's epilogue stores each
+      destination slab's rows straight into the owner's staging buffer
+      (tf_filter_stage_peers), so the all-to-all IS the filter's store
+      stream.  Two symmetric-memory barriers per step order it (previous
+      back-projection done before overwrite; all stores landed before K2);
     - "allgather" (north_star's literal variant): `all_gather_into_tensor`
       of the natural-layout chunks, N x the bytes, owners stage their rows.
 """
@@ -121,14 +127,28 @@ class ZSlabReconstructor:
             sizes = {e - s for s, e in self.chunks}
             if len(sizes) != 1:
                 raise ValueError("allgather exchange needs n_proj divisible by the world size")
-        elif exchange_mode != "alltoall":
+        elif exchange_mode not in ("alltoall", "p2p"):
             raise ValueError(f"unknown exchange mode {exchange_mode!r}")
-        # local slab engine; its staging buffer is the all-to-all landing zone
-        self.local = SlabReconstructor(params, dims, spec, i0, feather_band, rows=(self.r0, self.r1),
-                                       device=self.device)
         A = self.a1 - self.a0
-        self.send = torch.empty(sum(self.in_splits) if exchange_mode == "alltoall" else A * n_rows * n_chan,
-                                dtype=torch.float32, device=self.device)
+        self.symm = None
+        stage = None
+        if exchange_mode == "p2p":
+            import torch.distributed._symmetric_memory as symm
+
+            zper = [_rows_elems(e - s, n_chan, True) for s, e in self.slabs]  # floats per angle per slab
+            stage = symm.empty(n_proj * max(zper), dtype=torch.float32, device=self.device)
+            self.symm = symm.rendezvous(stage, group if group is not None else dist.group.WORLD)
+            # slab s's rows of my angles go to rank s's staging buffer at angle a0
+            dst = [int(self.symm.buffer_ptrs[s]) + self.a0 * zper[s] * 4 for s in range(self.world)]
+            self._dst = (ctypes.c_void_p * self.world)(*dst)
+        # local slab engine; its staging buffer is the exchange landing zone
+        self.local = SlabReconstructor(params, dims, spec, i0, feather_band, rows=(self.r0, self.r1),
+                                       device=self.device, stage=stage)
+        if exchange_mode == "p2p":
+            self.send = None
+        else:
+            self.send = torch.empty(sum(self.in_splits) if exchange_mode == "alltoall" else A * n_rows * n_chan,
+                                    dtype=torch.float32, device=self.device)
         if exchange_mode == "allgather":
             self.gathered = torch.empty((n_proj, n_rows, n_chan), dtype=torch.float32,
                                         device=self.device)
@@ -149,6 +169,13 @@ class ZSlabReconstructor:
         (allgather)."""
         p = self.params
         n_lines = raw_chunk.numel() // p.n_chan
+        if self.mode == "p2p":
+            row0, _ = self._map
+            self.symm.barrier(channel=0)  # owners finished reading their staging (previous step)
+            check(lib().tf_filter_stage_peers(self.local.fplan.handle, self.local.bplan.handle,
+                                              ctypes.c_void_p(raw_chunk.data_ptr()), n_lines, self.local.i0,
+                                              p.n_rows, self.world, row0, self._dst, self._s()))
+            return
         if self._map is None:
             check(lib().tf_filter(self.local.fplan.handle, ctypes.c_void_p(raw_chunk.data_ptr()),
                                   ctypes.c_void_p(self.send.data_ptr()), n_lines, self.local.i0,
@@ -162,6 +189,9 @@ class ZSlabReconstructor:
     def exchange(self):
         import torch.distributed as dist
 
+        if self.mode == "p2p":  # the stores already landed; wait until every peer's have
+            self.symm.barrier(channel=0)
+            return
         if self.mode == "allgather":
             dist.all_gather_into_tensor(self.gathered.view(-1), self.send, group=self.group)
         else:  # lands directly in this rank's staging buffer

@@ -33,7 +33,7 @@ def _ptr(t):
 class SlabReconstructor:
     def __init__(self, params: AcquisitionParams, dims: VolumeDims, spec: FilterSpec | None = None,
                  i0: float = 1e5, feather_band: int = 32, rows: tuple[int, int] | None = None,
-                 device=None, in_place_filter: bool = False):
+                 device=None, in_place_filter: bool = False, stage=None):
         import torch
 
         self.torch = torch
@@ -48,8 +48,14 @@ class SlabReconstructor:
             self.bplan = bp_plan(params, dims, feather_band)
             self.in_place = in_place_filter
             self._filt = None  # natural-layout filtered rows, only for the unfused path
-            self.stage = torch.empty(self.bplan.stage_bytes(self.k), dtype=torch.uint8,
-                                     device=self.device)
+            need = self.bplan.stage_bytes(self.k)
+            if stage is not None:  # caller-provided (e.g. NVLink-mapped symmetric memory)
+                stage = stage.view(torch.uint8).view(-1)
+                if stage.numel() < need:
+                    raise ValueError(f"staging buffer too small: {stage.numel()} < {need} bytes")
+                self.stage = stage[:need]
+            else:
+                self.stage = torch.empty(need, dtype=torch.uint8, device=self.device)
             self.vol = torch.empty((self.k, dims.ny, dims.nx), dtype=torch.float32,
                                    device=self.device)
 

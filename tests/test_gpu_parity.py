@@ -418,9 +418,9 @@ def test_multi_gpu_zslab_bitwise(F):
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for mode in ("alltoall", "allgather"):
+    for i, mode in enumerate(("alltoall", "allgather", "p2p")):
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-               "--master-addr", "127.0.0.1", "--master-port", str(29500 + (mode == "allgather")),
+               "--master-addr", "127.0.0.1", "--master-port", str(29500 + i),
                os.path.join(root, "tools", "mgpu_check.py"), "--exchange", mode]
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
         print(r.stdout[-2000:], r.stderr[-2000:])

@@ -30,6 +30,7 @@ z = ZSlabReconstructor(p, d, i0=1e5, exchange_mode=args.exchange, device=dev)
 chunk = torch.empty(z.chunk_shape(), device=dev)
 phantom_raw(p, d, chunk, a0=z.a0, a1=z.a1)
 vol = z.run(chunk)
+vol = z.run(chunk)  # a second step exercises the buffer-reuse ordering
 torch.cuda.synchronize()
 k_max = max(e - s for s, e in z.slabs)
 buf = torch.zeros((k_max, n, n), device=dev)
