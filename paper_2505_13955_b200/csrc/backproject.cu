@@ -36,6 +36,8 @@ struct tf_bp_plan {
     double2* d_trig;  // (cos, sin) of k * (span / n_proj), fp64 libm, per angle
     float* d_w;       // feather weights (fp32, as numpy casts them)
     double ext;       // max channel extent of a tile's rays over all angles
+    int* d_tiles;     // FoV-active tile indices, then the inactive ones
+    int n_active, n_inactive;
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
 };
@@ -81,6 +83,8 @@ struct Layout {
 
 struct BPArgs {
     const double2* trig;
+    const int* tiles;  // FoV-active tile indices (persistent launches)
+    int n_active, n_items;
     float* vol;
     int a0, a1, nzb, n_rows, nx, ny, n_chan;
     int x0, x1, y0, y1;
@@ -132,39 +136,74 @@ __device__ __forceinline__ void accumulate_roles(float (&acc)[4][ZT], const floa
 template <class L>
 struct Setup;
 
-template <class L>
+// One work item = one 16x16 tile x one 32-row z-block.  Non-persistent
+// launches map (blockIdx.x, blockIdx.y) -> (tile, z-block) over all tiles
+// and early-out on tiles outside the FoV / requested tile.  Persistent
+// launches (PERSIST) walk a precomputed list of FoV-active tiles, item
+// k of CTA b being b + k*gridDim.x in z-block-major order: the CTAs resident
+// at any moment work on the same z-block at nearly the same angle (every
+// item costs the same), so the angle working set of the staged slab stays
+// L2-resident instead of being re-read from HBM by every tile.
+struct Item {
+    int X0, Y0, zb;
+    int ux0, ux1, uy0, uy1;  // requested-tile clip of this tile
+};
+
+template <bool PERSIST>
+__device__ __forceinline__ Item decode_item(const BPArgs& a, int k) {
+    Item it;
+    int tile;
+    if constexpr (PERSIST) {
+        const int idx = blockIdx.x + k * gridDim.x;
+        it.zb = idx / a.n_active;
+        tile = a.tiles[idx - it.zb * a.n_active];
+    } else {
+        it.zb = blockIdx.y;
+        tile = blockIdx.x;
+    }
+    it.X0 = (tile % a.ntx) * TX;
+    it.Y0 = (tile / a.ntx) * TY;
+    it.ux0 = max(it.X0, a.x0);
+    it.ux1 = min(min(it.X0 + TX, a.nx), a.x1);
+    it.uy0 = max(it.Y0, a.y0);
+    it.uy1 = min(min(it.Y0 + TY, a.ny), a.y1);
+    return it;
+}
+
+template <class L, bool PERSIST>
 __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     bp_kernel(const __grid_constant__ CUtensorMap map, const BPArgs args) {
     constexpr int VX = L::VX_, VY = L::VY_, NT = L::NT_, ZT = L::ZT_;
     constexpr int STAGES = L::STAGES, APS = L::APS;
     extern __shared__ __align__(128) uint8_t smem[];
-    const int tx = blockIdx.x % args.ntx, ty = blockIdx.x / args.ntx, zb = blockIdx.y;
-    const int X0 = tx * TX, Y0 = ty * TY;
 
-    // ---- tile-level early outs (uniform over the CTA, before any barrier)
-    const int xe = min(X0 + TX, args.nx), ye = min(Y0 + TY, args.ny);
-    const int ux0 = max(X0, args.x0), ux1 = min(xe, args.x1);
-    const int uy0 = max(Y0, args.y0), uy1 = min(ye, args.y1);
-    if (ux0 >= ux1 || uy0 >= uy1) return;  // nothing of the requested tile here
-    {
+    int n_items = 1;
+    if constexpr (PERSIST) {
+        n_items = (args.n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+        if (n_items <= 0) return;
+    } else {
+        // ---- tile-level early outs (uniform over the CTA, before any barrier)
+        const Item it = decode_item<false>(args, 0);
+        const int xe = min(it.X0 + TX, args.nx), ye = min(it.Y0 + TY, args.ny);
+        if (it.ux0 >= it.ux1 || it.uy0 >= it.uy1) return;  // nothing of the requested tile here
         // nearest voxel of the tile to the rotation centre decides "all outside"
-        int nxv = (int)fmin(fmax(rint(args.cx), (double)X0), (double)(xe - 1));
-        int nyv = (int)fmin(fmax(rint(args.cy), (double)Y0), (double)(ye - 1));
+        int nxv = (int)fmin(fmax(rint(args.cx), (double)it.X0), (double)(xe - 1));
+        int nyv = (int)fmin(fmax(rint(args.cy), (double)it.Y0), (double)(ye - 1));
         bool all_out = true;
         for (int ddx = -1; ddx <= 1; ++ddx)
             for (int ddy = -1; ddy <= 1; ++ddy) {
-                int xx = min(max(nxv + ddx, X0), xe - 1), yy = min(max(nyv + ddy, Y0), ye - 1);
+                int xx = min(max(nxv + ddx, it.X0), xe - 1), yy = min(max(nyv + ddy, it.Y0), ye - 1);
                 all_out = all_out && outside_fov(xx, yy, args);
             }
         if (all_out) {
             if (args.flags & TF_BP_FINALIZE) {
-                const int nz = min(kZB, args.n_rows - zb * kZB);
+                const int nz = min(kZB, args.n_rows - it.zb * kZB);
                 const size_t plane = (size_t)args.nx * args.ny;
                 for (int i = threadIdx.x; i < TX * TY * nz; i += blockDim.x) {
                     int z = i / (TX * TY), r = i % (TX * TY);
-                    int x = X0 + (r % TX), y = Y0 + (r / TX);
-                    if (x >= ux0 && x < ux1 && y >= uy0 && y < uy1)
-                        args.vol[(size_t)(zb * kZB + z) * plane + (size_t)y * args.nx + x] = 0.f;
+                    int x = it.X0 + (r % TX), y = it.Y0 + (r / TX);
+                    if (x >= it.ux0 && x < it.ux1 && y >= it.uy0 && y < it.uy1)
+                        args.vol[(size_t)(it.zb * kZB + z) * plane + (size_t)y * args.nx + x] = 0.f;
                 }
             }
             return;
@@ -172,8 +211,8 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     }
 
     uint8_t* ring = smem;
-    float4* prm = reinterpret_cast<float4*>(smem + STAGES * APS * args.slot_bytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(prm + STAGES * APS);
+    float4* prm = reinterpret_cast<float4*>(smem + L::RING * args.slot_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(prm + L::RING);
     uint64_t* empty = full + STAGES;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -187,35 +226,46 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     __syncthreads();
 
     const int n_ang = args.a1 - args.a0;
-    const int n_it = (n_ang + APS - 1) / APS;
+    const int G = n_items * n_ang;  // angles this CTA streams, item-major
 
     if (warp == L::NCW) {
         // ================= TMA producer (one thread)
-        if (lane == 0) {
+        if (lane == 0 && G > 0) {
             tma_prefetch_desc(&map);
-            const double dX = (double)X0 - args.cx, dY = (double)Y0 - args.cy;
             const uint32_t box_bytes = (uint32_t)(kZP * 4 * args.W);
-            for (int it = 0; it < n_it; ++it) {
+            int cur_k = -1;
+            double dX = 0.0, dY = 0.0;
+            int zb = 0;
+            for (int it = 0; it * APS < G; ++it) {
                 const int s = it % STAGES;
                 const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
                 mbar_wait(&empty[s], ph ^ 1u);
-                const int kb = args.a0 + it * APS;
-                const int na = min(APS, args.a1 - kb);
-                int c_lo[APS];
+                const int na = min(APS, G - it * APS);
+                int c_lo[APS], row[APS];
                 for (int a = 0; a < na; ++a) {
-                    const double2 cs = args.trig[kb + a];
+                    const int gg = it * APS + a;
+                    const int k = gg / n_ang;
+                    if (k != cur_k) {
+                        const Item item = decode_item<PERSIST>(args, k);
+                        dX = (double)item.X0 - args.cx;
+                        dY = (double)item.Y0 - args.cy;
+                        zb = item.zb;
+                        cur_k = k;
+                    }
+                    const int ang = args.a0 + (gg - k * n_ang);
+                    const double2 cs = args.trig[ang];
                     // t at the tile origin, same operation order as geometry.py:151-153
                     double t0 = __dadd_rn(__dmul_rn(dX, cs.x), __dmul_rn(dY, cs.y));
                     t0 = __dadd_rn(__dmul_rn(t0, args.scale), args.axis);
                     const double B = cs.x * args.scale, C = cs.y * args.scale;
                     const double tmin = t0 + fmin(0.0, B * (TX - 1)) + fmin(0.0, C * (TY - 1));
                     c_lo[a] = (int)floor(tmin);
+                    row[a] = ang * args.nzb + zb;
                     prm[s * APS + a] = make_float4((float)(t0 - (double)c_lo[a]), (float)B, (float)C, 0.f);
                 }
                 mbar_arrive_expect_tx(&full[s], box_bytes * (uint32_t)na);
                 for (int a = 0; a < na; ++a)
-                    tma_load_3d(ring + (size_t)(s * APS + a) * args.slot_bytes, &map, &full[s], 0, c_lo[a],
-                                (kb + a) * args.nzb + zb);
+                    tma_load_3d(ring + (size_t)(s * APS + a) * args.slot_bytes, &map, &full[s], 0, c_lo[a], row[a]);
             }
         }
         return;
@@ -223,7 +273,7 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
 
     // ================= consumers
     // z-group per warp (all lanes of a warp read the same 16-B column of a
-    // tap row); a warp covers 8x4 blocks, each 8-lane LDS.128 phase a 4x2
+    // tap row); a warp covers 8x4 blocks, each 8-lane LDS.128 phase a PWxPH
     // patch, so a phase's tap rows stay within 8 consecutive channels ->
     // distinct bank quads (row pitch 144 B = 9 quads).
     const int zg = threadIdx.x / L::COLS;
@@ -234,25 +284,47 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     const int by = (wg / L::WX) * 4 + (q / QW) * L::PH + (i8 / L::PW);
     const int dx0 = bx * VX, dy0 = by * VY;
     const size_t plane = (size_t)args.nx * args.ny;
-    const int zrow0 = zb * kZB + zg * ZT;                 // first volume row of this thread
-    const int nz = min(ZT, args.n_rows - zrow0);          // may be <= 0 for a ragged last block
 
     float acc[VX * VY][ZT];
+    Item item;
+    int zrow0 = 0, nz = 0;
+    auto item_begin = [&](int k) {
+        item = decode_item<PERSIST>(args, k);
+        zrow0 = item.zb * kZB + zg * ZT;          // first volume row of this thread
+        nz = min(ZT, args.n_rows - zrow0);        // may be <= 0 for a ragged last block
 #pragma unroll
-    for (int v = 0; v < VX * VY; ++v)
+        for (int v = 0; v < VX * VY; ++v)
 #pragma unroll
-        for (int j = 0; j < ZT; ++j) acc[v][j] = 0.f;
-    if (args.flags & TF_BP_ACCUMULATE) {
+            for (int j = 0; j < ZT; ++j) acc[v][j] = 0.f;
+        if (args.flags & TF_BP_ACCUMULATE) {
 #pragma unroll
-        for (int v = 0; v < VX * VY; ++v) {
-            const int x = X0 + dx0 + (v % VX), y = Y0 + dy0 + (v / VX);
-            if (x >= ux0 && x < ux1 && y >= uy0 && y < uy1) {
+            for (int v = 0; v < VX * VY; ++v) {
+                const int x = item.X0 + dx0 + (v % VX), y = item.Y0 + dy0 + (v / VX);
+                if (x >= item.ux0 && x < item.ux1 && y >= item.uy0 && y < item.uy1) {
 #pragma unroll
-                for (int j = 0; j < ZT; ++j)
-                    if (j < nz) acc[v][j] = args.vol[(size_t)(zrow0 + j) * plane + (size_t)y * args.nx + x];
+                    for (int j = 0; j < ZT; ++j)
+                        if (j < nz) acc[v][j] = args.vol[(size_t)(zrow0 + j) * plane + (size_t)y * args.nx + x];
+                }
             }
         }
-    }
+    };
+    auto item_end = [&]() {
+#pragma unroll
+        for (int v = 0; v < VX * VY; ++v) {
+            const int x = item.X0 + dx0 + (v % VX), y = item.Y0 + dy0 + (v / VX);
+            if (!(x >= item.ux0 && x < item.ux1 && y >= item.uy0 && y < item.uy1)) continue;
+            float scale = 1.f;
+            bool zero = false;
+            if (args.flags & TF_BP_FINALIZE) {
+                scale = args.angle_wf;
+                zero = outside_fov(x, y, args);
+            }
+            float* out = args.vol + (size_t)zrow0 * plane + (size_t)y * args.nx + x;
+#pragma unroll
+            for (int j = 0; j < ZT; ++j)
+                if (j < nz) out[(size_t)j * plane] = zero ? 0.f : acc[v][j] * scale;
+        }
+    };
 
     // per-angle setup: detector coordinates -> tap row + interpolation weights
     const uint8_t* ring_z = ring + zg * ZT * 4;
@@ -374,31 +446,45 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
         if (lane == 0) mbar_arrive(&empty[(g / APS) % STAGES]);
     };
 
+    if (n_ang == 0) {  // empty angle range: FINALIZE still writes (zeros / scaled partials)
+        for (int k = 0; k < n_items; ++k) {
+            item_begin(k);
+            item_end();
+        }
+        return;
+    }
     if constexpr (!L::PIPE) {
-        for (int g = 0; g < n_ang; ++g) {
+        for (int g = 0; g < G; ++g) {
+            if (g % n_ang == 0) item_begin(g / n_ang);
             if (g % APS == 0) wait_full(g);
             const float* p0;
             float w[VX * VY][NT];
             int cls;
             setup(g, p0, w, cls);
             accumulate(p0, w, cls);
-            if (g % APS == APS - 1 || g == n_ang - 1) release(g);
+            if (g % APS == APS - 1 || g == G - 1) release(g);
+            if (g % n_ang == n_ang - 1) item_end();
         }
-    } else if (n_ang > 0) {
+    } else {
+        item_begin(0);
         wait_full(0);
         const float* p0;
         float w[VX * VY][NT];
         int cls;
         setup(0, p0, w, cls);
-        for (int g = 0; g < n_ang; ++g) {
+        for (int g = 0; g < G; ++g) {
             const int gn = g + 1;
-            if (gn < n_ang && gn % APS == 0) wait_full(gn);
+            if (gn < G && gn % APS == 0) wait_full(gn);
             const float* q0;
             float wn[VX * VY][NT];
             int clsn;
-            setup(min(gn, n_ang - 1), q0, wn, clsn);  // independent of this angle's FMAs
+            setup(min(gn, G - 1), q0, wn, clsn);  // independent of this angle's FMAs
             accumulate(p0, w, cls);
-            if (gn % APS == 0 || gn == n_ang) release(g);
+            if (gn % APS == 0 || gn == G) release(g);
+            if (gn % n_ang == 0) {
+                item_end();
+                if (gn < G) item_begin(gn / n_ang);
+            }
             p0 = q0;
             cls = clsn;
 #pragma unroll
@@ -407,21 +493,22 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
                 for (int j = 0; j < NT; ++j) w[v][j] = wn[v][j];
         }
     }
+}
 
-#pragma unroll
-    for (int v = 0; v < VX * VY; ++v) {
-        const int x = X0 + dx0 + (v % VX), y = Y0 + dy0 + (v / VX);
-        if (!(x >= ux0 && x < ux1 && y >= uy0 && y < uy1)) continue;
-        float scale = 1.f;
-        bool zero = false;
-        if (args.flags & TF_BP_FINALIZE) {
-            scale = args.angle_wf;
-            zero = outside_fov(x, y, args);
-        }
-        float* out = args.vol + (size_t)zrow0 * plane + (size_t)y * args.nx + x;
-#pragma unroll
-        for (int j = 0; j < ZT; ++j)
-            if (j < nz) out[(size_t)j * plane] = zero ? 0.f : acc[v][j] * scale;
+// Zero the volume columns of FoV-inactive tiles (the persistent kernel never
+// visits them).
+__global__ void zero_tiles_kernel(float* __restrict__ vol, const int* __restrict__ tiles, int n_tiles, int ntx, int nx,
+                                  int ny, int n_rows) {
+    const size_t plane = (size_t)nx * ny;
+    const long long total = (long long)n_tiles * n_rows * TY;
+    for (long long i = blockIdx.x * (long long)(blockDim.x / TX) + threadIdx.x / TX; i < total;
+         i += (long long)gridDim.x * (blockDim.x / TX)) {
+        const int yy = (int)(i % TY);
+        const long long rz = i / TY;
+        const int z = (int)(rz % n_rows);
+        const int tile = tiles[rz / n_rows];
+        const int x = (tile % ntx) * TX + (threadIdx.x % TX), y = (tile / ntx) * TY + yy;
+        if (x < nx && y < ny) vol[(size_t)z * plane + (size_t)y * nx + x] = 0.f;
     }
 }
 
@@ -516,11 +603,29 @@ int select_variant(const tf_bp_plan* p, int flags) {
     return variant;
 }
 
+bool persistent_enabled() {
+    static int v = [] {
+        const char* e = getenv("TF_BP_PERSIST");  // benchmarking knob: 0 disables the work-list schedule
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 template <class L>
-int launch_bp(const CUtensorMap& map, const BPArgs& a, dim3 grid, void* stream) {
+int launch_bp(const CUtensorMap& map, const BPArgs& a, dim3 grid, void* stream, bool persist) {
     const int smem = bp_smem_bytes<L>(a.slot_bytes);
-    TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    bp_kernel<L><<<grid, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
+    if (persist) {
+        TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int per_sm = 0, dev = 0, sms = 0;
+        TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bp_kernel<L, true>, L::NTHREADS, smem));
+        TF_CUDA_TRY(cudaGetDevice(&dev));
+        TF_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int g = std::max(1, std::min(a.n_items, std::max(1, per_sm) * sms));
+        bp_kernel<L, true><<<g, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
+    } else {
+        TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        bp_kernel<L, false><<<grid, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
+    }
     return TF_OK;
 }
 }  // namespace
@@ -590,6 +695,29 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     p->sc2 = p->scale * p->scale;
     const double step = g->angle_span / g->n_proj;
     p->angle_wf = (float)step;
+    // tiles with any voxel inside the FoV (same fp64 test as the kernel's early-out)
+    const int ntx = (g->nx + TX - 1) / TX, nty = (g->ny + TY - 1) / TY;
+    std::vector<int> act, inact;
+    for (int t = 0; t < ntx * nty; ++t) {
+        const int X0 = (t % ntx) * TX, Y0 = (t / ntx) * TY;
+        const int xe = std::min(X0 + TX, g->nx), ye = std::min(Y0 + TY, g->ny);
+        const int nxv = (int)std::min(std::max(std::nearbyint(p->cx), (double)X0), (double)(xe - 1));
+        const int nyv = (int)std::min(std::max(std::nearbyint(p->cy), (double)Y0), (double)(ye - 1));
+        bool all_out = true;
+        for (int ddx = -1; ddx <= 1; ++ddx)
+            for (int ddy = -1; ddy <= 1; ++ddy) {
+                const int xx = std::min(std::max(nxv + ddx, X0), xe - 1), yy = std::min(std::max(nyv + ddy, Y0), ye - 1);
+                volatile double dx = (double)xx - p->cx, dy = (double)yy - p->cy;
+                volatile double s2 = dx * dx;
+                volatile double t2 = dy * dy;
+                volatile double rr = (s2 + t2) * p->sc2;
+                all_out = all_out && (rr > p->R2);
+            }
+        (all_out ? inact : act).push_back(t);
+    }
+    p->n_active = (int)act.size();
+    p->n_inactive = (int)inact.size();
+    act.insert(act.end(), inact.begin(), inact.end());
     std::vector<double2> trig(g->n_proj);
     for (int k = 0; k < g->n_proj; ++k) {  // theta_k = k * (span / n_proj), geometry.py:69-70
         const double th = (double)k * step;
@@ -598,6 +726,9 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     std::vector<float> wf(g->n_chan);
     for (int i = 0; i < g->n_chan; ++i) wf[i] = (float)w[i];
     cudaError_t e = cudaMalloc(&p->d_trig, sizeof(double2) * g->n_proj);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_tiles, sizeof(int) * std::max<size_t>(1, act.size()));
+    if (e == cudaSuccess && !act.empty())
+        e = cudaMemcpy(p->d_tiles, act.data(), sizeof(int) * act.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_w, sizeof(float) * g->n_chan);
     if (e == cudaSuccess)
         e = cudaMemcpy(p->d_trig, trig.data(), sizeof(double2) * g->n_proj, cudaMemcpyHostToDevice);
@@ -614,6 +745,7 @@ extern "C" int tf_bp_plan_destroy(tf_bp_plan* p) {
     if (!p) return TF_OK;
     cudaFree(p->d_trig);
     cudaFree(p->d_w);
+    cudaFree(p->d_tiles);
     delete p;
     return TF_OK;
 }
@@ -698,18 +830,32 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     a.angle_wf = p->angle_wf;
     const int nty = (g.ny + TY - 1) / TY;
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)nzb);
+    // full-volume calls walk the FoV-active tile list with persistent CTAs
+    const bool persist = persistent_enabled() && x0 == 0 && x1 == g.nx && y0 == 0 && y1 == g.ny;
+    a.tiles = p->d_tiles;
+    a.n_active = p->n_active;
+    a.n_items = p->n_active * nzb;
+    if (persist && !(flags & TF_BP_ACCUMULATE) && p->n_inactive > 0) {
+        const long long work = (long long)p->n_inactive * n_rows * TY;
+        const int blocks = (int)std::min<long long>((work + 15) / 16, 148LL * 16);
+        zero_tiles_kernel<<<blocks, 256, 0, as_stream(stream)>>>(vol, p->d_tiles + p->n_active, p->n_inactive, a.ntx,
+                                                                g.nx, g.ny, n_rows);
+        int zs = check_launch("zero_tiles_kernel");
+        if (zs) return zs;
+    }
+    if (persist && a.n_items == 0) return TF_OK;
     int st;
     switch (variant) {
-        case 0: st = launch_bp<V1Cfg>(map, a, grid, stream); break;
-        case 1: st = launch_bp<V4Cfg1>(map, a, grid, stream); break;
-        case 2: st = launch_bp<V4Cfg2>(map, a, grid, stream); break;
-        case 3: st = launch_bp<V4Cfg3>(map, a, grid, stream); break;
-        case 4: st = launch_bp<V4Cfg4>(map, a, grid, stream); break;
-        case 5: st = launch_bp<P3Cfg5>(map, a, grid, stream); break;
-        case 6: st = launch_bp<P3Cfg6>(map, a, grid, stream); break;
-        case 7: st = launch_bp<P3Cfg7>(map, a, grid, stream); break;
-        case 8: st = launch_bp<Q4Cfg8>(map, a, grid, stream); break;
-        default: st = launch_bp<Q4Cfg9>(map, a, grid, stream); break;
+        case 0: st = launch_bp<V1Cfg>(map, a, grid, stream, persist); break;
+        case 1: st = launch_bp<V4Cfg1>(map, a, grid, stream, persist); break;
+        case 2: st = launch_bp<V4Cfg2>(map, a, grid, stream, persist); break;
+        case 3: st = launch_bp<V4Cfg3>(map, a, grid, stream, persist); break;
+        case 4: st = launch_bp<V4Cfg4>(map, a, grid, stream, persist); break;
+        case 5: st = launch_bp<P3Cfg5>(map, a, grid, stream, persist); break;
+        case 6: st = launch_bp<P3Cfg6>(map, a, grid, stream, persist); break;
+        case 7: st = launch_bp<P3Cfg7>(map, a, grid, stream, persist); break;
+        case 8: st = launch_bp<Q4Cfg8>(map, a, grid, stream, persist); break;
+        default: st = launch_bp<Q4Cfg9>(map, a, grid, stream, persist); break;
     }
     if (st) return st;
     return check_launch("bp_kernel");
