@@ -38,6 +38,8 @@ struct tf_bp_plan {
     double ext;       // max channel extent of a tile's rays over all angles
     int* d_tiles;     // FoV-active tile indices, then the inactive ones
     int n_active, n_inactive;
+    int* d_counters;  // persistent-launch work counters (a pool: concurrent launches on
+    unsigned seq;     // different streams take different counters)
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
 };
@@ -84,6 +86,7 @@ struct Layout {
 struct BPArgs {
     const double2* trig;
     const int* tiles;  // FoV-active tile indices (persistent launches)
+    int* counter;      // work counter (persistent launches), zeroed before the launch
     int n_active, n_items;
     float* vol;
     int a0, a1, nzb, n_rows, nx, ny, n_chan;
@@ -150,11 +153,10 @@ struct Item {
 };
 
 template <bool PERSIST>
-__device__ __forceinline__ Item decode_item(const BPArgs& a, int k) {
+__device__ __forceinline__ Item decode_item(const BPArgs& a, int idx) {
     Item it;
     int tile;
     if constexpr (PERSIST) {
-        const int idx = blockIdx.x + k * gridDim.x;
         it.zb = idx / a.n_active;
         tile = a.tiles[idx - it.zb * a.n_active];
     } else {
@@ -177,11 +179,7 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     constexpr int STAGES = L::STAGES, APS = L::APS;
     extern __shared__ __align__(128) uint8_t smem[];
 
-    int n_items = 1;
-    if constexpr (PERSIST) {
-        n_items = (args.n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-        if (n_items <= 0) return;
-    } else {
+    if constexpr (!PERSIST) {
         // ---- tile-level early outs (uniform over the CTA, before any barrier)
         const Item it = decode_item<false>(args, 0);
         const int xe = min(it.X0 + TX, args.nx), ye = min(it.Y0 + TY, args.ny);
@@ -226,33 +224,45 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     __syncthreads();
 
     const int n_ang = args.a1 - args.a0;
-    const int G = n_items * n_ang;  // angles this CTA streams, item-major
+    // prm[slot].w tags the first angle of every item with its index; -1 ends the stream
+    constexpr int kEnd = -1, kCont = -2;
 
     if (warp == L::NCW) {
-        // ================= TMA producer (one thread)
-        if (lane == 0 && G > 0) {
+        // ================= TMA producer (one thread): fetches items (an atomic
+        // work counter when persistent) and streams their angles back to back
+        if (lane == 0 && n_ang > 0) {
             tma_prefetch_desc(&map);
             const uint32_t box_bytes = (uint32_t)(kZP * 4 * args.W);
-            int cur_k = -1;
+            int a_in = n_ang;  // angle within the current item (n_ang: fetch a new one)
+            int fetched = 0;
             double dX = 0.0, dY = 0.0;
-            int zb = 0;
-            for (int it = 0; it * APS < G; ++it) {
+            int zb = 0, idx = 0;
+            bool done = false;
+            for (int it = 0; !done; ++it) {
                 const int s = it % STAGES;
                 const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
                 mbar_wait(&empty[s], ph ^ 1u);
-                const int na = min(APS, G - it * APS);
+                int na = 0;
                 int c_lo[APS], row[APS];
-                for (int a = 0; a < na; ++a) {
-                    const int gg = it * APS + a;
-                    const int k = gg / n_ang;
-                    if (k != cur_k) {
-                        const Item item = decode_item<PERSIST>(args, k);
+                for (int a = 0; a < APS; ++a) {
+                    int tag = kCont;
+                    if (a_in == n_ang) {
+                        if constexpr (PERSIST) idx = atomicAdd(args.counter, 1);
+                        else idx = fetched;
+                        ++fetched;
+                        if (idx >= (PERSIST ? args.n_items : 1)) {
+                            prm[s * APS + a] = make_float4(0.f, 0.f, 0.f, __int_as_float(kEnd));
+                            done = true;
+                            break;
+                        }
+                        const Item item = decode_item<PERSIST>(args, idx);
                         dX = (double)item.X0 - args.cx;
                         dY = (double)item.Y0 - args.cy;
                         zb = item.zb;
-                        cur_k = k;
+                        a_in = 0;
+                        tag = idx;
                     }
-                    const int ang = args.a0 + (gg - k * n_ang);
+                    const int ang = args.a0 + a_in;
                     const double2 cs = args.trig[ang];
                     // t at the tile origin, same operation order as geometry.py:151-153
                     double t0 = __dadd_rn(__dmul_rn(dX, cs.x), __dmul_rn(dY, cs.y));
@@ -261,7 +271,9 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
                     const double tmin = t0 + fmin(0.0, B * (TX - 1)) + fmin(0.0, C * (TY - 1));
                     c_lo[a] = (int)floor(tmin);
                     row[a] = ang * args.nzb + zb;
-                    prm[s * APS + a] = make_float4((float)(t0 - (double)c_lo[a]), (float)B, (float)C, 0.f);
+                    prm[s * APS + a] = make_float4((float)(t0 - (double)c_lo[a]), (float)B, (float)C, __int_as_float(tag));
+                    ++na;
+                    ++a_in;
                 }
                 mbar_arrive_expect_tx(&full[s], box_bytes * (uint32_t)na);
                 for (int a = 0; a < na; ++a)
@@ -288,8 +300,8 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     float acc[VX * VY][ZT];
     Item item;
     int zrow0 = 0, nz = 0;
-    auto item_begin = [&](int k) {
-        item = decode_item<PERSIST>(args, k);
+    auto item_begin = [&](int idx) {
+        item = decode_item<PERSIST>(args, idx);
         zrow0 = item.zb * kZB + zg * ZT;          // first volume row of this thread
         nz = min(ZT, args.n_rows - zrow0);        // may be <= 0 for a ragged last block
 #pragma unroll
@@ -446,52 +458,51 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
         if (lane == 0) mbar_arrive(&empty[(g / APS) % STAGES]);
     };
 
-    if (n_ang == 0) {  // empty angle range: FINALIZE still writes (zeros / scaled partials)
-        for (int k = 0; k < n_items; ++k) {
-            item_begin(k);
-            item_end();
-        }
+    if (n_ang == 0) {  // empty angle range (non-persistent launches only): FINALIZE still writes
+        item_begin(0);
+        item_end();
         return;
     }
-    if constexpr (!L::PIPE) {
-        for (int g = 0; g < G; ++g) {
-            if (g % n_ang == 0) item_begin(g / n_ang);
-            if (g % APS == 0) wait_full(g);
+    for (int gg = 0;; gg += n_ang) {
+        if (gg % APS == 0) wait_full(gg);
+        const int id = __float_as_int(prm[gg & (L::RING - 1)].w);
+        if (id == kEnd) break;  // same for every consumer thread
+        item_begin(id);
+        if constexpr (!L::PIPE) {
+            for (int a = 0; a < n_ang; ++a) {
+                const int g = gg + a;
+                if (a > 0 && g % APS == 0) wait_full(g);
+                const float* p0;
+                float w[VX * VY][NT];
+                int cls;
+                setup(g, p0, w, cls);
+                accumulate(p0, w, cls);
+                if (g % APS == APS - 1) release(g);
+            }
+        } else {
             const float* p0;
             float w[VX * VY][NT];
             int cls;
-            setup(g, p0, w, cls);
-            accumulate(p0, w, cls);
-            if (g % APS == APS - 1 || g == G - 1) release(g);
-            if (g % n_ang == n_ang - 1) item_end();
-        }
-    } else {
-        item_begin(0);
-        wait_full(0);
-        const float* p0;
-        float w[VX * VY][NT];
-        int cls;
-        setup(0, p0, w, cls);
-        for (int g = 0; g < G; ++g) {
-            const int gn = g + 1;
-            if (gn < G && gn % APS == 0) wait_full(gn);
-            const float* q0;
-            float wn[VX * VY][NT];
-            int clsn;
-            setup(min(gn, G - 1), q0, wn, clsn);  // independent of this angle's FMAs
-            accumulate(p0, w, cls);
-            if (gn % APS == 0 || gn == G) release(g);
-            if (gn % n_ang == 0) {
-                item_end();
-                if (gn < G) item_begin(gn / n_ang);
+            setup(gg, p0, w, cls);
+            for (int a = 0; a < n_ang; ++a) {
+                const int g = gg + a, gn = g + 1;
+                const bool more = a + 1 < n_ang;
+                if (more && gn % APS == 0) wait_full(gn);
+                const float* q0;
+                float wn[VX * VY][NT];
+                int clsn;
+                setup(more ? gn : g, q0, wn, clsn);  // independent of this angle's FMAs
+                accumulate(p0, w, cls);
+                if (g % APS == APS - 1) release(g);
+                p0 = q0;
+                cls = clsn;
+#pragma unroll
+                for (int v = 0; v < VX * VY; ++v)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) w[v][j] = wn[v][j];
             }
-            p0 = q0;
-            cls = clsn;
-#pragma unroll
-            for (int v = 0; v < VX * VY; ++v)
-#pragma unroll
-                for (int j = 0; j < NT; ++j) w[v][j] = wn[v][j];
         }
+        item_end();
     }
 }
 
@@ -715,6 +726,15 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
             }
         (all_out ? inact : act).push_back(t);
     }
+    // Morton (Z-order) tile order: the CTAs resident at one moment (consecutive
+    // list entries) cover a compact patch, so their per-angle channel windows
+    // overlap and the patch's angle working set is small enough for L2
+    auto morton = [&](int t) {
+        unsigned x = (unsigned)(t % ntx), y = (unsigned)(t / ntx), m = 0;
+        for (int b = 0; b < 16; ++b) m |= ((x >> b) & 1u) << (2 * b) | ((y >> b) & 1u) << (2 * b + 1);
+        return m;
+    };
+    std::stable_sort(act.begin(), act.end(), [&](int a, int b) { return morton(a) < morton(b); });
     p->n_active = (int)act.size();
     p->n_inactive = (int)inact.size();
     act.insert(act.end(), inact.begin(), inact.end());
@@ -727,6 +747,7 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     for (int i = 0; i < g->n_chan; ++i) wf[i] = (float)w[i];
     cudaError_t e = cudaMalloc(&p->d_trig, sizeof(double2) * g->n_proj);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_tiles, sizeof(int) * std::max<size_t>(1, act.size()));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_counters, sizeof(int) * 64);
     if (e == cudaSuccess && !act.empty())
         e = cudaMemcpy(p->d_tiles, act.data(), sizeof(int) * act.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_w, sizeof(float) * g->n_chan);
@@ -746,6 +767,7 @@ extern "C" int tf_bp_plan_destroy(tf_bp_plan* p) {
     cudaFree(p->d_trig);
     cudaFree(p->d_w);
     cudaFree(p->d_tiles);
+    cudaFree(p->d_counters);
     delete p;
     return TF_OK;
 }
@@ -831,10 +853,15 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     const int nty = (g.ny + TY - 1) / TY;
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)nzb);
     // full-volume calls walk the FoV-active tile list with persistent CTAs
-    const bool persist = persistent_enabled() && x0 == 0 && x1 == g.nx && y0 == 0 && y1 == g.ny;
+    const bool persist = persistent_enabled() && a0 < a1 && x0 == 0 && x1 == g.nx && y0 == 0 && y1 == g.ny;
     a.tiles = p->d_tiles;
     a.n_active = p->n_active;
     a.n_items = p->n_active * nzb;
+    if (persist) {
+        const unsigned slot = __atomic_fetch_add(&const_cast<tf_bp_plan*>(p)->seq, 1u, __ATOMIC_RELAXED) % 64u;
+        a.counter = p->d_counters + slot;
+        TF_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(int), as_stream(stream)));
+    }
     if (persist && !(flags & TF_BP_ACCUMULATE) && p->n_inactive > 0) {
         const long long work = (long long)p->n_inactive * n_rows * TY;
         const int blocks = (int)std::min<long long>((work + 15) / 16, 148LL * 16);
