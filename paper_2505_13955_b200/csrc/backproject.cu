@@ -36,10 +36,7 @@ struct tf_bp_plan {
     double2* d_trig;  // (cos, sin) of k * (span / n_proj), fp64 libm, per angle
     float* d_w;       // feather weights (fp32, as numpy casts them)
     double ext;       // max channel extent of a tile's rays over all angles
-    int* d_tiles;     // FoV-active tile indices, then the inactive ones
-    int n_active, n_inactive;
-    int* d_counters;  // persistent-launch work counters (a pool: concurrent launches on
-    unsigned seq;     // different streams take different counters)
+    int* d_order;     // launch order of the tiles (Morton, FoV-active first)
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
 };
@@ -85,9 +82,7 @@ struct Layout {
 
 struct BPArgs {
     const double2* trig;
-    const int* tiles;  // FoV-active tile indices (persistent launches)
-    int* counter;      // work counter (persistent launches), zeroed before the launch
-    int n_active, n_items;
+    const int* order;  // blockIdx.x -> tile index (Morton order, FoV-active tiles first)
     float* vol;
     int a0, a1, nzb, n_rows, nx, ny, n_chan;
     int x0, x1, y0, y1;
@@ -139,69 +134,44 @@ __device__ __forceinline__ void accumulate_roles(float (&acc)[4][ZT], const floa
 template <class L>
 struct Setup;
 
-// One work item = one 16x16 tile x one 32-row z-block.  Non-persistent
-// launches map (blockIdx.x, blockIdx.y) -> (tile, z-block) over all tiles
-// and early-out on tiles outside the FoV / requested tile.  Persistent
-// launches (PERSIST) walk a precomputed list of FoV-active tiles, item
-// k of CTA b being b + k*gridDim.x in z-block-major order: the CTAs resident
-// at any moment work on the same z-block at nearly the same angle (every
-// item costs the same), so the angle working set of the staged slab stays
-// L2-resident instead of being re-read from HBM by every tile.
-struct Item {
-    int X0, Y0, zb;
-    int ux0, ux1, uy0, uy1;  // requested-tile clip of this tile
-};
-
-template <bool PERSIST>
-__device__ __forceinline__ Item decode_item(const BPArgs& a, int idx) {
-    Item it;
-    int tile;
-    if constexpr (PERSIST) {
-        it.zb = idx / a.n_active;
-        tile = a.tiles[idx - it.zb * a.n_active];
-    } else {
-        it.zb = blockIdx.y;
-        tile = blockIdx.x;
-    }
-    it.X0 = (tile % a.ntx) * TX;
-    it.Y0 = (tile / a.ntx) * TY;
-    it.ux0 = max(it.X0, a.x0);
-    it.ux1 = min(min(it.X0 + TX, a.nx), a.x1);
-    it.uy0 = max(it.Y0, a.y0);
-    it.uy1 = min(min(it.Y0 + TY, a.ny), a.y1);
-    return it;
-}
-
-template <class L, bool PERSIST>
+template <class L>
 __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     bp_kernel(const __grid_constant__ CUtensorMap map, const BPArgs args) {
     constexpr int VX = L::VX_, VY = L::VY_, NT = L::NT_, ZT = L::ZT_;
     constexpr int STAGES = L::STAGES, APS = L::APS;
     extern __shared__ __align__(128) uint8_t smem[];
+    // CTAs launch in blockIdx order and the resident set is a sliding window of
+    // ~3 x 148 consecutive entries: a Morton order makes that window a compact
+    // patch whose channel windows overlap, so the z-block's angle working set
+    // stays in L2 instead of being re-read from HBM tile by tile.
+    const int tile = args.order ? args.order[blockIdx.x] : (int)blockIdx.x;
+    const int tx = tile % args.ntx, ty = tile / args.ntx, zb = blockIdx.y;
+    const int X0 = tx * TX, Y0 = ty * TY;
 
-    if constexpr (!PERSIST) {
-        // ---- tile-level early outs (uniform over the CTA, before any barrier)
-        const Item it = decode_item<false>(args, 0);
-        const int xe = min(it.X0 + TX, args.nx), ye = min(it.Y0 + TY, args.ny);
-        if (it.ux0 >= it.ux1 || it.uy0 >= it.uy1) return;  // nothing of the requested tile here
+    // ---- tile-level early outs (uniform over the CTA, before any barrier)
+    const int xe = min(X0 + TX, args.nx), ye = min(Y0 + TY, args.ny);
+    const int ux0 = max(X0, args.x0), ux1 = min(xe, args.x1);
+    const int uy0 = max(Y0, args.y0), uy1 = min(ye, args.y1);
+    if (ux0 >= ux1 || uy0 >= uy1) return;  // nothing of the requested tile here
+    {
         // nearest voxel of the tile to the rotation centre decides "all outside"
-        int nxv = (int)fmin(fmax(rint(args.cx), (double)it.X0), (double)(xe - 1));
-        int nyv = (int)fmin(fmax(rint(args.cy), (double)it.Y0), (double)(ye - 1));
+        int nxv = (int)fmin(fmax(rint(args.cx), (double)X0), (double)(xe - 1));
+        int nyv = (int)fmin(fmax(rint(args.cy), (double)Y0), (double)(ye - 1));
         bool all_out = true;
         for (int ddx = -1; ddx <= 1; ++ddx)
             for (int ddy = -1; ddy <= 1; ++ddy) {
-                int xx = min(max(nxv + ddx, it.X0), xe - 1), yy = min(max(nyv + ddy, it.Y0), ye - 1);
+                int xx = min(max(nxv + ddx, X0), xe - 1), yy = min(max(nyv + ddy, Y0), ye - 1);
                 all_out = all_out && outside_fov(xx, yy, args);
             }
         if (all_out) {
             if (args.flags & TF_BP_FINALIZE) {
-                const int nz = min(kZB, args.n_rows - it.zb * kZB);
+                const int nz = min(kZB, args.n_rows - zb * kZB);
                 const size_t plane = (size_t)args.nx * args.ny;
                 for (int i = threadIdx.x; i < TX * TY * nz; i += blockDim.x) {
                     int z = i / (TX * TY), r = i % (TX * TY);
-                    int x = it.X0 + (r % TX), y = it.Y0 + (r / TX);
-                    if (x >= it.ux0 && x < it.ux1 && y >= it.uy0 && y < it.uy1)
-                        args.vol[(size_t)(it.zb * kZB + z) * plane + (size_t)y * args.nx + x] = 0.f;
+                    int x = X0 + (r % TX), y = Y0 + (r / TX);
+                    if (x >= ux0 && x < ux1 && y >= uy0 && y < uy1)
+                        args.vol[(size_t)(zb * kZB + z) * plane + (size_t)y * args.nx + x] = 0.f;
                 }
             }
             return;
@@ -209,8 +179,8 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     }
 
     uint8_t* ring = smem;
-    float4* prm = reinterpret_cast<float4*>(smem + L::RING * args.slot_bytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(prm + L::RING);
+    float4* prm = reinterpret_cast<float4*>(smem + STAGES * APS * args.slot_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(prm + STAGES * APS);
     uint64_t* empty = full + STAGES;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -224,60 +194,35 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     __syncthreads();
 
     const int n_ang = args.a1 - args.a0;
-    // prm[slot].w tags the first angle of every item with its index; -1 ends the stream
-    constexpr int kEnd = -1, kCont = -2;
+    const int n_it = (n_ang + APS - 1) / APS;
 
     if (warp == L::NCW) {
-        // ================= TMA producer (one thread): fetches items (an atomic
-        // work counter when persistent) and streams their angles back to back
-        if (lane == 0 && n_ang > 0) {
+        // ================= TMA producer (one thread)
+        if (lane == 0) {
             tma_prefetch_desc(&map);
+            const double dX = (double)X0 - args.cx, dY = (double)Y0 - args.cy;
             const uint32_t box_bytes = (uint32_t)(kZP * 4 * args.W);
-            int a_in = n_ang;  // angle within the current item (n_ang: fetch a new one)
-            int fetched = 0;
-            double dX = 0.0, dY = 0.0;
-            int zb = 0, idx = 0;
-            bool done = false;
-            for (int it = 0; !done; ++it) {
+            for (int it = 0; it < n_it; ++it) {
                 const int s = it % STAGES;
                 const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
                 mbar_wait(&empty[s], ph ^ 1u);
-                int na = 0;
-                int c_lo[APS], row[APS];
-                for (int a = 0; a < APS; ++a) {
-                    int tag = kCont;
-                    if (a_in == n_ang) {
-                        if constexpr (PERSIST) idx = atomicAdd(args.counter, 1);
-                        else idx = fetched;
-                        ++fetched;
-                        if (idx >= (PERSIST ? args.n_items : 1)) {
-                            prm[s * APS + a] = make_float4(0.f, 0.f, 0.f, __int_as_float(kEnd));
-                            done = true;
-                            break;
-                        }
-                        const Item item = decode_item<PERSIST>(args, idx);
-                        dX = (double)item.X0 - args.cx;
-                        dY = (double)item.Y0 - args.cy;
-                        zb = item.zb;
-                        a_in = 0;
-                        tag = idx;
-                    }
-                    const int ang = args.a0 + a_in;
-                    const double2 cs = args.trig[ang];
+                const int kb = args.a0 + it * APS;
+                const int na = min(APS, args.a1 - kb);
+                int c_lo[APS];
+                for (int a = 0; a < na; ++a) {
+                    const double2 cs = args.trig[kb + a];
                     // t at the tile origin, same operation order as geometry.py:151-153
                     double t0 = __dadd_rn(__dmul_rn(dX, cs.x), __dmul_rn(dY, cs.y));
                     t0 = __dadd_rn(__dmul_rn(t0, args.scale), args.axis);
                     const double B = cs.x * args.scale, C = cs.y * args.scale;
                     const double tmin = t0 + fmin(0.0, B * (TX - 1)) + fmin(0.0, C * (TY - 1));
                     c_lo[a] = (int)floor(tmin);
-                    row[a] = ang * args.nzb + zb;
-                    prm[s * APS + a] = make_float4((float)(t0 - (double)c_lo[a]), (float)B, (float)C, __int_as_float(tag));
-                    ++na;
-                    ++a_in;
+                    prm[s * APS + a] = make_float4((float)(t0 - (double)c_lo[a]), (float)B, (float)C, 0.f);
                 }
                 mbar_arrive_expect_tx(&full[s], box_bytes * (uint32_t)na);
                 for (int a = 0; a < na; ++a)
-                    tma_load_3d(ring + (size_t)(s * APS + a) * args.slot_bytes, &map, &full[s], 0, c_lo[a], row[a]);
+                    tma_load_3d(ring + (size_t)(s * APS + a) * args.slot_bytes, &map, &full[s], 0, c_lo[a],
+                                (kb + a) * args.nzb + zb);
             }
         }
         return;
@@ -285,7 +230,7 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
 
     // ================= consumers
     // z-group per warp (all lanes of a warp read the same 16-B column of a
-    // tap row); a warp covers 8x4 blocks, each 8-lane LDS.128 phase a PWxPH
+    // tap row); a warp covers 8x4 blocks, each 8-lane LDS.128 phase a 4x2
     // patch, so a phase's tap rows stay within 8 consecutive channels ->
     // distinct bank quads (row pitch 144 B = 9 quads).
     const int zg = threadIdx.x / L::COLS;
@@ -296,47 +241,25 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     const int by = (wg / L::WX) * 4 + (q / QW) * L::PH + (i8 / L::PW);
     const int dx0 = bx * VX, dy0 = by * VY;
     const size_t plane = (size_t)args.nx * args.ny;
+    const int zrow0 = zb * kZB + zg * ZT;                 // first volume row of this thread
+    const int nz = min(ZT, args.n_rows - zrow0);          // may be <= 0 for a ragged last block
 
     float acc[VX * VY][ZT];
-    Item item;
-    int zrow0 = 0, nz = 0;
-    auto item_begin = [&](int idx) {
-        item = decode_item<PERSIST>(args, idx);
-        zrow0 = item.zb * kZB + zg * ZT;          // first volume row of this thread
-        nz = min(ZT, args.n_rows - zrow0);        // may be <= 0 for a ragged last block
 #pragma unroll
-        for (int v = 0; v < VX * VY; ++v)
+    for (int v = 0; v < VX * VY; ++v)
 #pragma unroll
-            for (int j = 0; j < ZT; ++j) acc[v][j] = 0.f;
-        if (args.flags & TF_BP_ACCUMULATE) {
-#pragma unroll
-            for (int v = 0; v < VX * VY; ++v) {
-                const int x = item.X0 + dx0 + (v % VX), y = item.Y0 + dy0 + (v / VX);
-                if (x >= item.ux0 && x < item.ux1 && y >= item.uy0 && y < item.uy1) {
-#pragma unroll
-                    for (int j = 0; j < ZT; ++j)
-                        if (j < nz) acc[v][j] = args.vol[(size_t)(zrow0 + j) * plane + (size_t)y * args.nx + x];
-                }
-            }
-        }
-    };
-    auto item_end = [&]() {
+        for (int j = 0; j < ZT; ++j) acc[v][j] = 0.f;
+    if (args.flags & TF_BP_ACCUMULATE) {
 #pragma unroll
         for (int v = 0; v < VX * VY; ++v) {
-            const int x = item.X0 + dx0 + (v % VX), y = item.Y0 + dy0 + (v / VX);
-            if (!(x >= item.ux0 && x < item.ux1 && y >= item.uy0 && y < item.uy1)) continue;
-            float scale = 1.f;
-            bool zero = false;
-            if (args.flags & TF_BP_FINALIZE) {
-                scale = args.angle_wf;
-                zero = outside_fov(x, y, args);
-            }
-            float* out = args.vol + (size_t)zrow0 * plane + (size_t)y * args.nx + x;
+            const int x = X0 + dx0 + (v % VX), y = Y0 + dy0 + (v / VX);
+            if (x >= ux0 && x < ux1 && y >= uy0 && y < uy1) {
 #pragma unroll
-            for (int j = 0; j < ZT; ++j)
-                if (j < nz) out[(size_t)j * plane] = zero ? 0.f : acc[v][j] * scale;
+                for (int j = 0; j < ZT; ++j)
+                    if (j < nz) acc[v][j] = args.vol[(size_t)(zrow0 + j) * plane + (size_t)y * args.nx + x];
+            }
         }
-    };
+    }
 
     // per-angle setup: detector coordinates -> tap row + interpolation weights
     const uint8_t* ring_z = ring + zg * ZT * 4;
@@ -458,68 +381,54 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
         if (lane == 0) mbar_arrive(&empty[(g / APS) % STAGES]);
     };
 
-    if (n_ang == 0) {  // empty angle range (non-persistent launches only): FINALIZE still writes
-        item_begin(0);
-        item_end();
-        return;
-    }
-    for (int gg = 0;; gg += n_ang) {
-        if (gg % APS == 0) wait_full(gg);
-        const int id = __float_as_int(prm[gg & (L::RING - 1)].w);
-        if (id == kEnd) break;  // same for every consumer thread
-        item_begin(id);
-        if constexpr (!L::PIPE) {
-            for (int a = 0; a < n_ang; ++a) {
-                const int g = gg + a;
-                if (a > 0 && g % APS == 0) wait_full(g);
-                const float* p0;
-                float w[VX * VY][NT];
-                int cls;
-                setup(g, p0, w, cls);
-                accumulate(p0, w, cls);
-                if (g % APS == APS - 1) release(g);
-            }
-        } else {
+    if constexpr (!L::PIPE) {
+        for (int g = 0; g < n_ang; ++g) {
+            if (g % APS == 0) wait_full(g);
             const float* p0;
             float w[VX * VY][NT];
             int cls;
-            setup(gg, p0, w, cls);
-            for (int a = 0; a < n_ang; ++a) {
-                const int g = gg + a, gn = g + 1;
-                const bool more = a + 1 < n_ang;
-                if (more && gn % APS == 0) wait_full(gn);
-                const float* q0;
-                float wn[VX * VY][NT];
-                int clsn;
-                setup(more ? gn : g, q0, wn, clsn);  // independent of this angle's FMAs
-                accumulate(p0, w, cls);
-                if (g % APS == APS - 1) release(g);
-                p0 = q0;
-                cls = clsn;
-#pragma unroll
-                for (int v = 0; v < VX * VY; ++v)
-#pragma unroll
-                    for (int j = 0; j < NT; ++j) w[v][j] = wn[v][j];
-            }
+            setup(g, p0, w, cls);
+            accumulate(p0, w, cls);
+            if (g % APS == APS - 1 || g == n_ang - 1) release(g);
         }
-        item_end();
+    } else if (n_ang > 0) {
+        wait_full(0);
+        const float* p0;
+        float w[VX * VY][NT];
+        int cls;
+        setup(0, p0, w, cls);
+        for (int g = 0; g < n_ang; ++g) {
+            const int gn = g + 1;
+            if (gn < n_ang && gn % APS == 0) wait_full(gn);
+            const float* q0;
+            float wn[VX * VY][NT];
+            int clsn;
+            setup(min(gn, n_ang - 1), q0, wn, clsn);  // independent of this angle's FMAs
+            accumulate(p0, w, cls);
+            if (gn % APS == 0 || gn == n_ang) release(g);
+            p0 = q0;
+            cls = clsn;
+#pragma unroll
+            for (int v = 0; v < VX * VY; ++v)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) w[v][j] = wn[v][j];
+        }
     }
-}
 
-// Zero the volume columns of FoV-inactive tiles (the persistent kernel never
-// visits them).
-__global__ void zero_tiles_kernel(float* __restrict__ vol, const int* __restrict__ tiles, int n_tiles, int ntx, int nx,
-                                  int ny, int n_rows) {
-    const size_t plane = (size_t)nx * ny;
-    const long long total = (long long)n_tiles * n_rows * TY;
-    for (long long i = blockIdx.x * (long long)(blockDim.x / TX) + threadIdx.x / TX; i < total;
-         i += (long long)gridDim.x * (blockDim.x / TX)) {
-        const int yy = (int)(i % TY);
-        const long long rz = i / TY;
-        const int z = (int)(rz % n_rows);
-        const int tile = tiles[rz / n_rows];
-        const int x = (tile % ntx) * TX + (threadIdx.x % TX), y = (tile / ntx) * TY + yy;
-        if (x < nx && y < ny) vol[(size_t)z * plane + (size_t)y * nx + x] = 0.f;
+#pragma unroll
+    for (int v = 0; v < VX * VY; ++v) {
+        const int x = X0 + dx0 + (v % VX), y = Y0 + dy0 + (v / VX);
+        if (!(x >= ux0 && x < ux1 && y >= uy0 && y < uy1)) continue;
+        float scale = 1.f;
+        bool zero = false;
+        if (args.flags & TF_BP_FINALIZE) {
+            scale = args.angle_wf;
+            zero = outside_fov(x, y, args);
+        }
+        float* out = args.vol + (size_t)zrow0 * plane + (size_t)y * args.nx + x;
+#pragma unroll
+        for (int j = 0; j < ZT; ++j)
+            if (j < nz) out[(size_t)j * plane] = zero ? 0.f : acc[v][j] * scale;
     }
 }
 
@@ -607,6 +516,14 @@ int default_variant() {
     return v;
 }
 
+bool tile_order_enabled() {
+    static int v = [] {
+        const char* e = getenv("TF_BP_MORTON");  // benchmarking knob: 0 = row-major tile launch order
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 int select_variant(const tf_bp_plan* p, int flags) {
     int variant = (flags & TF_BP_KERNEL_V1) ? 0 : default_variant();
     if (variant >= 5 && variant <= 7 && p->scale > 1.0) variant = 0;  // x-pairs need |cos|*scale <= 1 (3 taps)
@@ -614,29 +531,11 @@ int select_variant(const tf_bp_plan* p, int flags) {
     return variant;
 }
 
-bool persistent_enabled() {
-    static int v = [] {
-        const char* e = getenv("TF_BP_PERSIST");  // benchmarking knob: 0 disables the work-list schedule
-        return e ? atoi(e) : 1;
-    }();
-    return v != 0;
-}
-
 template <class L>
-int launch_bp(const CUtensorMap& map, const BPArgs& a, dim3 grid, void* stream, bool persist) {
+int launch_bp(const CUtensorMap& map, const BPArgs& a, dim3 grid, void* stream) {
     const int smem = bp_smem_bytes<L>(a.slot_bytes);
-    if (persist) {
-        TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        int per_sm = 0, dev = 0, sms = 0;
-        TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bp_kernel<L, true>, L::NTHREADS, smem));
-        TF_CUDA_TRY(cudaGetDevice(&dev));
-        TF_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        const int g = std::max(1, std::min(a.n_items, std::max(1, per_sm) * sms));
-        bp_kernel<L, true><<<g, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
-    } else {
-        TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        bp_kernel<L, false><<<grid, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
-    }
+    TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    bp_kernel<L><<<grid, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
     return TF_OK;
 }
 }  // namespace
@@ -706,7 +605,8 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     p->sc2 = p->scale * p->scale;
     const double step = g->angle_span / g->n_proj;
     p->angle_wf = (float)step;
-    // tiles with any voxel inside the FoV (same fp64 test as the kernel's early-out)
+    // tile launch order: FoV-active tiles (same fp64 test as the kernel's
+    // early-out) in Morton order, then the inactive ones (they exit at once)
     const int ntx = (g->nx + TX - 1) / TX, nty = (g->ny + TY - 1) / TY;
     std::vector<int> act, inact;
     for (int t = 0; t < ntx * nty; ++t) {
@@ -726,17 +626,12 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
             }
         (all_out ? inact : act).push_back(t);
     }
-    // Morton (Z-order) tile order: the CTAs resident at one moment (consecutive
-    // list entries) cover a compact patch, so their per-angle channel windows
-    // overlap and the patch's angle working set is small enough for L2
     auto morton = [&](int t) {
         unsigned x = (unsigned)(t % ntx), y = (unsigned)(t / ntx), m = 0;
         for (int b = 0; b < 16; ++b) m |= ((x >> b) & 1u) << (2 * b) | ((y >> b) & 1u) << (2 * b + 1);
         return m;
     };
     std::stable_sort(act.begin(), act.end(), [&](int a, int b) { return morton(a) < morton(b); });
-    p->n_active = (int)act.size();
-    p->n_inactive = (int)inact.size();
     act.insert(act.end(), inact.begin(), inact.end());
     std::vector<double2> trig(g->n_proj);
     for (int k = 0; k < g->n_proj; ++k) {  // theta_k = k * (span / n_proj), geometry.py:69-70
@@ -746,10 +641,8 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     std::vector<float> wf(g->n_chan);
     for (int i = 0; i < g->n_chan; ++i) wf[i] = (float)w[i];
     cudaError_t e = cudaMalloc(&p->d_trig, sizeof(double2) * g->n_proj);
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_tiles, sizeof(int) * std::max<size_t>(1, act.size()));
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_counters, sizeof(int) * 64);
-    if (e == cudaSuccess && !act.empty())
-        e = cudaMemcpy(p->d_tiles, act.data(), sizeof(int) * act.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_order, sizeof(int) * act.size());
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_order, act.data(), sizeof(int) * act.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_w, sizeof(float) * g->n_chan);
     if (e == cudaSuccess)
         e = cudaMemcpy(p->d_trig, trig.data(), sizeof(double2) * g->n_proj, cudaMemcpyHostToDevice);
@@ -766,8 +659,7 @@ extern "C" int tf_bp_plan_destroy(tf_bp_plan* p) {
     if (!p) return TF_OK;
     cudaFree(p->d_trig);
     cudaFree(p->d_w);
-    cudaFree(p->d_tiles);
-    cudaFree(p->d_counters);
+    cudaFree(p->d_order);
     delete p;
     return TF_OK;
 }
@@ -827,6 +719,7 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
 
     BPArgs a{};
     a.trig = p->d_trig;
+    a.order = tile_order_enabled() ? p->d_order : nullptr;
     a.vol = vol;
     a.a0 = a0;
     a.a1 = a1;
@@ -852,37 +745,18 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     a.angle_wf = p->angle_wf;
     const int nty = (g.ny + TY - 1) / TY;
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)nzb);
-    // full-volume calls walk the FoV-active tile list with persistent CTAs
-    const bool persist = persistent_enabled() && a0 < a1 && x0 == 0 && x1 == g.nx && y0 == 0 && y1 == g.ny;
-    a.tiles = p->d_tiles;
-    a.n_active = p->n_active;
-    a.n_items = p->n_active * nzb;
-    if (persist) {
-        const unsigned slot = __atomic_fetch_add(&const_cast<tf_bp_plan*>(p)->seq, 1u, __ATOMIC_RELAXED) % 64u;
-        a.counter = p->d_counters + slot;
-        TF_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(int), as_stream(stream)));
-    }
-    if (persist && !(flags & TF_BP_ACCUMULATE) && p->n_inactive > 0) {
-        const long long work = (long long)p->n_inactive * n_rows * TY;
-        const int blocks = (int)std::min<long long>((work + 15) / 16, 148LL * 16);
-        zero_tiles_kernel<<<blocks, 256, 0, as_stream(stream)>>>(vol, p->d_tiles + p->n_active, p->n_inactive, a.ntx,
-                                                                g.nx, g.ny, n_rows);
-        int zs = check_launch("zero_tiles_kernel");
-        if (zs) return zs;
-    }
-    if (persist && a.n_items == 0) return TF_OK;
     int st;
     switch (variant) {
-        case 0: st = launch_bp<V1Cfg>(map, a, grid, stream, persist); break;
-        case 1: st = launch_bp<V4Cfg1>(map, a, grid, stream, persist); break;
-        case 2: st = launch_bp<V4Cfg2>(map, a, grid, stream, persist); break;
-        case 3: st = launch_bp<V4Cfg3>(map, a, grid, stream, persist); break;
-        case 4: st = launch_bp<V4Cfg4>(map, a, grid, stream, persist); break;
-        case 5: st = launch_bp<P3Cfg5>(map, a, grid, stream, persist); break;
-        case 6: st = launch_bp<P3Cfg6>(map, a, grid, stream, persist); break;
-        case 7: st = launch_bp<P3Cfg7>(map, a, grid, stream, persist); break;
-        case 8: st = launch_bp<Q4Cfg8>(map, a, grid, stream, persist); break;
-        default: st = launch_bp<Q4Cfg9>(map, a, grid, stream, persist); break;
+        case 0: st = launch_bp<V1Cfg>(map, a, grid, stream); break;
+        case 1: st = launch_bp<V4Cfg1>(map, a, grid, stream); break;
+        case 2: st = launch_bp<V4Cfg2>(map, a, grid, stream); break;
+        case 3: st = launch_bp<V4Cfg3>(map, a, grid, stream); break;
+        case 4: st = launch_bp<V4Cfg4>(map, a, grid, stream); break;
+        case 5: st = launch_bp<P3Cfg5>(map, a, grid, stream); break;
+        case 6: st = launch_bp<P3Cfg6>(map, a, grid, stream); break;
+        case 7: st = launch_bp<P3Cfg7>(map, a, grid, stream); break;
+        case 8: st = launch_bp<Q4Cfg8>(map, a, grid, stream); break;
+        default: st = launch_bp<Q4Cfg9>(map, a, grid, stream); break;
     }
     if (st) return st;
     return check_launch("bp_kernel");
