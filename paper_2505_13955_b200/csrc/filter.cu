@@ -32,6 +32,7 @@ struct tf_filter_plan {
     int smem;          // dynamic shared memory per CTA
     int max_grid;      // persistent grid: resident CTAs per SM x SMs
     const void* kernel;  // ramp_filter_kernel instantiation for this P
+    bool fused;          // fused-I/O FFT path
 };
 
 namespace tf {
@@ -148,10 +149,22 @@ __device__ __forceinline__ void dft(float2 (&v)[R]) {
 
 // One Stockham pass of radix R over a padded smem line of length P; each
 // thread holds NB radix-R butterflies in registers across the sync.
-// Twiddles come from `tw` (exp(-2 pi i m / P), m in [0, P)), staged in
-// shared memory for P <= 8192, else read from global.
-template <int R, int NB>
-__device__ __forceinline__ void stockham_pass(float2* buf, const float2* tw, int P, int Ns, int tid, int T) {
+// IN/OUT select fused I/O so no separate load / multiply / store sweeps
+// (and their __syncthreads) are needed:
+//   IN_GLOBAL : inputs come from `load(m)` (the first pass; Ns == 1 so inputs
+//               r >= R/2 are at m >= P/2 >= n, the zero pad -- pruned);
+//   OUT_MULT  : outputs (the natural-order spectrum of the last forward pass)
+//               are multiplied by the ramp spectrum / P and conjugated;
+//   OUT_GLOBAL: outputs m < n go to `store(m, v)` (the last inverse pass).
+// Twiddles `tw` are this pass's [r][k] table (consecutive lanes read
+// consecutive entries); with the 1-in-16 padding of pad_idx the radix-16
+// passes are bank-conflict-free.
+enum { IN_SMEM = 0, IN_GLOBAL = 1 };
+enum { OUT_SMEM = 0, OUT_MULT = 1, OUT_GLOBAL = 2 };
+
+template <int R, int NB, int IN, int OUT, class Load, class Store>
+__device__ __forceinline__ void fft_pass(float2* buf, const float2* tw, int P, int Ns, int n, int tid, int T,
+                                         const Load& load, const float* __restrict__ mult, const Store& store) {
     float2 v[NB][R];
     const int nb = P / R;
 #pragma unroll
@@ -161,16 +174,16 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* tw, int
             const int k = j & (Ns - 1);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                float2 x = buf[pad_idx(j + r * nb)];
-                // pass table [r][k] = exp(-2 pi i k r / (Ns R)): consecutive lanes
-                // read consecutive entries (no bank conflicts)
+                float2 x;
+                if constexpr (IN == IN_GLOBAL) x = (r < R / 2) ? load(j + r * nb) : make_float2(0.f, 0.f);
+                else x = buf[pad_idx(j + r * nb)];
                 if (r > 0 && Ns > 1) x = cmul(x, tw[r * Ns + k]);
                 v[b][r] = x;
             }
             dft<R>(v[b]);
         }
     }
-    __syncthreads();
+    if constexpr (OUT != OUT_GLOBAL) __syncthreads();  // every read of buf done before it is overwritten
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
         const int j = tid + b * T;
@@ -178,50 +191,114 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* tw, int
             const int k = j & (Ns - 1);
             const int base = (j - k) * R + k;
 #pragma unroll
-            for (int r = 0; r < R; ++r) buf[pad_idx(base + r * Ns)] = v[b][r];
+            for (int r = 0; r < R; ++r) {
+                const int m = base + r * Ns;
+                const float2 x = v[b][r];
+                if constexpr (OUT == OUT_SMEM) {
+                    buf[pad_idx(m)] = x;
+                } else if constexpr (OUT == OUT_MULT) {
+                    // X <- conj(X * M / P): the inverse transform is conj(FFT(conj(.)))
+                    const float g = __ldg(&mult[m <= P / 2 ? m : P - m]);
+                    buf[pad_idx(m)] = make_float2(x.x * g, -x.y * g);
+                } else {
+                    if (m < n) store(m, x);
+                }
+            }
         }
     }
-    __syncthreads();
+    if constexpr (OUT != OUT_GLOBAL) __syncthreads();
 }
 
-// Radix-16 passes (one butterfly per thread, T >= P/16) plus one radix-8/4/2
-// pass.  With the 1-in-16 padding of pad_idx, every radix-16 pass reads and
-// writes shared memory without bank conflicts.  `tw` holds the per-pass
-// twiddle tables back to back (twiddle_tables() on the host).
-__device__ __forceinline__ void fft_forward(float2* buf, const float2* tw, int P, int log2P, int tid, int T) {
+// Radix sequences.  Generic path: radix-16 passes, remainder (2/4/8) last.
+// Fused path (P >= 256, no blur): radix 16, then the remainder, then radix
+// 16 -- so the first pass (global input, pruned zero half) and the last
+// pass (global output, pruned half) are always radix 16.
+std::vector<int> radix_plan(int log2P, bool fused) {
+    std::vector<int> rs;
+    const int tail = log2P % 4;
+    int n16 = log2P / 4;
+    if (fused) {
+        rs.push_back(16);
+        --n16;
+        if (tail) rs.push_back(1 << tail);
+        for (int i = 0; i < n16; ++i) rs.push_back(16);
+    } else {
+        for (int i = 0; i < n16; ++i) rs.push_back(16);
+        if (tail) rs.push_back(1 << tail);
+    }
+    return rs;
+}
+
+// Per-pass twiddle tables in pass order: for each pass with Ns > 1, R*Ns
+// entries [r][k] = exp(-2 pi i k r / (Ns R)) (fp64, rounded once).
+std::vector<float2> twiddle_tables(const std::vector<int>& rs) {
+    std::vector<float2> t;
+    int Ns = 1;
+    for (int R : rs) {
+        if (Ns > 1)
+            for (int r = 0; r < R; ++r)
+                for (int k = 0; k < Ns; ++k) {
+                    const double a = -2.0 * M_PI * (double)k * (double)r / ((double)Ns * (double)R);
+                    t.push_back(make_float2((float)cos(a), (float)sin(a)));
+                }
+        Ns *= R;
+    }
+    if (t.empty()) t.push_back(make_float2(1.f, 0.f));
+    return t;
+}
+
+struct NoIO {
+    __device__ float2 operator()(int) const { return make_float2(0.f, 0.f); }
+    __device__ void operator()(int, float2) const {}
+};
+
+// Generic path: smem -> smem passes only (radix_plan(.., false)).
+__device__ __forceinline__ void fft_smem(float2* buf, const float2* tw, int P, int log2P, int tid, int T) {
+    const NoIO io;
     int Ns = 1, rem = log2P;
     while (rem >= 4) {
-        stockham_pass<16, 1>(buf, tw, P, Ns, tid, T);
+        fft_pass<16, 1, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, P, tid, T, io, nullptr, io);
         if (Ns > 1) tw += 16 * Ns;
         Ns <<= 4;
         rem -= 4;
     }
-    if (rem == 3) stockham_pass<8, 2>(buf, tw, P, Ns, tid, T);
-    else if (rem == 2) stockham_pass<4, 4>(buf, tw, P, Ns, tid, T);
-    else if (rem == 1) stockham_pass<2, 8>(buf, tw, P, Ns, tid, T);
+    if (rem == 3) fft_pass<8, 2, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, P, tid, T, io, nullptr, io);
+    else if (rem == 2) fft_pass<4, 4, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, P, tid, T, io, nullptr, io);
+    else if (rem == 1) fft_pass<2, 8, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, P, tid, T, io, nullptr, io);
 }
 
-// Per-pass twiddle tables, same pass sequence as fft_forward: for each pass
-// with Ns > 1, R*Ns entries [r][k] = exp(-2 pi i k r / (Ns R)) (fp64, rounded once).
-std::vector<float2> twiddle_tables(int P, int log2P) {
-    std::vector<float2> t;
-    auto add = [&](int R, int Ns) {
-        if (Ns == 1) return;
-        for (int r = 0; r < R; ++r)
-            for (int k = 0; k < Ns; ++k) {
-                const double a = -2.0 * M_PI * (double)k * (double)r / ((double)Ns * (double)R);
-                t.push_back(make_float2((float)cos(a), (float)sin(a)));
-            }
-    };
-    int Ns = 1, rem = log2P;
-    while (rem >= 4) {
-        add(16, Ns);
-        Ns <<= 4;
-        rem -= 4;
+// Fused path (radix_plan(.., true), P >= 256): forward with the input load
+// and the spectrum multiply folded into its first / last pass, then the
+// inverse with the store folded into its last pass.
+template <class Load, class Store>
+__device__ __forceinline__ void fft_fused(float2* buf, const float2* tw0, int P, int log2P, int n, int tid, int T,
+                                          const Load& load, const float* mult, const Store& store) {
+    const int tail = log2P % 4;
+    const int n16 = log2P / 4;  // >= 2
+    for (int dir = 0; dir < 2; ++dir) {
+        const float2* tw = tw0;
+        int Ns = 1;
+        // pass 0: radix 16
+        if (dir == 0) fft_pass<16, 1, IN_GLOBAL, OUT_SMEM>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+        else fft_pass<16, 1, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+        Ns = 16;
+        if (tail) {
+            const int R = 1 << tail;
+            if (R == 8) fft_pass<8, 2, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+            else if (R == 4) fft_pass<4, 4, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+            else fft_pass<2, 8, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+            tw += R * Ns;
+            Ns *= R;
+        }
+        for (int p = 1; p < n16; ++p) {
+            const bool last = p == n16 - 1;
+            if (!last) fft_pass<16, 1, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+            else if (dir == 0) fft_pass<16, 1, IN_SMEM, OUT_MULT>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+            else fft_pass<16, 1, IN_SMEM, OUT_GLOBAL>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+            tw += 16 * Ns;
+            Ns *= 16;
+        }
     }
-    if (rem > 0) add(1 << rem, Ns);
-    if (t.empty()) t.push_back(make_float2(1.f, 0.f));
-    return t;
 }
 
 // Where filtered line l = (angle a, row r) goes (tf_filter's slab map and
@@ -257,7 +334,7 @@ __device__ __forceinline__ float* out_ptr(long long l, int n, const OutMap& m, c
 
 // Persistent: each CTA loops over line pairs; the twiddle table is loaded
 // into shared memory once per CTA.
-template <bool SMEM_TW, int MAXT>
+template <bool SMEM_TW, int MAXT, bool FUSED>
 __global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kernel(const float* __restrict__ in, float* out,
                                                            long long n_lines, int n, int P, int log2P,
                                                            const float2* __restrict__ tw_g,
@@ -288,86 +365,81 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kerne
         const bool has_b = la + 1 < n_lines;
         const float* pa = in + la * n;
         const float* pb = pa + n;
-        // load (+ Beer-Lambert) the two lines as one complex line, zero-padded
-        for (int m = tid; m < P; m += T) {
-            float2 z = make_float2(0.f, 0.f);
-            if (m < n) {
-                float a = __ldcs(pa + m);
-                float b = has_b ? __ldcs(pb + m) : 0.f;
-                if (log_in) {  // -ln(max(raw, 1) / i0), fbp.py:80-83
-                    a = -logf(__fdiv_rn(fmaxf(a, 1.f), i0));
-                    b = has_b ? -logf(__fdiv_rn(fmaxf(b, 1.f), i0)) : 0.f;
-                }
-                z = make_float2(a, b);
+        // the two lines as one complex line, Beer-Lambert fused (fbp.py:80-83)
+        auto load = [&](int m) -> float2 {
+            if (m >= n) return make_float2(0.f, 0.f);
+            float a = __ldcs(pa + m);
+            float b = has_b ? __ldcs(pb + m) : 0.f;
+            if (log_in) {  // -ln(max(raw, 1) / i0)
+                a = -logf(__fdiv_rn(fmaxf(a, 1.f), i0));
+                b = has_b ? -logf(__fdiv_rn(fmaxf(b, 1.f), i0)) : 0.f;
             }
-            data[pad_idx(m)] = z;
-        }
-        __syncthreads();
-
-        if (radius > 0) {  // scipy gaussian_filter1d(mode="nearest") restated (fbp.py:125-126)
-            float2 acc[8];  // n <= P/2 <= 8*T
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int m = tid + q * T;
-                float2 s = make_float2(0.f, 0.f);
-                if (m < n) {
-                    for (int j = -radius; j <= radius; ++j) {
-                        const int c = min(max(m + j, 0), n - 1);
-                        const float wj = __ldg(&blur[j + radius]);
-                        const float2 x = data[pad_idx(c)];
-                        s.x = fmaf(wj, x.x, s.x);
-                        s.y = fmaf(wj, x.y, s.y);
-                    }
-                }
-                acc[q] = s;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int m = tid + q * T;
-                if (m < n) data[pad_idx(m)] = acc[q];
-            }
-            __syncthreads();
-        }
-
-        fft_forward(data, tw, P, log2P, tid, T);
-
-        // X <- conj(X * M / P): the inverse transform is conj(FFT(conj(.)))
-        for (int m = tid; m < P; m += T) {
-            const float g = __ldg(&mult[m <= P / 2 ? m : P - m]);
-            const float2 x = data[pad_idx(m)];
-            data[pad_idx(m)] = make_float2(x.x * g, -x.y * g);
-        }
-        __syncthreads();
-
-        fft_forward(data, tw, P, log2P, tid, T);
-
+            return make_float2(a, b);
+        };
         int za, zb = 0;
         float* oa = out_ptr(la, n, map, s_row0, s_dst, za);
         float* ob = has_b ? out_ptr(la + 1, n, map, s_row0, s_dst, zb) : nullptr;
-        if (!map.zblocked) {
-            for (int m = tid; m < n; m += T) {
-                const float2 y = data[pad_idx(m)];
+        // both rows in one 8-B store when they are z-neighbours of the same block
+        const bool pairwise = map.zblocked && has_b && (ob == oa + 1) && ((za & 1) == 0);
+        auto store = [&](int m, float2 y) {
+            if (!map.zblocked) {
                 __stcs(oa + m, y.x);
                 if (has_b) __stcs(ob + m, -y.y);
+                return;
             }
+            // feather applied after the filter, as fbp.py:242 does (f32 product)
+            const float wm = map.w ? __ldg(&map.w[m]) : 1.f;
+            const float va = y.x * wm, vb = -y.y * wm;
+            if (pairwise) {
+                *reinterpret_cast<float2*>(oa + (size_t)m * kZP) = make_float2(va, vb);
+            } else {
+                oa[(size_t)m * kZP] = va;
+                if (has_b) ob[(size_t)m * kZP] = vb;
+            }
+        };
+
+        if constexpr (FUSED) {
+            fft_fused(data, tw, P, log2P, n, tid, T, load, mult, store);
         } else {
-            // both rows in one 8-B store when they are z-neighbours of the same block
-            const bool pairwise = has_b && (ob == oa + 1) && ((za & 1) == 0);
-            for (int m = tid; m < n; m += T) {
-                const float2 y = data[pad_idx(m)];
-                const float wm = map.w ? __ldg(&map.w[m]) : 1.f;
-                // feather applied after the filter, as fbp.py:242 does (f32 product)
-                const float va = y.x * wm, vb = -y.y * wm;
-                if (pairwise) {
-                    *reinterpret_cast<float2*>(oa + (size_t)m * kZP) = make_float2(va, vb);
-                } else {
-                    oa[(size_t)m * kZP] = va;
-                    if (has_b) ob[(size_t)m * kZP] = vb;
+            __syncthreads();  // previous pair may still read data[]
+            for (int m = tid; m < P; m += T) data[pad_idx(m)] = load(m);
+            __syncthreads();
+            if (radius > 0) {  // scipy gaussian_filter1d(mode="nearest") restated (fbp.py:125-126)
+                float2 acc[8];  // n <= P/2 <= 8*T
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int m = tid + q * T;
+                    float2 s = make_float2(0.f, 0.f);
+                    if (m < n) {
+                        for (int j = -radius; j <= radius; ++j) {
+                            const int c = min(max(m + j, 0), n - 1);
+                            const float wj = __ldg(&blur[j + radius]);
+                            const float2 x = data[pad_idx(c)];
+                            s.x = fmaf(wj, x.x, s.x);
+                            s.y = fmaf(wj, x.y, s.y);
+                        }
+                    }
+                    acc[q] = s;
                 }
+                __syncthreads();
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int m = tid + q * T;
+                    if (m < n) data[pad_idx(m)] = acc[q];
+                }
+                __syncthreads();
             }
+            fft_smem(data, tw, P, log2P, tid, T);
+            // X <- conj(X * M / P): the inverse transform is conj(FFT(conj(.)))
+            for (int m = tid; m < P; m += T) {
+                const float g = __ldg(&mult[m <= P / 2 ? m : P - m]);
+                const float2 x = data[pad_idx(m)];
+                data[pad_idx(m)] = make_float2(x.x * g, -x.y * g);
+            }
+            __syncthreads();
+            fft_smem(data, tw, P, log2P, tid, T);
+            for (int m = tid; m < n; m += T) store(m, data[pad_idx(m)]);
         }
-        __syncthreads();  // data[] is reused by the next pair
     }
 }
 
@@ -416,7 +488,8 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
     p->P = P;
     p->log2P = ilog2(P);
     p->threads = std::max(32, P / 16);  // one radix-16 butterfly per thread (P <= 16384 -> <= 1024)
-    std::vector<float2> tw = twiddle_tables(P, p->log2P);
+    p->fused = p->log2P >= 8 && blur_sigma <= 0;  // I/O folded into the first/last FFT passes
+    std::vector<float2> tw = twiddle_tables(radix_plan(p->log2P, p->fused));
     p->n_tw = (int)tw.size();
     std::vector<double> mult(P / 2 + 1);
     multiplier_fp64(kind, P, pixel_pitch, mult.data());
@@ -446,9 +519,14 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
         e = cudaMemcpy(p->d_blur, bw.data(), sizeof(float) * (2 * rad + 1), cudaMemcpyHostToDevice);
     p->smem_tw = P <= 8192;  // twiddle table in shared memory next to the line buffer
     p->smem = (P + P / 16 + (p->smem_tw ? p->n_tw : 0)) * (int)sizeof(float2);
-    p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256>
-                : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512>
-                                    : (const void*)ramp_filter_kernel<false, 1024>;
+    if (p->fused)
+        p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256, true>
+                    : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512, true>
+                                        : (const void*)ramp_filter_kernel<false, 1024, true>;
+    else
+        p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256, false>
+                    : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512, false>
+                                        : (const void*)ramp_filter_kernel<false, 1024, false>;
     if (e == cudaSuccess) e = cudaFuncSetAttribute(p->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem);
     if (e == cudaSuccess) {
         int blocks = 0;
