@@ -147,6 +147,39 @@ __device__ __forceinline__ void dft(float2 (&v)[R]) {
     }
 }
 
+// In-place radix-4 DFT of (a, b, c, d) -> (X0, X1, X2, X3), forward sign.
+__device__ __forceinline__ void dft4_ip(float2& a, float2& b, float2& c, float2& d) {
+    const float2 s0 = make_float2(a.x + c.x, a.y + c.y), d0 = make_float2(a.x - c.x, a.y - c.y);
+    const float2 s1 = make_float2(b.x + d.x, b.y + d.y);
+    const float2 d1 = make_float2(b.y - d.y, d.x - b.x);  // (b - d) * (-i)
+    a = make_float2(s0.x + s1.x, s0.y + s1.y);
+    c = make_float2(s0.x - s1.x, s0.y - s1.y);
+    b = make_float2(d0.x + d1.x, d0.y + d1.y);
+    d = make_float2(d0.x - d1.x, d0.y - d1.y);
+}
+
+// In-place radix-16 as 4 x 4 (n = n1 + 4 n2, k = 4 k1 + k2): radix-4 over n2,
+// twiddle W16^(n1 k2), radix-4 over n1.  Few temporaries, so a thread keeps
+// only its 16 complex values live.  Result X[k] sits at v[dft16_pos(k)].
+__host__ __device__ constexpr int dft16_pos(int k) { return 4 * (k % 4) + k / 4; }
+
+__device__ __forceinline__ void dft16_ip(float2 (&v)[16]) {
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) dft4_ip(v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]);
+    // now v[n1 + 4 k2] = y[n1][k2]; multiply by W16^(n1 k2)
+#pragma unroll
+    for (int n1 = 1; n1 < 4; ++n1)
+#pragma unroll
+        for (int k2 = 1; k2 < 4; ++k2) {
+            const int e = (n1 * k2) & 15;
+            const float2 w = e < 8 ? w16(e) : make_float2(-w16(e - 8).x, -w16(e - 8).y);
+            v[n1 + 4 * k2] = cmul(v[n1 + 4 * k2], w);
+        }
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) dft4_ip(v[4 * k2], v[4 * k2 + 1], v[4 * k2 + 2], v[4 * k2 + 3]);
+    // v[4 k2 + k1] = X[4 k1 + k2]
+}
+
 // One Stockham pass of radix R over a padded smem line of length P; each
 // thread holds NB radix-R butterflies in registers across the sync.
 // IN/OUT select fused I/O so no separate load / multiply / store sweeps
@@ -180,7 +213,8 @@ __device__ __forceinline__ void fft_pass(float2* buf, const float2* tw, int P, i
                 if (r > 0 && Ns > 1) x = cmul(x, tw[r * Ns + k]);
                 v[b][r] = x;
             }
-            dft<R>(v[b]);
+            if constexpr (R == 16) dft16_ip(v[b]);
+            else dft<R>(v[b]);
         }
     }
     if constexpr (OUT != OUT_GLOBAL) __syncthreads();  // every read of buf done before it is overwritten
@@ -193,7 +227,7 @@ __device__ __forceinline__ void fft_pass(float2* buf, const float2* tw, int P, i
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int m = base + r * Ns;
-                const float2 x = v[b][r];
+                const float2 x = v[b][R == 16 ? dft16_pos(r) : r];
                 if constexpr (OUT == OUT_SMEM) {
                     buf[pad_idx(m)] = x;
                 } else if constexpr (OUT == OUT_MULT) {
