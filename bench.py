@@ -345,6 +345,14 @@ def main():
         pass
     stage_bytes = slab.stage.numel()
     hbm_alg = stage_bytes + slab.vol.numel() * 4  # one pass over the staged slab + the volume write
+    traffic = None  # ncu dram bytes of this kernel/config, captured separately (profiles/)
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", f"bp_traffic_{args.config}.json")))
+        if world == 1:
+            traffic = {"bytes_per_launch": tr["dram_bytes_per_launch"], "algorithmic_bytes": hbm_alg,
+                       "ratio": round(tr["dram_bytes_per_launch"] / hbm_alg, 2), "source": tr["source"]}
+    except (OSError, KeyError, ValueError):
+        pass
 
     # ---- e2e through host pinned buffers: StreamedReconstructor (public API)
     e2e = None
@@ -460,7 +468,8 @@ def main():
             "peak": round(smem_peak, 1),
             "unit": "GB/s",
             "frac": round(smem_achieved / smem_peak, 4),
-            "traffic": None,
+            "traffic": traffic["bytes_per_launch"] if traffic else None,
+            "traffic_detail": traffic,
             "peak_source": "derived: 128 B/clk/SM x 148 SMs x measured median SM clock "
                            "(shared-memory data path; no tensor-core or HBM bound applies, SURVEY 8d)",
             "roof_updates_per_s_e9": round(smem_peak / bytes_per_update, 1),
