@@ -172,6 +172,13 @@ TF_API int tf_bp_smem_bytes_per_update(const tf_bp_plan* plan, int flags, double
  * bit-identical to numpy for the same input values. */
 TF_API int tf_quantize(const void* vol, int vol_dtype, uint16_t* out, int64_t n, double lo, double hi, void* stream);
 
+/* ---- forward projection (phantom.py:199-255) ----------------------------- */
+/* K5: the transpose of K2's interpolation (linear splat of each in-FoV voxel
+ * onto its two channels), vol (n_rows, ny, nx) fp32 -> sino (n_proj, n_rows,
+ * n_chan) fp32 scaled by voxel_pitch.  project_volume uses voxel_pitch =
+ * pixel_pitch, as the reference does. */
+TF_API int tf_forward_project(const tf_geometry* g, const float* vol, float* sino, void* stream);
+
 /* ---- host <-> device slab streaming --------------------------------------- */
 /* Strided 2-D async copy (cudaMemcpy2DAsync, direction inferred from UVA):
  * `height` rows of `width_bytes`, with the given pitches.  Used to move one

@@ -53,6 +53,7 @@ SIGNATURES = {
     "tf_bp_smem_bytes_per_update": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_double)]),
     "tf_quantize": (_i, [_vp, _i, _vp, _i64, _d, _d, _vp]),
     "tf_phantom_sinogram": (_i, [_pg, _i, _i, _i, _i, _d, _d, _vp, _vp]),
+    "tf_forward_project": (_i, [_pg, _vp, _vp, _vp]),
     "tf_copy2d_async": (_i, [_vp, ctypes.c_size_t, _vp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, _vp]),
 }
 

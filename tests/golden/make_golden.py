@@ -168,6 +168,15 @@ def main():
     g["pipe_q"] = res.quantized["s0"]
     meta["cases"]["pipe"] = dict(geom_record(p, d), grid=[2, 2, 1])
 
+    # --- forward projector phantom.project_volume (phantom.py:199-255)
+    for name, p in [("fp_normal", params(6, 3, 24)), ("fp_offset", params(10, 2, 30, offset=7)),
+                     ("fp_pitch", params(9, 2, 20, pitch=2.5))]:
+        n = p.n_chan
+        vol = rng.random((p.n_rows, n + 4, n + 2))
+        g[name + "_vol"] = vol
+        g[name + "_sino"] = phantom.project_volume(vol, p)
+        meta["cases"][name] = geom_record(p, VolumeDims(n + 2, n + 4, p.n_rows, voxel_pitch=p.pixel_pitch))
+
     g["meta_json"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT}: {len(g)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")

@@ -529,3 +529,53 @@ def test_accepts_reference_style_dataclasses(F, golden):
     assert rel_l2(got, g["bp_small_f64"]) <= REL_L2
     out = F.ramp_filter(g["rf_in"], RefSpec())
     assert np.abs(out - g["rf_ramlak"]).max() <= 2e-6 * np.abs(g["rf_ramlak"]).max()
+
+
+# ---------------------------------------------------------------- K5 forward projector
+@pytest.mark.parametrize("name", ["fp_normal", "fp_offset", "fp_pitch"])
+def test_project_volume_matches_reference(F, golden, name):
+    from paper_2505_13955_b200 import phantom
+
+    g, meta = golden
+    p, _ = ref_objects(meta["cases"][name])
+    got = phantom.project_volume(g[name + "_vol"], p)
+    ref = g[name + "_sino"]
+    assert got.dtype == np.float64 and got.shape == ref.shape
+    err = rel_l2(got, ref)
+    print(f"{name}: rel_l2 {err:.2e}")
+    assert err <= 1e-6
+
+
+@pytest.mark.parametrize("pitch,n_proj", [(1.0, 20), (12.0, 24)])
+def test_projection_pair_adjointness(F, pitch, n_proj):
+    """<FP x, y> dtheta == <x, BP y> dvoxel (test_phantom.py:134-146,
+    acceptance criterion 10: tolerance 1e-4)."""
+    from paper_2505_13955_b200 import phantom
+    from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
+
+    rng = np.random.default_rng(123)
+    p = AcquisitionParams(n_proj=n_proj, n_rows=32, n_chan=32, pixel_pitch=pitch)
+    d = VolumeDims(32, 32, 32, voxel_pitch=pitch)
+    worst = 0.0
+    for _ in range(5):
+        x = rng.random(d.shape)
+        y = rng.random((n_proj, 32, 32))
+        lhs = np.vdot(phantom.project_volume(x, p), y) * (p.angle_span / p.n_proj)
+        rhs = np.vdot(x, F.back_project(y, d, p)) * d.voxel_pitch
+        worst = max(worst, abs(lhs - rhs) / abs(rhs))
+    print(f"adjointness defect (pitch {pitch}): {worst:.2e}")
+    assert worst <= 1e-4
+
+
+def test_single_center_voxel_bump(F):  # test_phantom.py:94-107
+    from paper_2505_13955_b200 import phantom
+    from paper_2505_13955_b200.geometry import AcquisitionParams
+
+    n, a = 17, 0.25
+    vol = np.zeros((1, n, n))
+    vol[0, 8, 8] = a
+    for pitch in (1.0, 2.5):
+        p = AcquisitionParams(n_proj=12, n_rows=1, n_chan=n, pixel_pitch=pitch)
+        sino = phantom.project_volume(vol, p)
+        assert np.allclose(sino.sum(axis=2)[:, 0], a * pitch, rtol=1e-6)
+        assert np.all(sino.argmax(axis=2)[:, 0] == (n - 1) // 2)
