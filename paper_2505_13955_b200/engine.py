@@ -166,18 +166,21 @@ class StreamedReconstructor:
         check(lib().tf_copy2d_async(ctypes.c_void_p(dst), dpitch, ctypes.c_void_p(src), spitch, width, height,
                                     ctypes.c_void_p(stream.cuda_stream)))
 
-    def run(self, raw_host, vol_host, row_range=None, host_row0=0):
+    def run(self, raw_host, vol_host, row_range=None, host_row0=0, quantize=None):
         """raw_host: pinned (n_proj, H, n_chan) fp32 counts holding detector
         rows [host_row0, host_row0 + H); vol_host: pinned (R, ny, nx) fp32
-        receiving volume rows `row_range` = [r0, r1) (default: all rows).
-        Work is queued on this object's streams (ordered after the current
-        stream); returns the last D2H event."""
+        receiving volume rows `row_range` = [r0, r1) (default: all rows), or
+        uint16 when `quantize` = (lo, hi) (K3 runs per slab on the device, so
+        only 2 B/voxel cross PCIe).  Work is queued on this object's streams
+        (ordered after the current stream); returns the last D2H event."""
         torch = self.torch
         p, d = self.params, self.dims
         R0, R1 = row_range if row_range is not None else (0, p.n_rows)
         n = p.n_chan
         line = n * 4
-        plane = d.nx * d.ny * 4
+        plane = d.nx * d.ny * (2 if quantize is not None else 4)
+        if quantize is not None and getattr(self, "_q", None) is None:
+            self._q = [torch.empty(self.vol[0].shape, dtype=torch.uint16, device=self.device) for _ in range(2)]
         cur = torch.cuda.current_stream(self.device)
         for s in (self.s_h2d, self.s_comp, self.s_d2h):
             s.wait_stream(cur)
@@ -209,11 +212,17 @@ class StreamedReconstructor:
             check(lib().tf_backproject(self.eng.bplan.handle, _ptr(self.eng.stage), k, _ptr(self.vol[b]), 0,
                                        p.n_proj, 0, d.nx, 0, d.ny, _lib.TF_BP_FINALIZE,
                                        ctypes.c_void_p(self.s_comp.cuda_stream)))
+            src_vol = self.vol[b]
+            if quantize is not None:  # fbp.quantize on the device (K3)
+                lo, hi = quantize
+                check(lib().tf_quantize(_ptr(self.vol[b]), _lib.TF_F32, _ptr(self._q[b]), k * d.nx * d.ny,
+                                        float(lo), float(hi), ctypes.c_void_p(self.s_comp.cuda_stream)))
+                src_vol = self._q[b]
             comp_done = torch.cuda.Event()
             comp_done.record(self.s_comp)
             # D2H: contiguous volume slab
             self.s_d2h.wait_event(comp_done)
-            self._copy2d(vol_host.data_ptr() + (r0 - R0) * plane, plane, self.vol[b].data_ptr(), plane, plane, k,
+            self._copy2d(vol_host.data_ptr() + (r0 - R0) * plane, plane, src_vol.data_ptr(), plane, plane, k,
                          self.s_d2h)
             ev = torch.cuda.Event()
             ev.record(self.s_d2h)

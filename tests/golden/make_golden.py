@@ -177,6 +177,18 @@ def main():
         g[name + "_sino"] = phantom.project_volume(vol, p)
         meta["cases"][name] = geom_record(p, VolumeDims(n + 2, n + 4, p.n_rows, voxel_pitch=p.pixel_pitch))
 
+    # --- on-disk containers (formats.py): the reference's own bytes
+    import tempfile
+
+    from tomofuse import formats
+
+    with tempfile.TemporaryDirectory() as td:
+        sp, vp = os.path.join(td, "a.sino"), os.path.join(td, "a.vol")
+        formats.write_sino(sp, g["pipe_raw"], params(36, 40, 40))
+        formats.write_vol(vp, g["pipe_q"], 12.0)
+        g["file_sino"] = np.frombuffer(open(sp, "rb").read(), dtype=np.uint8)
+        g["file_vol"] = np.frombuffer(open(vp, "rb").read(), dtype=np.uint8)
+
     g["meta_json"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT}: {len(g)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")

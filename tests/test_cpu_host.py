@@ -308,3 +308,34 @@ def test_oracle_matches_reference_pipeline_run(golden):
     serial = O.fbp_rows(g["pipe_raw"], geom, dtype=np.float32)
     scale = np.abs(serial).max()
     assert np.abs(serial - g["pipe_vol"]).max() <= 1e-5 * scale
+
+
+def test_formats_bytes_match_reference(golden, tmp_path):
+    """SINO/VOL writers produce the reference's exact bytes; readers parse
+    the reference's files (formats.py:30-134)."""
+    from paper_2505_13955_b200 import formats
+    from paper_2505_13955_b200.geometry import AcquisitionParams
+
+    g, _ = golden
+    p = AcquisitionParams(n_proj=36, n_rows=40, n_chan=40)
+    sp, vp = tmp_path / "x.sino", tmp_path / "x.vol"
+    formats.write_sino(sp, g["pipe_raw"], p)
+    assert sp.read_bytes() == g["file_sino"].tobytes()
+    formats.write_vol(vp, g["pipe_q"], 12.0)
+    assert vp.read_bytes() == g["file_vol"].tobytes()
+    ref_sino = tmp_path / "ref.sino"
+    ref_sino.write_bytes(g["file_sino"].tobytes())
+    data, params = formats.read_sino(ref_sino, pixel_pitch=12.0)
+    assert data.dtype == np.float64 and np.array_equal(data, g["pipe_raw"].astype(np.float64))
+    assert (params.n_proj, params.n_rows, params.n_chan, params.pixel_pitch) == (36, 40, 40, 12.0)
+    vol, dims = formats.read_vol(vp)
+    assert np.array_equal(vol, g["pipe_q"]) and dims.voxel_pitch == 12.0
+    bad = tmp_path / "bad.sino"
+    bad.write_bytes(g["file_sino"].tobytes()[:-4])
+    with pytest.raises(ValueError, match="malformed payload"):
+        formats.read_sino(bad)
+    bad.write_bytes(b"XXXX" + g["file_sino"].tobytes()[4:])
+    with pytest.raises(ValueError, match="not a SINO"):
+        formats.read_sino(bad)
+    with pytest.raises(ValueError, match="missing file"):
+        formats.read_sino(tmp_path / "none.sino")
