@@ -339,3 +339,14 @@ def test_formats_bytes_match_reference(golden, tmp_path):
         formats.read_sino(bad)
     with pytest.raises(ValueError, match="missing file"):
         formats.read_sino(tmp_path / "none.sino")
+
+
+def test_cli_error_mapping(tmp_path):
+    """Input errors exit 2 with the reference's prefixes (cli.py:264-285),
+    before any GPU work."""
+    from paper_2505_13955_b200.__main__ import main
+
+    bad = tmp_path / "bad.sino"
+    bad.write_bytes(b"nonsense")
+    assert main(["reconstruct", str(bad), "--out", str(tmp_path / "o")]) == 2
+    assert main(["reconstruct", str(tmp_path / "missing.sino"), "--out", str(tmp_path / "o")]) == 2

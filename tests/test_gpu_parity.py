@@ -595,3 +595,20 @@ def test_reconstruct_file_sino_to_vol(F, golden, tmp_path):
     dq = np.abs(vol.astype(int) - g["pipe_q"].astype(int))
     print(f"reconstruct_file: max |dq| {dq.max()} LSB")
     assert dq.max() <= 2
+
+
+def test_cli_reconstruct(F, golden, tmp_path):
+    import subprocess
+    import sys
+
+    from paper_2505_13955_b200 import formats
+
+    g, _ = golden
+    sp = tmp_path / "in.sino"
+    sp.write_bytes(g["file_sino"].tobytes())
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "paper_2505_13955_b200", "reconstruct", str(sp), "--out",
+                        str(tmp_path / "o"), "--pitch", "1.0"], capture_output=True, text=True, cwd=root)
+    assert r.returncode == 0, r.stderr
+    vol, _ = formats.read_vol(tmp_path / "o" / "volume.vol")
+    assert np.abs(vol.astype(int) - g["pipe_q"].astype(int)).max() <= 2
