@@ -561,7 +561,15 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
         p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256, false>
                     : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512, false>
                                         : (const void*)ramp_filter_kernel<false, 1024, false>;
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(p->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem);
+    // the attribute is per-function global state shared by every plan: raise it
+    // to the device's opt-in maximum (never lower it to this plan's size)
+    if (e == cudaSuccess) {
+        int dev = 0, optin = 0;
+        e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (e == cudaSuccess && p->smem > optin) e = cudaErrorInvalidValue;
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(p->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    }
     if (e == cudaSuccess) {
         int blocks = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, p->kernel, p->threads, p->smem);
