@@ -567,8 +567,11 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
         int dev = 0, optin = 0;
         e = cudaGetDevice(&dev);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        if (e == cudaSuccess && p->smem > optin) e = cudaErrorInvalidValue;
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(p->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+        cudaFuncAttributes fa{};
+        if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, p->kernel);
+        const int maxdyn = optin - (int)fa.sharedSizeBytes;  // static smem counts against the opt-in limit
+        if (e == cudaSuccess && p->smem > maxdyn) e = cudaErrorInvalidValue;
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(p->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, maxdyn);
     }
     if (e == cudaSuccess) {
         int blocks = 0;
