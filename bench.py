@@ -34,6 +34,8 @@ CONFIGS = {
     "c1": dict(n=128, n_proj=180),
     "c2": dict(n=512, n_proj=720),
     "c3": dict(n=2048, n_proj=1800),
+    "c4": dict(n=4096, n_proj=3600),
+    "c5": dict(n=8192, n_proj=7200),  # N_p assumed (~0.88 N)
 }
 PITCH = 12.0   # um (config.py:40,47)
 I0 = 1e5       # config.py:59
@@ -56,6 +58,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--stream", action="store_true",
+                    help="z-sub-slab streaming mode (automatic when the per-GPU slab exceeds HBM)")
+    ap.add_argument("--rows", type=int, default=None,
+                    help="streaming mode: reconstruct only this many rows per GPU (bounded sample)")
     ap.add_argument("--cpu-angles", type=int, default=None,
                     help="angles per CPU-baseline sample (default sized for ~10 s)")
     return ap.parse_args()
@@ -233,11 +239,132 @@ def executed_updates(d, n_proj, k):
     return active * TX * TY * n_proj * (-(-k // ZB) * ZB), active
 
 
+def run_streamed(args, cfg, world, rank, local, dev):
+    """Volumes larger than (aggregate) HBM -- configs C4/C5: each GPU walks
+    its z-slab in sub-slabs; per sub-slab the raw counts are generated on the
+    device (K4; the host cannot hold a 1.9 TB C5 sinogram), filtered straight
+    into staging (K1), back-projected (K2), quantized (K3) and the uint16
+    slab is copied into a pinned host ring (2 slabs), overlapped on 2 streams."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_13955_b200 import _lib
+    from paper_2505_13955_b200._lib import check, lib
+    from paper_2505_13955_b200.engine import SlabReconstructor, phantom_raw
+    from paper_2505_13955_b200.geometry import split_range
+
+    p, d = geometry(cfg)
+    n, n_proj = cfg["n"], cfg["n_proj"]
+    r0, r1 = split_range(n, world)[rank]
+    if args.rows:
+        r1 = min(r1, r0 + args.rows)
+    S = min(args.slab_rows, r1 - r0)
+    eng = SlabReconstructor(p, d, i0=I0, rows=(0, S), device=dev)
+    raw = torch.empty((n_proj, S, n), dtype=torch.float32, device=dev)
+    q = [torch.empty((S, n, n), dtype=torch.uint16, device=dev) for _ in range(2)]
+    ring = [torch.empty((S, n, n), dtype=torch.uint16, pin_memory=True) for _ in range(2)]
+    s_comp = torch.cuda.current_stream(dev)
+    s_d2h = torch.cuda.Stream(dev)
+    d2h_done = [None, None]
+    bp_events = []
+
+    def one_pass(record=False):
+        for i, s0 in enumerate(range(r0, r1, S)):
+            k = min(S, r1 - s0)
+            b = i % 2
+            src = raw.view(-1)[: n_proj * k * n].view(n_proj, k, n)
+            phantom_raw(p, d, src, r0=s0, r1=s0 + k, i0=I0)
+            check(lib().tf_filter_stage(eng.fplan.handle, eng.bplan.handle, ctypes.c_void_p(src.data_ptr()),
+                                        ctypes.c_void_p(eng.stage.data_ptr()), n_proj * k, I0, k, 0, None, None,
+                                        ctypes.c_void_p(s_comp.cuda_stream)))
+            if d2h_done[b] is not None:
+                s_comp.wait_event(d2h_done[b])
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s_comp)
+            check(lib().tf_backproject(eng.bplan.handle, ctypes.c_void_p(eng.stage.data_ptr()), k,
+                                       ctypes.c_void_p(eng.vol.data_ptr()), 0, n_proj, 0, n, 0, n,
+                                       _lib.TF_BP_FINALIZE, ctypes.c_void_p(s_comp.cuda_stream)))
+            e1.record(s_comp)
+            if record:
+                bp_events.append((e0, e1, k))
+            check(lib().tf_quantize(ctypes.c_void_p(eng.vol.data_ptr()), _lib.TF_F32,
+                                    ctypes.c_void_p(q[b].data_ptr()), k * n * n, 0.0, 4e-4,
+                                    ctypes.c_void_p(s_comp.cuda_stream)))
+            ev = torch.cuda.Event()
+            ev.record(s_comp)
+            s_d2h.wait_event(ev)
+            with torch.cuda.stream(s_d2h):
+                ring[b][:k].copy_(q[b][:k], non_blocking=True)
+            dd = torch.cuda.Event()
+            dd.record(s_d2h)
+            d2h_done[b] = dd
+        s_comp.wait_stream(s_d2h)
+
+    for _ in range(args.warmup):
+        one_pass()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record()
+    for _ in range(args.steps):
+        one_pass(record=True)
+    eb.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([ea.elapsed_time(eb) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    rows_all = (r1 - r0) * world if args.rows else n
+    upd = n_proj * rows_all * n * n
+    bp_ms = sum(e0.elapsed_time(e1) for e0, e1, _ in bp_events)
+    bp_upd = sum(n_proj * k * n * n for _, _, k in bp_events)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(upd / (ms / 1e3) / 1e9, 3), "unit": "GUPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "strong" if not args.rows else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (analytic 3-D Shepp-Logan raw counts generated on device per sub-slab)",
+            "config": {"workload": workload_desc(cfg), "volume": [n, n, n], "n_proj": n_proj,
+                       "mode": f"z-sub-slab streaming ({S} rows), uint16 volume D2H into a 2-slab pinned ring",
+                       "rows_per_gpu": r1 - r0, "sample": bool(args.rows),
+                       "s_per_volume_extrapolated": round(ms / 1e3 * n / rows_all, 2)},
+            "roofline": {"bound": "smem", "kernel": "bp_kernel (K2)",
+                         "bp_gups_full_count": round(bp_upd / (bp_ms / 1e3) / 1e9, 1)},
+            "clocks": clk, "gpu_launches": 5 * len(bp_events) // max(1, args.steps) * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg)
+        return
+    if args.stream or cfg["n"] >= 4096 and int(os.environ.get("WORLD_SIZE", "1")) * 180e9 < 2.2 * 4 * cfg["n"] ** 3:
+        import torch
+        import torch.distributed as dist
+
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+        if world > 1:
+            dist.init_process_group("nccl", device_id=dev)
+        run_streamed(args, cfg, world, rank, local, dev)
         return
 
     import numpy as np
