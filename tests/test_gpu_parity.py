@@ -612,3 +612,30 @@ def test_cli_reconstruct(F, golden, tmp_path):
     assert r.returncode == 0, r.stderr
     vol, _ = formats.read_vol(tmp_path / "o" / "volume.vol")
     assert np.abs(vol.astype(int) - g["pipe_q"].astype(int)).max() <= 2
+
+
+@pytest.mark.parametrize("n,n_proj", [(4096, 3600), (8192, 7200)])
+def test_large_detector_parity_c4_c5(F, n, n_proj):
+    """Configs C4 / C5 geometry (4096^2 x 3600, 8192^2 x 7200): one detector
+    row, centre 256^2 tile vs the float64 oracle.  This is where a plain fp32
+    detector coordinate fails 1e-5; K2's fp64 tile origin keeps
+    it ~1e-6."""
+    from oracle import c_oracle as C
+    from oracle import fbp_oracle as O
+    from paper_2505_13955_b200.engine import SlabReconstructor
+    from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
+
+    pitch, row = 12.0, n // 2 + 7
+    p = AcquisitionParams(n_proj=n_proj, n_rows=n, n_chan=n, pixel_pitch=pitch)
+    d = VolumeDims(n, n, n, voxel_pitch=pitch)
+    raw = _phantom_rows(p, d, row, row + 1)
+    vol = SlabReconstructor(p, d, i0=1e5, rows=(row, row + 1)).run(raw)
+    t0 = (n - 256) // 2
+    got = vol[0, t0:t0 + 256, t0:t0 + 256].cpu().numpy().astype(np.float64)
+    raw_h = raw.cpu().numpy()
+    filt = O.ramp_filter(O.preprocess(raw_h, 1e5), pixel_pitch=pitch)
+    geom = O.make_geom(n_proj, 1, n, pixel_pitch=pitch, voxel_pitch=pitch)
+    ref = C.back_project(filt, geom, tile=(t0, t0 + 256, t0, t0 + 256))[0, t0:t0 + 256, t0:t0 + 256]
+    err = rel_l2(got, ref)
+    print(f"{n}^2 x {n_proj}, row {row}: rel_l2 {err:.2e} max_abs {np.abs(got - ref).max():.2e}")
+    assert err <= REL_L2
