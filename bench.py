@@ -458,9 +458,11 @@ def main():
 
     from paper_2505_13955_b200._lib import TF_BP_FINALIZE, lib as _tf_lib
 
-    bpu = ctypes.c_double()
-    _tf_lib().tf_bp_smem_bytes_per_update(slab.bplan.handle, TF_BP_FINALIZE, ctypes.byref(bpu))
+    bpu, exe = ctypes.c_double(), ctypes.c_int64()
+    _tf_lib().tf_bp_kernel_info(slab.bplan.handle, TF_BP_FINALIZE, k_rows, 0, n_proj, ctypes.byref(bpu),
+                                ctypes.byref(exe))
     bytes_per_update = bpu.value
+    exec_upd = exe.value  # the library's own count: FoV-active tiles x tile voxels x padded rows x angles
     smem_achieved = exec_upd * bytes_per_update / (bp_avg_ms / 1e3) / 1e9
     fp32_peak_tflops = 128 * 2 * SM_COUNT * sm_mhz * 1e6 / 1e12
     fp32_achieved = exec_upd * 4 / (bp_avg_ms / 1e3) / 1e12

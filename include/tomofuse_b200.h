@@ -166,6 +166,11 @@ TF_API int tf_backproject(const tf_bp_plan* plan, const void* stage, int n_rows,
  * update for these flags (8 = 2-tap, 6 = x-pair 3-tap, 4 = 2x2 4-tap): the
  * algorithmic numerator of K2's roofline. */
 TF_API int tf_bp_smem_bytes_per_update(const tf_bp_plan* plan, int flags, double* bytes);
+/* Same, plus the voxel x projection updates K2 executes for a full-volume
+ * call over n_rows rows and angles [a0, a1) (FoV-skipped tiles excluded,
+ * rows padded to the 32-row z-block): the roofline's work count. */
+TF_API int tf_bp_kernel_info(const tf_bp_plan* plan, int flags, int n_rows, int a0, int a1, double* bytes,
+                             int64_t* executed_updates);
 
 /* ---- quantize (fbp.py:255-259) ------------------------------------------ */
 /* vol is fp32 or fp64 (vol_dtype); arithmetic is fp64, round-half-even,

@@ -36,7 +36,8 @@ struct tf_bp_plan {
     double2* d_trig;  // (cos, sin) of k * (span / n_proj), fp64 libm, per angle
     float* d_w;       // feather weights (fp32, as numpy casts them)
     double ext;       // max channel extent of a tile's rays over all angles
-    int* d_order;     // launch order of the tiles (Morton, FoV-active first)
+    int* d_order[2];  // launch order of the tiles (Morton, FoV-active first): 16x16, 32x16 tiles
+    int n_active[2];
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
 };
@@ -44,7 +45,6 @@ struct tf_bp_plan {
 namespace tf {
 namespace {
 
-constexpr int TX = 16, TY = 16;           // voxel columns per CTA tile
 
 // Consumer layouts.  A thread owns a VX x VY block of voxel columns and ZT of
 // the tile's 32 rows.  NT detector taps per block serve all its voxels:
@@ -56,8 +56,9 @@ constexpr int TX = 16, TY = 16;           // voxel columns per CTA tile
 //       two live taps and 0 elsewhere, so the FMA sequence -- and the result
 //       -- is bit-identical to V1.
 template <int VX, int VY, int NT, int ZT, int STAGES_ = 3, int APS_ = 4, bool PIPE_ = false, int MINB_ = 2,
-          int PW_ = 4, bool ROLE_ = false>
+          int PW_ = 4, bool ROLE_ = false, int TX_ = 16, int TY_ = 16>
 struct Layout {
+    static constexpr int TX = TX_, TY = TY_;  // voxel columns per CTA tile
     // ROLE (2x2, 4 taps): per angle the block voxel with the smallest t is
     // the "base" (its taps are exactly 0,1); its x-, y- and diagonal
     // neighbours need taps 0..2, 0..2 and 0..3.  Accumulating each voxel only
@@ -139,6 +140,7 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     bp_kernel(const __grid_constant__ CUtensorMap map, const BPArgs args) {
     constexpr int VX = L::VX_, VY = L::VY_, NT = L::NT_, ZT = L::ZT_;
     constexpr int STAGES = L::STAGES, APS = L::APS;
+    constexpr int TX = L::TX, TY = L::TY;
     extern __shared__ __align__(128) uint8_t smem[];
     // CTAs launch in blockIdx order and the resident set is a sliding window of
     // ~3 x 148 consecutive entries: a Morton order makes that window a compact
@@ -506,12 +508,15 @@ using P3Cfg6 = Layout<2, 1, 3, 32, 8, 2, true, 3, 2>;
 using P3Cfg7 = Layout<2, 1, 3, 32, 8, 2, false, 3, 2>;
 using Q4Cfg8 = Layout<2, 2, 4, 16, 8, 2, true, 3, 2, true>;
 using Q4Cfg9 = Layout<2, 2, 4, 16, 8, 2, false, 3, 2, true>;
+// 2x2 role kernel with a full 32-row column per thread (128 accumulators) on
+// a 32x16 tile: setup amortised over 128 updates, 4 B smem + 3 FMA per update
+using Q4Cfg10 = Layout<2, 2, 4, 32, 8, 2, true, 2, 2, true, 32, 16>;
 
 int default_variant() {
     static int v = [] {
         const char* e = getenv("TF_BP_VARIANT");  // benchmarking knob: 1..4
         int x = e ? atoi(e) : 0;
-        return (x >= 1 && x <= 9) ? x : 6;
+        return (x >= 1 && x <= 10) ? x : 6;
     }();
     return v;
 }
@@ -589,8 +594,8 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     p->g = *g;
     p->feather_band = feather_band;
     p->scale = g->voxel_pitch / g->pixel_pitch;
-    // window: max over angles of the tile's channel extent + taps + floor slack
-    p->ext = std::sqrt((double)(TX - 1) * (TX - 1) + (double)(TY - 1) * (TY - 1)) * p->scale;
+    // window: max over angles of a 16x16 tile's channel extent + taps + floor slack
+    p->ext = std::sqrt(15.0 * 15.0 * 2) * p->scale;
     if (bp_smem_bytes<V1Cfg>((kRowBytes * (int)std::ceil(p->ext + 3.0) + 127) / 128 * 128) > 227 * 1024) {
         delete p;
         return set_error(TF_ERR_UNSUPPORTED, "voxel/pixel pitch ratio %.3g too large for the tile window",
@@ -605,34 +610,40 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     p->sc2 = p->scale * p->scale;
     const double step = g->angle_span / g->n_proj;
     p->angle_wf = (float)step;
-    // tile launch order: FoV-active tiles (same fp64 test as the kernel's
-    // early-out) in Morton order, then the inactive ones (they exit at once)
-    const int ntx = (g->nx + TX - 1) / TX, nty = (g->ny + TY - 1) / TY;
-    std::vector<int> act, inact;
-    for (int t = 0; t < ntx * nty; ++t) {
-        const int X0 = (t % ntx) * TX, Y0 = (t / ntx) * TY;
-        const int xe = std::min(X0 + TX, g->nx), ye = std::min(Y0 + TY, g->ny);
-        const int nxv = (int)std::min(std::max(std::nearbyint(p->cx), (double)X0), (double)(xe - 1));
-        const int nyv = (int)std::min(std::max(std::nearbyint(p->cy), (double)Y0), (double)(ye - 1));
-        bool all_out = true;
-        for (int ddx = -1; ddx <= 1; ++ddx)
-            for (int ddy = -1; ddy <= 1; ++ddy) {
-                const int xx = std::min(std::max(nxv + ddx, X0), xe - 1), yy = std::min(std::max(nyv + ddy, Y0), ye - 1);
-                volatile double dx = (double)xx - p->cx, dy = (double)yy - p->cy;
-                volatile double s2 = dx * dx;
-                volatile double t2 = dy * dy;
-                volatile double rr = (s2 + t2) * p->sc2;
-                all_out = all_out && (rr > p->R2);
-            }
-        (all_out ? inact : act).push_back(t);
+    // tile launch order per tile shape: FoV-active tiles (same fp64 test as
+    // the kernel's early-out) in Morton order, then the inactive ones
+    std::vector<int> orders[2];
+    for (int shape = 0; shape < 2; ++shape) {
+        const int TXs = shape ? 32 : 16, TYs = 16;
+        const int ntx = (g->nx + TXs - 1) / TXs, nty = (g->ny + TYs - 1) / TYs;
+        std::vector<int> act, inact;
+        for (int t = 0; t < ntx * nty; ++t) {
+            const int X0 = (t % ntx) * TXs, Y0 = (t / ntx) * TYs;
+            const int xe = std::min(X0 + TXs, g->nx), ye = std::min(Y0 + TYs, g->ny);
+            const int nxv = (int)std::min(std::max(std::nearbyint(p->cx), (double)X0), (double)(xe - 1));
+            const int nyv = (int)std::min(std::max(std::nearbyint(p->cy), (double)Y0), (double)(ye - 1));
+            bool all_out = true;
+            for (int ddx = -1; ddx <= 1; ++ddx)
+                for (int ddy = -1; ddy <= 1; ++ddy) {
+                    const int xx = std::min(std::max(nxv + ddx, X0), xe - 1), yy = std::min(std::max(nyv + ddy, Y0), ye - 1);
+                    volatile double dx = (double)xx - p->cx, dy = (double)yy - p->cy;
+                    volatile double s2 = dx * dx;
+                    volatile double t2 = dy * dy;
+                    volatile double rr = (s2 + t2) * p->sc2;
+                    all_out = all_out && (rr > p->R2);
+                }
+            (all_out ? inact : act).push_back(t);
+        }
+        auto morton = [&](int t) {
+            unsigned x = (unsigned)(t % ntx), y = (unsigned)(t / ntx), m = 0;
+            for (int b = 0; b < 16; ++b) m |= ((x >> b) & 1u) << (2 * b) | ((y >> b) & 1u) << (2 * b + 1);
+            return m;
+        };
+        std::stable_sort(act.begin(), act.end(), [&](int a, int b) { return morton(a) < morton(b); });
+        p->n_active[shape] = (int)act.size();
+        act.insert(act.end(), inact.begin(), inact.end());
+        orders[shape] = act;
     }
-    auto morton = [&](int t) {
-        unsigned x = (unsigned)(t % ntx), y = (unsigned)(t / ntx), m = 0;
-        for (int b = 0; b < 16; ++b) m |= ((x >> b) & 1u) << (2 * b) | ((y >> b) & 1u) << (2 * b + 1);
-        return m;
-    };
-    std::stable_sort(act.begin(), act.end(), [&](int a, int b) { return morton(a) < morton(b); });
-    act.insert(act.end(), inact.begin(), inact.end());
     std::vector<double2> trig(g->n_proj);
     for (int k = 0; k < g->n_proj; ++k) {  // theta_k = k * (span / n_proj), geometry.py:69-70
         const double th = (double)k * step;
@@ -641,8 +652,11 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     std::vector<float> wf(g->n_chan);
     for (int i = 0; i < g->n_chan; ++i) wf[i] = (float)w[i];
     cudaError_t e = cudaMalloc(&p->d_trig, sizeof(double2) * g->n_proj);
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_order, sizeof(int) * act.size());
-    if (e == cudaSuccess) e = cudaMemcpy(p->d_order, act.data(), sizeof(int) * act.size(), cudaMemcpyHostToDevice);
+    for (int s = 0; s < 2 && e == cudaSuccess; ++s) {
+        e = cudaMalloc(&p->d_order[s], sizeof(int) * orders[s].size());
+        if (e == cudaSuccess)
+            e = cudaMemcpy(p->d_order[s], orders[s].data(), sizeof(int) * orders[s].size(), cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess) e = cudaMalloc(&p->d_w, sizeof(float) * g->n_chan);
     if (e == cudaSuccess)
         e = cudaMemcpy(p->d_trig, trig.data(), sizeof(double2) * g->n_proj, cudaMemcpyHostToDevice);
@@ -659,7 +673,8 @@ extern "C" int tf_bp_plan_destroy(tf_bp_plan* p) {
     if (!p) return TF_OK;
     cudaFree(p->d_trig);
     cudaFree(p->d_w);
-    cudaFree(p->d_order);
+    cudaFree(p->d_order[0]);
+    cudaFree(p->d_order[1]);
     delete p;
     return TF_OK;
 }
@@ -703,7 +718,10 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     // kernel variant: the 2x2-block 4-tap gather needs the block's rays to span
     // < 2 channels (sqrt(2) * voxel/pixel pitch ratio); else the 2-tap kernel
     const int variant = select_variant(p, flags);
-    const int W = (int)std::ceil(p->ext + (variant == 0 ? 3.0 : 4.0));
+    const int shape = variant == 10 ? 1 : 0;  // 32x16 tiles for the Q32 variant
+    const int TXv = shape ? 32 : 16, TYv = 16;
+    const double ext = std::sqrt((double)(TXv - 1) * (TXv - 1) + (double)(TYv - 1) * (TYv - 1)) * p->scale;
+    const int W = (int)std::ceil(ext + (variant == 0 ? 3.0 : 4.0));
 
     PFN_encodeTiled_t enc = encode_fn();
     if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
@@ -719,7 +737,7 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
 
     BPArgs a{};
     a.trig = p->d_trig;
-    a.order = tile_order_enabled() ? p->d_order : nullptr;
+    a.order = tile_order_enabled() ? p->d_order[shape] : nullptr;
     a.vol = vol;
     a.a0 = a0;
     a.a1 = a1;
@@ -732,7 +750,7 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     a.x1 = x1;
     a.y0 = y0;
     a.y1 = y1;
-    a.ntx = (g.nx + TX - 1) / TX;
+    a.ntx = (g.nx + TXv - 1) / TXv;
     a.W = W;
     a.slot_bytes = ((kRowBytes * W) + 127) / 128 * 128;
     a.flags = flags;
@@ -743,7 +761,7 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     a.R2 = p->R2;
     a.sc2 = p->sc2;
     a.angle_wf = p->angle_wf;
-    const int nty = (g.ny + TY - 1) / TY;
+    const int nty = (g.ny + TYv - 1) / TYv;
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)nzb);
     int st;
     switch (variant) {
@@ -756,10 +774,23 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
         case 6: st = launch_bp<P3Cfg6>(map, a, grid, stream); break;
         case 7: st = launch_bp<P3Cfg7>(map, a, grid, stream); break;
         case 8: st = launch_bp<Q4Cfg8>(map, a, grid, stream); break;
-        default: st = launch_bp<Q4Cfg9>(map, a, grid, stream); break;
+        case 9: st = launch_bp<Q4Cfg9>(map, a, grid, stream); break;
+        default: st = launch_bp<Q4Cfg10>(map, a, grid, stream); break;
     }
     if (st) return st;
     return check_launch("bp_kernel");
+}
+
+extern "C" int tf_bp_kernel_info(const tf_bp_plan* p, int flags, int n_rows, int a0, int a1, double* bytes,
+                                 int64_t* executed_updates) {
+    if (!p || !bytes || !executed_updates) return set_error(TF_ERR_INVALID_ARGUMENT, "null argument");
+    const int v = select_variant(p, flags);
+    *bytes = v == 0 ? 8.0 : ((v >= 5 && v <= 7) ? 6.0 : 4.0);
+    const int shape = v == 10 ? 1 : 0;
+    const int64_t tile_vox = shape ? 32 * 16 : 16 * 16;
+    const int64_t rows = (int64_t)((n_rows + kZB - 1) / kZB) * kZB;
+    *executed_updates = (int64_t)p->n_active[shape] * tile_vox * rows * (int64_t)(a1 - a0);
+    return TF_OK;
 }
 
 extern "C" int tf_bp_smem_bytes_per_update(const tf_bp_plan* p, int flags, double* bytes) {

@@ -33,8 +33,10 @@ for _ in range(a.reps):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.reps
-import bench
-exec_upd, _ = bench.executed_updates(d, a.proj, a.rows)
+import ctypes
+bpu, exe = ctypes.c_double(), ctypes.c_int64()
+_lib.lib().tf_bp_kernel_info(eng.bplan.handle, flags, a.rows, 0, a.proj, ctypes.byref(bpu), ctypes.byref(exe))
+exec_upd = exe.value
 ref = eng.backproject(flags=_lib.TF_BP_FINALIZE | _lib.TF_BP_KERNEL_V1).clone()
 out = eng.backproject(flags=flags)
 rel = float((out - ref).norm() / ref.norm())
