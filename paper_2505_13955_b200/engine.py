@@ -162,6 +162,27 @@ class StreamedReconstructor:
             self.s_comp = torch.cuda.Stream(self.device)
             self.s_d2h = torch.cuda.Stream(self.device)
 
+    def sub_slabs(self, R0, R1):
+        """Sub-slab boundaries: full `slab_rows` slabs in the middle, with the
+        first and last slab cut to a quarter (32-row aligned) so that the
+        un-overlapped pipeline fill (first H2D) and drain (last D2H) are short."""
+        S = self.slab_rows
+        edge = max(32, (S // 4) // 32 * 32) if S >= 64 else S
+        cuts, r = [], R0
+        if R1 - R0 > 2 * S:
+            cuts.append((r, r + edge))
+            r += edge
+            tail = R1 - edge
+            while r < tail:
+                cuts.append((r, min(r + S, tail)))
+                r = cuts[-1][1]
+            cuts.append((r, R1))
+        else:
+            while r < R1:
+                cuts.append((r, min(r + S, R1)))
+                r = cuts[-1][1]
+        return cuts
+
     def _copy2d(self, dst, dpitch, src, spitch, width, height, stream):
         check(lib().tf_copy2d_async(ctypes.c_void_p(dst), dpitch, ctypes.c_void_p(src), spitch, width, height,
                                     ctypes.c_void_p(stream.cuda_stream)))
@@ -187,9 +208,7 @@ class StreamedReconstructor:
         raw_free = [None, None]
         vol_free = [None, None]
         done = None
-        starts = list(range(R0, R1, self.slab_rows))
-        for i, r0 in enumerate(starts):
-            r1 = min(r0 + self.slab_rows, R1)
+        for i, (r0, r1) in enumerate(self.sub_slabs(R0, R1)):
             k = r1 - r0
             b = i % 2
             # H2D: rows [r0, r1) of every angle (n_proj strided chunks)
