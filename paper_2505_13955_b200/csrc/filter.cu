@@ -33,6 +33,7 @@ struct tf_filter_plan {
     int max_grid;      // persistent grid: resident CTAs per SM x SMs
     const void* kernel;  // ramp_filter_kernel instantiation for this P
     bool fused;          // fused-I/O FFT path
+    int mode;            // 0 generic, 1 fused radix-16, 2 fused radix-8
 };
 
 namespace tf {
@@ -195,9 +196,10 @@ __device__ __forceinline__ void dft16_ip(float2 (&v)[16]) {
 enum { IN_SMEM = 0, IN_GLOBAL = 1 };
 enum { OUT_SMEM = 0, OUT_MULT = 1, OUT_GLOBAL = 2 };
 
-template <int R, int NB, int IN, int OUT, class Load, class Store>
+template <int R, int NB, int IN, int OUT, class Load, class Store, int PADS = 4>
 __device__ __forceinline__ void fft_pass(float2* buf, const float2* tw, int P, int Ns, int n, int tid, int T,
                                          const Load& load, const float* __restrict__ mult, const Store& store) {
+    auto pad = [](int i) { return i + (i >> PADS); };  // 1 float2 of padding per 2^PADS
     float2 v[NB][R];
     const int nb = P / R;
 #pragma unroll
@@ -209,7 +211,7 @@ __device__ __forceinline__ void fft_pass(float2* buf, const float2* tw, int P, i
             for (int r = 0; r < R; ++r) {
                 float2 x;
                 if constexpr (IN == IN_GLOBAL) x = (r < R / 2) ? load(j + r * nb) : make_float2(0.f, 0.f);
-                else x = buf[pad_idx(j + r * nb)];
+                else x = buf[pad(j + r * nb)];
                 if (r > 0 && Ns > 1) x = cmul(x, tw[r * Ns + k]);
                 v[b][r] = x;
             }
@@ -229,11 +231,11 @@ __device__ __forceinline__ void fft_pass(float2* buf, const float2* tw, int P, i
                 const int m = base + r * Ns;
                 const float2 x = v[b][R == 16 ? dft16_pos(r) : r];
                 if constexpr (OUT == OUT_SMEM) {
-                    buf[pad_idx(m)] = x;
+                    buf[pad(m)] = x;
                 } else if constexpr (OUT == OUT_MULT) {
                     // X <- conj(X * M / P): the inverse transform is conj(FFT(conj(.)))
                     const float g = __ldg(&mult[m <= P / 2 ? m : P - m]);
-                    buf[pad_idx(m)] = make_float2(x.x * g, -x.y * g);
+                    buf[pad(m)] = make_float2(x.x * g, -x.y * g);
                 } else {
                     if (m < n) store(m, x);
                 }
@@ -247,6 +249,14 @@ __device__ __forceinline__ void fft_pass(float2* buf, const float2* tw, int P, i
 // Fused path (P >= 256, no blur): radix 16, then the remainder, then radix
 // 16 -- so the first pass (global input, pruned zero half) and the last
 // pass (global output, pruned half) are always radix 16.
+std::vector<int> radix_plan8(int log2P) {  // fused radix-8 path: 8, remainder, 8, 8, ...
+    std::vector<int> rs{8};
+    const int tail = log2P % 3;
+    if (tail) rs.push_back(1 << tail);
+    for (int i = 1; i < log2P / 3; ++i) rs.push_back(8);
+    return rs;
+}
+
 std::vector<int> radix_plan(int log2P, bool fused) {
     std::vector<int> rs;
     const int tail = log2P % 4;
@@ -299,6 +309,41 @@ __device__ __forceinline__ void fft_smem(float2* buf, const float2* tw, int P, i
     if (rem == 3) fft_pass<8, 2, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, P, tid, T, io, nullptr, io);
     else if (rem == 2) fft_pass<4, 4, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, P, tid, T, io, nullptr, io);
     else if (rem == 1) fft_pass<2, 8, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, P, tid, T, io, nullptr, io);
+}
+
+// Fused radix-8 path (radix_plan8, 64 <= P <= 8192, T = P/8 threads): as
+// fft_fused but with 8-point butterflies -- 8 complex values per thread, so
+// a 64-register budget holds 2 CTAs x 512 threads per SM (twice the warps of
+// the radix-16 path), 1-in-8 padding keeps the radix-8 patterns conflict-free.
+template <class Load, class Store>
+__device__ __forceinline__ void fft_fused8(float2* buf, const float2* tw0, int P, int log2P, int n, int tid, int T,
+                                           const Load& load, const float* mult, const Store& store) {
+    const int tail = log2P % 3;
+    const int n8 = log2P / 3;  // >= 2
+    for (int dir = 0; dir < 2; ++dir) {
+        const float2* tw = tw0;
+        int Ns = 1;
+        if (dir == 0) fft_pass<8, 1, IN_GLOBAL, OUT_SMEM, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+        else fft_pass<8, 1, IN_SMEM, OUT_SMEM, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+        Ns = 8;
+        if (tail == 2) {
+            fft_pass<4, 2, IN_SMEM, OUT_SMEM, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+            tw += 4 * Ns;
+            Ns *= 4;
+        } else if (tail == 1) {
+            fft_pass<2, 4, IN_SMEM, OUT_SMEM, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+            tw += 2 * Ns;
+            Ns *= 2;
+        }
+        for (int p = 1; p < n8; ++p) {
+            const bool last = p == n8 - 1;
+            if (!last) fft_pass<8, 1, IN_SMEM, OUT_SMEM, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+            else if (dir == 0) fft_pass<8, 1, IN_SMEM, OUT_MULT, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+            else fft_pass<8, 1, IN_SMEM, OUT_GLOBAL, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
+            tw += 8 * Ns;
+            Ns *= 8;
+        }
+    }
 }
 
 // Fused path (radix_plan(.., true), P >= 256): forward with the input load
@@ -368,8 +413,8 @@ __device__ __forceinline__ float* out_ptr(long long l, int n, const OutMap& m, c
 
 // Persistent: each CTA loops over line pairs; the twiddle table is loaded
 // into shared memory once per CTA.
-template <bool SMEM_TW, int MAXT, bool FUSED>
-__global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kernel(const float* __restrict__ in, float* out,
+template <bool SMEM_TW, int MAXT, int MODE>
+__global__ void __launch_bounds__(MAXT, (MODE == 2 ? 1024 / MAXT : (MAXT <= 256 ? 2 : 1))) ramp_filter_kernel(const float* __restrict__ in, float* out,
                                                            long long n_lines, int n, int P, int log2P,
                                                            const float2* __restrict__ tw_g,
                                                            const float* __restrict__ mult,
@@ -388,7 +433,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kerne
     const float2* tw = tw_g;
     float2* data = sbuf;
     if constexpr (SMEM_TW) {
-        float2* tws = sbuf + (P + P / 16);
+        float2* tws = sbuf + (MODE == 2 ? P + P / 8 : P + P / 16);
         for (int m = tid; m < n_tw; m += T) tws[m] = tw_g[m];
         tw = tws;  // visible after the first __syncthreads below
     }
@@ -432,7 +477,9 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kerne
             }
         };
 
-        if constexpr (FUSED) {
+        if constexpr (MODE == 2) {
+            fft_fused8(data, tw, P, log2P, n, tid, T, load, mult, store);
+        } else if constexpr (MODE == 1) {
             fft_fused(data, tw, P, log2P, n, tid, T, load, mult, store);
         } else {
             __syncthreads();  // previous pair may still read data[]
@@ -522,8 +569,18 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
     p->P = P;
     p->log2P = ilog2(P);
     p->threads = std::max(32, P / 16);  // one radix-16 butterfly per thread (P <= 16384 -> <= 1024)
-    p->fused = p->log2P >= 8 && blur_sigma <= 0;  // I/O folded into the first/last FFT passes
-    std::vector<float2> tw = twiddle_tables(radix_plan(p->log2P, p->fused));
+    // K1 variant: fused radix-8 (64 <= P <= 8192), fused radix-16 (P = 16384 or
+    // TF_FILTER_MODE=1), generic smem path with the optional blur
+    const char* fm = getenv("TF_FILTER_MODE");
+    p->mode = blur_sigma > 0 ? 0 : (P >= 64 && P <= 8192 ? 2 : (p->log2P >= 8 ? 1 : 0));
+    if (fm && blur_sigma <= 0) {
+        const int want = atoi(fm);
+        if (want == 0 || (want == 1 && p->log2P >= 8) || (want == 2 && P >= 64 && P <= 8192)) p->mode = want;
+    }
+    p->fused = p->mode != 0;
+    if (p->mode == 2) p->threads = std::max(32, P / 8);
+    std::vector<float2> tw =
+        twiddle_tables(p->mode == 2 ? radix_plan8(p->log2P) : radix_plan(p->log2P, p->mode == 1));
     p->n_tw = (int)tw.size();
     std::vector<double> mult(P / 2 + 1);
     multiplier_fp64(kind, P, pixel_pitch, mult.data());
@@ -552,15 +609,19 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
     if (e == cudaSuccess && rad > 0)
         e = cudaMemcpy(p->d_blur, bw.data(), sizeof(float) * (2 * rad + 1), cudaMemcpyHostToDevice);
     p->smem_tw = P <= 8192;  // twiddle table in shared memory next to the line buffer
-    p->smem = (P + P / 16 + (p->smem_tw ? p->n_tw : 0)) * (int)sizeof(float2);
-    if (p->fused)
-        p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256, true>
-                    : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512, true>
-                                        : (const void*)ramp_filter_kernel<false, 1024, true>;
+    p->smem = ((p->mode == 2 ? P + P / 8 : P + P / 16) + (p->smem_tw ? p->n_tw : 0)) * (int)sizeof(float2);
+    if (p->mode == 2)
+        p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256, 2>
+                    : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512, 2>
+                                        : (const void*)ramp_filter_kernel<true, 1024, 2>;
+    else if (p->mode == 1)
+        p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256, 1>
+                    : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512, 1>
+                                        : (const void*)ramp_filter_kernel<false, 1024, 1>;
     else
-        p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256, false>
-                    : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512, false>
-                                        : (const void*)ramp_filter_kernel<false, 1024, false>;
+        p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256, 0>
+                    : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512, 0>
+                                        : (const void*)ramp_filter_kernel<false, 1024, 0>;
     // the attribute is per-function global state shared by every plan: raise it
     // to the device's opt-in maximum (never lower it to this plan's size)
     if (e == cudaSuccess) {
