@@ -196,10 +196,10 @@ __device__ __forceinline__ void dft16_ip(float2 (&v)[16]) {
 enum { IN_SMEM = 0, IN_GLOBAL = 1 };
 enum { OUT_SMEM = 0, OUT_MULT = 1, OUT_GLOBAL = 2 };
 
-template <int R, int NB, int IN, int OUT, class Load, class Store, int PADS = 4>
+template <int R, int NB, int IN, int OUT, class Load, class Store>
 __device__ __forceinline__ void fft_pass(float2* buf, const float2* tw, int P, int Ns, int n, int tid, int T,
                                          const Load& load, const float* __restrict__ mult, const Store& store) {
-    auto pad = [](int i) { return i + (i >> PADS); };  // 1 float2 of padding per 2^PADS
+    auto pad = [](int i) { return pad_idx(i); };
     float2 v[NB][R];
     const int nb = P / R;
 #pragma unroll
@@ -311,41 +311,6 @@ __device__ __forceinline__ void fft_smem(float2* buf, const float2* tw, int P, i
     else if (rem == 1) fft_pass<2, 8, IN_SMEM, OUT_SMEM>(buf, tw, P, Ns, P, tid, T, io, nullptr, io);
 }
 
-// Fused radix-8 path (radix_plan8, 64 <= P <= 8192, T = P/8 threads): as
-// fft_fused but with 8-point butterflies -- 8 complex values per thread, so
-// a 64-register budget holds 2 CTAs x 512 threads per SM (twice the warps of
-// the radix-16 path), 1-in-8 padding keeps the radix-8 patterns conflict-free.
-template <class Load, class Store>
-__device__ __forceinline__ void fft_fused8(float2* buf, const float2* tw0, int P, int log2P, int n, int tid, int T,
-                                           const Load& load, const float* mult, const Store& store) {
-    const int tail = log2P % 3;
-    const int n8 = log2P / 3;  // >= 2
-    for (int dir = 0; dir < 2; ++dir) {
-        const float2* tw = tw0;
-        int Ns = 1;
-        if (dir == 0) fft_pass<8, 1, IN_GLOBAL, OUT_SMEM, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
-        else fft_pass<8, 1, IN_SMEM, OUT_SMEM, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
-        Ns = 8;
-        if (tail == 2) {
-            fft_pass<4, 2, IN_SMEM, OUT_SMEM, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
-            tw += 4 * Ns;
-            Ns *= 4;
-        } else if (tail == 1) {
-            fft_pass<2, 4, IN_SMEM, OUT_SMEM, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
-            tw += 2 * Ns;
-            Ns *= 2;
-        }
-        for (int p = 1; p < n8; ++p) {
-            const bool last = p == n8 - 1;
-            if (!last) fft_pass<8, 1, IN_SMEM, OUT_SMEM, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
-            else if (dir == 0) fft_pass<8, 1, IN_SMEM, OUT_MULT, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
-            else fft_pass<8, 1, IN_SMEM, OUT_GLOBAL, Load, Store, 3>(buf, tw, P, Ns, n, tid, T, load, mult, store);
-            tw += 8 * Ns;
-            Ns *= 8;
-        }
-    }
-}
-
 // Fused path (radix_plan(.., true), P >= 256): forward with the input load
 // and the spectrum multiply folded into its first / last pass, then the
 // inverse with the store folded into its last pass.
@@ -414,7 +379,7 @@ __device__ __forceinline__ float* out_ptr(long long l, int n, const OutMap& m, c
 // Persistent: each CTA loops over line pairs; the twiddle table is loaded
 // into shared memory once per CTA.
 template <bool SMEM_TW, int MAXT, int MODE>
-__global__ void __launch_bounds__(MAXT, (MODE == 2 ? 1024 / MAXT : (MAXT <= 256 ? 2 : 1))) ramp_filter_kernel(const float* __restrict__ in, float* out,
+__global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kernel(const float* __restrict__ in, float* out,
                                                            long long n_lines, int n, int P, int log2P,
                                                            const float2* __restrict__ tw_g,
                                                            const float* __restrict__ mult,
@@ -430,10 +395,11 @@ __global__ void __launch_bounds__(MAXT, (MODE == 2 ? 1024 / MAXT : (MAXT <= 256 
 #pragma unroll
         for (int s = 0; s < 8; ++s) s_dst[s] = map.dst[s];
     }
+    __syncthreads();  // s_row0 / s_dst are read by every thread's out_ptr
     const float2* tw = tw_g;
     float2* data = sbuf;
     if constexpr (SMEM_TW) {
-        float2* tws = sbuf + (MODE == 2 ? P + P / 8 : P + P / 16);
+        float2* tws = sbuf + P + P / 16;
         for (int m = tid; m < n_tw; m += T) tws[m] = tw_g[m];
         tw = tws;  // visible after the first __syncthreads below
     }
@@ -477,9 +443,7 @@ __global__ void __launch_bounds__(MAXT, (MODE == 2 ? 1024 / MAXT : (MAXT <= 256 
             }
         };
 
-        if constexpr (MODE == 2) {
-            fft_fused8(data, tw, P, log2P, n, tid, T, load, mult, store);
-        } else if constexpr (MODE == 1) {
+        if constexpr (MODE == 1) {
             fft_fused(data, tw, P, log2P, n, tid, T, load, mult, store);
         } else {
             __syncthreads();  // previous pair may still read data[]
@@ -521,6 +485,231 @@ __global__ void __launch_bounds__(MAXT, (MODE == 2 ? 1024 / MAXT : (MAXT <= 256 
             fft_smem(data, tw, P, log2P, tid, T);
             for (int m = tid; m < n; m += T) store(m, data[pad_idx(m)]);
         }
+    }
+}
+
+// ----------------------------------------------------------- K1, radix-8 (mode 2)
+// Compile-time-shaped variant for 256 <= P <= 8192: T = P/8 threads per line
+// pair, one radix-8 butterfly per thread per pass, every stride, twiddle
+// offset and buffer a constant.  Two ping-pong line buffers: a pass reads one
+// and writes the other, so it needs no barrier between its reads and writes
+// and no butterfly value is live across a barrier (64 registers, no spills,
+// 2 CTAs x 512 threads per SM at P = 4096).  Instead of padding, an XOR
+// swizzle inside each 16-element block,
+//     sw8(i) = i ^ ((i >> 4) & 7) ^ (((i >> 6) & 1) << 3),
+// maps every radix-8 access pattern of a half-warp (consecutive, stride 8 and
+// the 64-blocks of pass 2) onto 16 distinct 8-byte bank pairs.  sw8 is linear
+// over GF(2), so for an index a | c with disjoint bit fields
+// sw8(a | c) = sw8(a) ^ sw8(c): per butterfly leg sw8(c) is a constant, and
+// an immediate address offset wherever it cannot overlap sw8(a)'s bits.
+__host__ __device__ constexpr int sw8(int i) { return i ^ ((i >> 4) & 7) ^ (((i >> 6) & 1) << 3); }
+
+// a_sw = sw8(a) for an index a confined to the bits of `amask`; c a constant
+// with bits disjoint from amask
+__device__ __forceinline__ int sw8_join(int a_sw, int amask, int c) {
+    const int cs = sw8(c);
+    return (cs & (amask | 15)) == 0 ? a_sw + cs : a_sw ^ cs;
+}
+
+template <int LOG2P>
+struct R8Plan {
+    static constexpr int P = 1 << LOG2P, T = P / 8, TAIL = LOG2P % 3, N8 = LOG2P / 3, NP = N8 + (TAIL > 0);
+    // the pass sequence of radix_plan8: 8, [2^TAIL], 8, 8, ...
+    static constexpr int radix(int i) { return i == 0 ? 8 : (TAIL && i == 1) ? (1 << TAIL) : 8; }
+    static constexpr int ns(int i) {
+        int s = 1;
+        for (int q = 0; q < i; ++q) s *= radix(q);
+        return s;
+    }
+    static constexpr int twoff(int i) {  // offset of pass i's [r][k] table in twiddle_tables()
+        int o = 0;
+        for (int q = 0; q < i; ++q)
+            if (ns(q) > 1) o += radix(q) * ns(q);
+        return o;
+    }
+};
+
+// In-place radix-8 (forward sign): X[k] lands in v[(k & 1) * 4 + k / 2].
+// HALF: inputs 4..7 are zero (the padded half of the first pass).
+template <bool HALF>
+__device__ __forceinline__ void dft8_ip(float2 (&v)[8]) {
+    constexpr float r2 = 0.70710678118654752f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if constexpr (HALF) {
+            v[k + 4] = v[k];
+        } else {
+            const float2 a = v[k], b = v[k + 4];
+            v[k] = make_float2(a.x + b.x, a.y + b.y);
+            v[k + 4] = make_float2(a.x - b.x, a.y - b.y);
+        }
+    }
+    // odd half times W8^k: W8 = (1 - i)/sqrt2, W8^2 = -i, W8^3 = -(1 + i)/sqrt2
+    {
+        const float2 b = v[5];
+        v[5] = make_float2((b.x + b.y) * r2, (b.y - b.x) * r2);
+    }
+    v[6] = make_float2(v[6].y, -v[6].x);
+    {
+        const float2 b = v[7];
+        v[7] = make_float2((b.y - b.x) * r2, -(b.x + b.y) * r2);
+    }
+    dft4_ip(v[0], v[1], v[2], v[3]);  // X0 X2 X4 X6
+    dft4_ip(v[4], v[5], v[6], v[7]);  // X1 X3 X5 X7
+}
+__host__ __device__ constexpr int dft8_pos(int k) { return (k & 1) * 4 + k / 2; }
+
+// One Stockham pass (radix R, input stride NS) of a P-point line: src -> dst.
+template <int LOG2P, int R, int NS, int IN, int OUT, class Load, class Store>
+__device__ __forceinline__ void r8_pass(const float2* src, float2* dst, const float2* tw, int tid, int n,
+                                        const Load& load, const float* __restrict__ mult, const Store& store) {
+    constexpr int P = 1 << LOG2P, T = P / 8, NB = 8 / R, STRIDE = P / R;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const int j = tid + b * T;  // butterfly, < P/R
+        float2 v[R];
+        const int j_sw = sw8(j);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if constexpr (IN == IN_GLOBAL) {
+                v[r] = r < R / 2 ? load(r, j + r * STRIDE) : make_float2(0.f, 0.f);
+            } else {
+                v[r] = src[sw8_join(j_sw, STRIDE - 1, r * STRIDE)];
+            }
+        }
+        const int k = j & (NS - 1);
+        if constexpr (NS > 1) {
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[r * NS + k]);
+        }
+        if constexpr (R == 8) {
+            if constexpr (IN == IN_GLOBAL) dft8_ip<true>(v);
+            else dft8_ip<false>(v);
+        } else if constexpr (R == 4) {
+            dft4_ip(v[0], v[1], v[2], v[3]);
+        } else {
+            const float2 a = v[0], c = v[1];
+            v[0] = make_float2(a.x + c.x, a.y + c.y);
+            v[1] = make_float2(a.x - c.x, a.y - c.y);
+        }
+        const int base = (j - k) * R + k;
+        const int b_sw = sw8(base);
+        constexpr int BMASK = (P - 1) & ~((NS * R - 1) & ~(NS - 1));  // bits base may occupy
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const float2 x = v[R == 8 ? dft8_pos(r) : r];
+            if constexpr (OUT == OUT_SMEM) {
+                dst[sw8_join(b_sw, BMASK, r * NS)] = x;
+            } else if constexpr (OUT == OUT_MULT) {
+                // X <- conj(X * M / P): the inverse transform is conj(FFT(conj(.)))
+                const int m = base + r * NS;
+                const float g = __ldg(&mult[m <= P / 2 ? m : P - m]);
+                dst[sw8_join(b_sw, BMASK, r * NS)] = make_float2(x.x * g, -x.y * g);
+            } else {
+                const int m = base + r * NS;
+                if (m < n) store(m, x);
+            }
+        }
+    }
+}
+
+// Passes I.. of one direction; pass G = DIR * NP + I writes buffer G % 2.
+template <int LOG2P, int I, int DIR, class Load, class Store>
+__device__ __forceinline__ void r8_run(float2* bufs, const float2* tw, int tid, int n, const Load& load,
+                                       const float* mult, const Store& store) {
+    using PL = R8Plan<LOG2P>;
+    if constexpr (I < PL::NP) {
+        constexpr int G = DIR * PL::NP + I;
+        constexpr int IN = (DIR == 0 && I == 0) ? IN_GLOBAL : IN_SMEM;
+        constexpr int OUT = I == PL::NP - 1 ? (DIR == 0 ? OUT_MULT : OUT_GLOBAL) : OUT_SMEM;
+        r8_pass<LOG2P, PL::radix(I), PL::ns(I), IN, OUT>(bufs + ((G + 1) % 2) * PL::P, bufs + (G % 2) * PL::P,
+                                                         tw + PL::twoff(I), tid, n, load, mult, store);
+        if constexpr (OUT != OUT_GLOBAL) __syncthreads();
+        r8_run<LOG2P, I + 1, DIR>(bufs, tw, tid, n, load, mult, store);
+    }
+}
+
+// Same arguments as ramp_filter_kernel (blur/radius unused: no blur in mode 2).
+template <int LOG2P>
+__global__ void __launch_bounds__(R8Plan<LOG2P>::T, 1024 / R8Plan<LOG2P>::T)
+    ramp_filter_r8(const float* __restrict__ in, float* out, long long n_lines, int n, int, int,
+                   const float2* __restrict__ tw_g, const float* __restrict__ mult, const float* __restrict__,
+                   int, float i0, OutMap map, int n_tw) {
+    constexpr int P = 1 << LOG2P;
+    extern __shared__ float2 sbuf[];  // [2][P] ping-pong lines, then the twiddle tables
+    __shared__ int32_t s_row0[9];
+    __shared__ float* s_dst[8];
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < 9; ++s) s_row0[s] = map.row0[s];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) s_dst[s] = map.dst[s];
+    }
+    float2* tws = sbuf + 2 * P;
+    for (int m = tid; m < n_tw; m += R8Plan<LOG2P>::T) tws[m] = tw_g[m];
+    __syncthreads();
+    const long long n_pairs = (n_lines + 1) / 2;
+    const bool log_in = i0 > 0.f;
+    const NoIO none;
+    // raw inputs of this thread's 4 first-pass legs (m = tid + r P/8, r < 4),
+    // loaded one pair ahead so the loads overlap the previous pair's inverse
+    float2 pf[4];
+    auto prefetch = [&](long long pr) {
+        if (pr >= n_pairs) return;
+        const long long l = 2 * pr;
+        const float* pa = in + l * n;
+        const bool hb = l + 1 < n_lines;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int m = tid + r * (P / 8);
+            pf[r] = make_float2(0.f, 0.f);
+            if (m < n) pf[r] = make_float2(__ldcs(pa + m), hb ? __ldcs(pa + n + m) : 0.f);
+        }
+    };
+    prefetch(blockIdx.x);
+    for (long long pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+        const long long la = 2 * pair;
+        const bool has_b = la + 1 < n_lines;
+        {
+            // the two lines as one complex line, Beer-Lambert fused (fbp.py:80-83)
+            auto load = [&](int r, int m) -> float2 {
+                if (m >= n) return make_float2(0.f, 0.f);
+                float a = pf[r].x, b = pf[r].y;
+                if (log_in) {  // -ln(max(raw, 1) / i0)
+                    a = -logf(__fdiv_rn(fmaxf(a, 1.f), i0));
+                    b = has_b ? -logf(__fdiv_rn(fmaxf(b, 1.f), i0)) : 0.f;
+                }
+                return make_float2(a, b);
+            };
+            __syncthreads();  // the previous pair's last pass may still read buffer 0
+            r8_run<LOG2P, 0, 0>(sbuf, tws, tid, n, load, mult, none);
+        }
+        prefetch(pair + gridDim.x);
+        // output pointers resolved after the forward half (fewer live registers)
+        int za, zb = 0;
+        float* oa = out_ptr(la, n, map, s_row0, s_dst, za);
+        float* ob = has_b ? out_ptr(la + 1, n, map, s_row0, s_dst, zb) : nullptr;
+        // both rows in one 8-B store when they are z-neighbours of the same block
+        const bool pairwise = map.zblocked && has_b && (ob == oa + 1) && ((za & 1) == 0);
+        const float* w = map.w;
+        const bool zbl = map.zblocked;
+        auto store = [&](int m, float2 y) {
+            if (!zbl) {
+                __stcs(oa + m, y.x);
+                if (has_b) __stcs(ob + m, -y.y);
+                return;
+            }
+            const float wm = w ? __ldg(&w[m]) : 1.f;  // feather after the filter (fbp.py:242)
+            const float va = y.x * wm, vb = -y.y * wm;
+            if (pairwise) {
+                *reinterpret_cast<float2*>(oa + (size_t)m * kZP) = make_float2(va, vb);
+            } else {
+                oa[(size_t)m * kZP] = va;
+                if (has_b) ob[(size_t)m * kZP] = vb;
+            }
+        };
+        r8_run<LOG2P, 0, 1>(sbuf, tws, tid, n, none, mult, store);
     }
 }
 
@@ -569,13 +758,13 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
     p->P = P;
     p->log2P = ilog2(P);
     p->threads = std::max(32, P / 16);  // one radix-16 butterfly per thread (P <= 16384 -> <= 1024)
-    // K1 variant: fused radix-8 (64 <= P <= 8192), fused radix-16 (P = 16384 or
-    // TF_FILTER_MODE=1), generic smem path with the optional blur
+    // K1 variant: radix-8 ramp_filter_r8 (256 <= P <= 8192), fused radix-16
+    // (P = 16384 or TF_FILTER_MODE=1), generic smem path (blur, P < 256)
     const char* fm = getenv("TF_FILTER_MODE");
-    p->mode = blur_sigma > 0 ? 0 : (P >= 64 && P <= 8192 ? 2 : (p->log2P >= 8 ? 1 : 0));
+    p->mode = blur_sigma > 0 ? 0 : (P >= 256 && P <= 8192 ? 2 : (p->log2P >= 8 ? 1 : 0));
     if (fm && blur_sigma <= 0) {
         const int want = atoi(fm);
-        if (want == 0 || (want == 1 && p->log2P >= 8) || (want == 2 && P >= 64 && P <= 8192)) p->mode = want;
+        if (want == 0 || (want == 1 && p->log2P >= 8) || (want == 2 && P >= 256 && P <= 8192)) p->mode = want;
     }
     p->fused = p->mode != 0;
     if (p->mode == 2) p->threads = std::max(32, P / 8);
@@ -609,12 +798,17 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
     if (e == cudaSuccess && rad > 0)
         e = cudaMemcpy(p->d_blur, bw.data(), sizeof(float) * (2 * rad + 1), cudaMemcpyHostToDevice);
     p->smem_tw = P <= 8192;  // twiddle table in shared memory next to the line buffer
-    p->smem = ((p->mode == 2 ? P + P / 8 : P + P / 16) + (p->smem_tw ? p->n_tw : 0)) * (int)sizeof(float2);
-    if (p->mode == 2)
-        p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256, 2>
-                    : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512, 2>
-                                        : (const void*)ramp_filter_kernel<true, 1024, 2>;
-    else if (p->mode == 1)
+    p->smem = ((p->mode == 2 ? 2 * P : P + P / 16) + (p->smem_tw ? p->n_tw : 0)) * (int)sizeof(float2);
+    if (p->mode == 2) {
+        switch (p->log2P) {
+            case 8: p->kernel = (const void*)ramp_filter_r8<8>; break;
+            case 9: p->kernel = (const void*)ramp_filter_r8<9>; break;
+            case 10: p->kernel = (const void*)ramp_filter_r8<10>; break;
+            case 11: p->kernel = (const void*)ramp_filter_r8<11>; break;
+            case 12: p->kernel = (const void*)ramp_filter_r8<12>; break;
+            default: p->kernel = (const void*)ramp_filter_r8<13>; break;
+        }
+    } else if (p->mode == 1)
         p->kernel = p->threads <= 256 ? (const void*)ramp_filter_kernel<true, 256, 1>
                     : p->threads <= 512 ? (const void*)ramp_filter_kernel<true, 512, 1>
                                         : (const void*)ramp_filter_kernel<false, 1024, 1>;
