@@ -36,7 +36,7 @@ struct tf_bp_plan {
     double2* d_trig;  // (cos, sin) of k * (span / n_proj), fp64 libm, per angle
     float* d_w;       // feather weights (fp32, as numpy casts them)
     double ext;       // max channel extent of a tile's rays over all angles
-    int* d_order[2];  // launch order of the tiles (Morton, FoV-active first): 16x16, 32x16 tiles
+    int* d_order[2];  // launch order of the tiles (Morton, FoV-active first) per tile shape
     int n_active[2];
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
@@ -101,6 +101,14 @@ __device__ __forceinline__ bool outside_fov(int x, int y, const BPArgs& a) {
     return rr > a.R2;
 }
 
+// acc[0..3] += t * w as two packed FFMA2 (sm_100 FP32x2; per lane the same
+// fused, round-to-nearest operation as fmaf, so results are bit-identical)
+// with w as the broadcast scalar operand: half the issue slots of 4 FFMA.
+__device__ __forceinline__ void fma4(float2& a01, float2& a23, const float4& t, float w) {
+    a01 = __ffma2_rn(make_float2(t.x, t.y), make_float2(w, w), a01);
+    a23 = __ffma2_rn(make_float2(t.z, t.w), make_float2(w, w), a23);
+}
+
 // Role-kernel inner loop for one angle: voxel (C ^ r) plays role r and only
 // touches taps 0..ntap(r)-1 (see Layout::ROLE).
 __host__ __device__ constexpr int role_taps(int r) { return r == 0 ? 2 : (r == 3 ? 4 : 3); }
@@ -115,19 +123,14 @@ __device__ __forceinline__ void accumulate_roles(float (&acc)[4][ZT], const floa
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             const int v = C ^ r;
-            float a0 = acc[v][4 * c + 0], a1 = acc[v][4 * c + 1];
-            float a2 = acc[v][4 * c + 2], a3 = acc[v][4 * c + 3];
+            float2 a01 = make_float2(acc[v][4 * c + 0], acc[v][4 * c + 1]);
+            float2 a23 = make_float2(acc[v][4 * c + 2], acc[v][4 * c + 3]);
 #pragma unroll
-            for (int j = 0; j < role_taps(r); ++j) {
-                a0 = fmaf(T[j].x, w[r][j], a0);
-                a1 = fmaf(T[j].y, w[r][j], a1);
-                a2 = fmaf(T[j].z, w[r][j], a2);
-                a3 = fmaf(T[j].w, w[r][j], a3);
-            }
-            acc[v][4 * c + 0] = a0;
-            acc[v][4 * c + 1] = a1;
-            acc[v][4 * c + 2] = a2;
-            acc[v][4 * c + 3] = a3;
+            for (int j = 0; j < role_taps(r); ++j) fma4(a01, a23, T[j], w[r][j]);
+            acc[v][4 * c + 0] = a01.x;
+            acc[v][4 * c + 1] = a01.y;
+            acc[v][4 * c + 2] = a23.x;
+            acc[v][4 * c + 3] = a23.y;
         }
     }
 }
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
             for (int it = 0; it < n_it; ++it) {
                 const int s = it % STAGES;
                 const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
-                mbar_wait(&empty[s], ph ^ 1u);
+                mbar_wait_parked(&empty[s], ph ^ 1u);
                 const int kb = args.a0 + it * APS;
                 const int na = min(APS, args.a1 - kb);
                 int c_lo[APS];
@@ -358,19 +361,14 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
             for (int j = 0; j < NT; ++j) T[j] = *reinterpret_cast<const float4*>(p0 + j * kZP + 4 * c);
 #pragma unroll
             for (int v = 0; v < VX * VY; ++v) {
-                float a0 = acc[v][4 * c + 0], a1 = acc[v][4 * c + 1];
-                float a2 = acc[v][4 * c + 2], a3 = acc[v][4 * c + 3];
+                float2 a01 = make_float2(acc[v][4 * c + 0], acc[v][4 * c + 1]);
+                float2 a23 = make_float2(acc[v][4 * c + 2], acc[v][4 * c + 3]);
 #pragma unroll
-                for (int j = 0; j < NT; ++j) {
-                    a0 = fmaf(T[j].x, w[v][j], a0);
-                    a1 = fmaf(T[j].y, w[v][j], a1);
-                    a2 = fmaf(T[j].z, w[v][j], a2);
-                    a3 = fmaf(T[j].w, w[v][j], a3);
-                }
-                acc[v][4 * c + 0] = a0;
-                acc[v][4 * c + 1] = a1;
-                acc[v][4 * c + 2] = a2;
-                acc[v][4 * c + 3] = a3;
+                for (int j = 0; j < NT; ++j) fma4(a01, a23, T[j], w[v][j]);
+                acc[v][4 * c + 0] = a01.x;
+                acc[v][4 * c + 1] = a01.y;
+                acc[v][4 * c + 2] = a23.x;
+                acc[v][4 * c + 3] = a23.y;
             }
         }
     };
@@ -529,6 +527,10 @@ bool tile_order_enabled() {
     return v != 0;
 }
 
+// tile shapes (TX, TY) with a launch order each; variant -> shape
+constexpr int kTileShape[2][2] = {{16, 16}, {32, 16}};
+int variant_shape(int v) { return v == 10 ? 1 : 0; }
+
 int select_variant(const tf_bp_plan* p, int flags) {
     int variant = (flags & TF_BP_KERNEL_V1) ? 0 : default_variant();
     if (variant >= 5 && variant <= 7 && p->scale > 1.0) variant = 0;  // x-pairs need |cos|*scale <= 1 (3 taps)
@@ -614,7 +616,7 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     // the kernel's early-out) in Morton order, then the inactive ones
     std::vector<int> orders[2];
     for (int shape = 0; shape < 2; ++shape) {
-        const int TXs = shape ? 32 : 16, TYs = 16;
+        const int TXs = kTileShape[shape][0], TYs = kTileShape[shape][1];
         const int ntx = (g->nx + TXs - 1) / TXs, nty = (g->ny + TYs - 1) / TYs;
         std::vector<int> act, inact;
         for (int t = 0; t < ntx * nty; ++t) {
@@ -673,8 +675,7 @@ extern "C" int tf_bp_plan_destroy(tf_bp_plan* p) {
     if (!p) return TF_OK;
     cudaFree(p->d_trig);
     cudaFree(p->d_w);
-    cudaFree(p->d_order[0]);
-    cudaFree(p->d_order[1]);
+    for (int s = 0; s < 2; ++s) cudaFree(p->d_order[s]);
     delete p;
     return TF_OK;
 }
@@ -718,8 +719,8 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     // kernel variant: the 2x2-block 4-tap gather needs the block's rays to span
     // < 2 channels (sqrt(2) * voxel/pixel pitch ratio); else the 2-tap kernel
     const int variant = select_variant(p, flags);
-    const int shape = variant == 10 ? 1 : 0;  // 32x16 tiles for the Q32 variant
-    const int TXv = shape ? 32 : 16, TYv = 16;
+    const int shape = variant_shape(variant);
+    const int TXv = kTileShape[shape][0], TYv = kTileShape[shape][1];
     const double ext = std::sqrt((double)(TXv - 1) * (TXv - 1) + (double)(TYv - 1) * (TYv - 1)) * p->scale;
     const int W = (int)std::ceil(ext + (variant == 0 ? 3.0 : 4.0));
 
@@ -786,8 +787,8 @@ extern "C" int tf_bp_kernel_info(const tf_bp_plan* p, int flags, int n_rows, int
     if (!p || !bytes || !executed_updates) return set_error(TF_ERR_INVALID_ARGUMENT, "null argument");
     const int v = select_variant(p, flags);
     *bytes = v == 0 ? 8.0 : ((v >= 5 && v <= 7) ? 6.0 : 4.0);
-    const int shape = v == 10 ? 1 : 0;
-    const int64_t tile_vox = shape ? 32 * 16 : 16 * 16;
+    const int shape = variant_shape(v);
+    const int64_t tile_vox = kTileShape[shape][0] * kTileShape[shape][1];
     const int64_t rows = (int64_t)((n_rows + kZB - 1) / kZB) * kZB;
     *executed_updates = (int64_t)p->n_active[shape] * tile_vox * rows * (int64_t)(a1 - a0);
     return TF_OK;
