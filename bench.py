@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "allgather", "p2p"])
+    ap.add_argument("--exchange", default="alltoall",
+                    choices=["alltoall", "allgather", "p2p", "angles-p2p", "angles-nccl"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--slab-rows", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")
@@ -386,7 +387,23 @@ def main():
     total_updates = n_proj * n * n * n
 
     # ---- setup: engine + synthetic raw counts generated on the device (K4)
-    if world > 1:
+    bp_a0, bp_a1 = 0, n_proj  # angles K2 runs on this rank
+    angle_split = world > 1 and args.exchange.startswith("angles-")
+    if world > 1 and args.exchange.startswith("angles-"):
+        # P_proj: angle-split partials reduced onto the z-slab owners
+        from paper_2505_13955_b200.distributed import AngleSplitReconstructor
+
+        eng = slab = AngleSplitReconstructor(p, d, i0=I0, reduce=args.exchange[len("angles-"):], device=dev)
+        raw = torch.empty(eng.chunk_shape(), dtype=torch.float32, device=dev)
+        phantom_raw(p, d, raw, a0=eng.a0, a1=eng.a1)
+        k_rows = n
+        bp_a0, bp_a1 = eng.a0, eng.a1
+
+        def step_parts():
+            bp_ev[0].record()
+            eng.run(raw)  # K1, K2 with the reduction in its epilogue (or + NCCL), finalize
+            bp_ev[1].record()
+    elif world > 1:
         from paper_2505_13955_b200.distributed import ZSlabReconstructor
 
         eng = ZSlabReconstructor(p, d, i0=I0, exchange_mode=args.exchange, device=dev)
@@ -459,7 +476,7 @@ def main():
     from paper_2505_13955_b200._lib import TF_BP_FINALIZE, lib as _tf_lib
 
     bpu, exe = ctypes.c_double(), ctypes.c_int64()
-    _tf_lib().tf_bp_kernel_info(slab.bplan.handle, TF_BP_FINALIZE, k_rows, 0, n_proj, ctypes.byref(bpu),
+    _tf_lib().tf_bp_kernel_info(slab.bplan.handle, TF_BP_FINALIZE, k_rows, bp_a0, bp_a1, ctypes.byref(bpu),
                                 ctypes.byref(exe))
     bytes_per_update = bpu.value
     exec_upd = exe.value  # the library's own count: FoV-active tiles x tile voxels x padded rows x angles
@@ -473,7 +490,8 @@ def main():
     except OSError:
         pass
     stage_bytes = slab.stage.numel()
-    hbm_alg = stage_bytes + slab.vol.numel() * 4  # one pass over the staged slab + the volume write
+    vol_elems = slab.vol.numel() if hasattr(slab, "vol") else n * n * n
+    hbm_alg = stage_bytes + vol_elems * 4  # one pass over the staged slab + the volume write
     traffic = None  # ncu dram bytes of this kernel/config, captured separately (profiles/)
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", f"bp_traffic_{args.config}.json")))
@@ -585,10 +603,16 @@ def main():
         "dtype": "f32",
         "data": "synthetic (analytic 3-D Shepp-Logan raw counts generated on device, i0=1e5)",
         "config": {"workload": workload_desc(cfg), "volume": [n, n, n], "n_proj": n_proj,
-                   "parallelism": f"z-slab x{world}" + (f" ({args.exchange} exchange)" if world > 1 else ""),
+                   "parallelism": (f"angle-split x{world} ({args.exchange}: partials reduced onto z-slab owners)"
+                                   if angle_split else
+                                   f"z-slab x{world}" + (f" ({args.exchange} exchange)" if world > 1 else "")),
                    "l2": "inputs larger than L2 (raw %.1f GB, volume %.1f GB per step)" % (
-                       raw.numel() * 4 / 1e9, slab.vol.numel() * 4 / 1e9),
-                   "step": ("K1 Beer-Lambert+ramp+feather -> z-blocked staging -> [NCCL row-slab all-to-all "
+                       raw.numel() * 4 / 1e9, vol_elems * 4 / 1e9),
+                   "step": ("K1 Beer-Lambert+ramp+feather -> z-blocked staging -> K2 back-projection of this "
+                            "rank's angles over the whole volume, epilogue adds into each row's owner "
+                            "(NVLink peer memory, or + NCCL reduce-scatter) -> FoV/scale finalize"
+                            if angle_split else
+                            "K1 Beer-Lambert+ramp+feather -> z-blocked staging -> [NCCL row-slab all-to-all "
                             "landing in the owner's staging buffer] -> K2 back-projection")},
         "roofline": {
             "bound": "smem",
@@ -616,7 +640,7 @@ def main():
             "hbm_peak_measured": peaks.get("hbm_gbs"),
         },
         "clocks": clk,
-        "gpu_launches": (3 if (world > 1 and args.exchange == "allgather") else 2) * args.steps,
+        "gpu_launches": (3 if (world > 1 and args.exchange in ("allgather",) or angle_split) else 2) * args.steps,
     }
     if e2e is not None:
         line["e2e"] = e2e

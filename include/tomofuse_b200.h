@@ -148,9 +148,10 @@ TF_API int tf_bp_stage(const tf_bp_plan* plan, const float* sino, int rows_per_a
 enum {
     TF_BP_ACCUMULATE = 1, /* add to the unscaled partial sums already in vol */
     TF_BP_FINALIZE = 2,   /* apply FoV mask + angle_span/n_proj scale (fbp.py:246-251) */
-    TF_BP_KERNEL_V1 = 4   /* force the 1-voxel 2-tap kernel (default: 2x2-block
-                             4-tap kernel when voxel/pixel pitch <= 1.4; both
-                             give bit-identical volumes) */
+    TF_BP_KERNEL_V1 = 4,  /* force the 1-voxel 2-tap kernel (default: x-pair
+                             3-tap kernel when voxel/pixel pitch <= 1; both give
+                             bit-identical volumes) */
+    TF_BP_REDUCE = 8      /* internal: set by tf_backproject_reduce */
 };
 
 /* Back-projects angles [a0, a1) of a staged slab of `n_rows` rows into
@@ -161,6 +162,26 @@ enum {
  * ascending in angle, fbp.py:198-201). */
 TF_API int tf_backproject(const tf_bp_plan* plan, const void* stage, int n_rows, float* vol, int a0, int a1, int x0,
                    int x1, int y0, int y1, int flags, void* stream);
+
+/* Angle-split back-projection with the reduction fused into K2's epilogue
+ * (replaces the P_proj partials + Fabric.reduce_scatter_block of
+ * pipeline.py:239-275 / fabric.py:67-101).  Back-projects angles [a0, a1) of
+ * a staged full-height slab (rows [0, n_rows)) over the whole (ny, nx) plane
+ * and ADDS the unscaled partial sums of volume row z into the slab that owns
+ * it: slab_dst[s] + (z - slab_row0[s]) * ny * nx, for slab_row0[s] <= z <
+ * slab_row0[s+1] (n_slabs <= 8; slab_row0[0] = 0, slab_row0[n_slabs] =
+ * n_rows).  slab_dst may point into other GPUs' memory (NVLink peer
+ * mappings); the adds are atomic, so concurrent ranks may target the same
+ * slab.  Owners zero their slab first and call tf_bp_finalize after every
+ * rank's adds have landed.  Summation order across ranks is not fixed.
+ * `stage` holds only angles [a0, a1) (a rank's chunk, as tf_filter_stage
+ * writes it), not all n_proj. */
+TF_API int tf_backproject_reduce(const tf_bp_plan* plan, const void* stage, int n_rows, int a0, int a1, int n_slabs,
+                                 const int32_t* slab_row0, void* const* slab_dst, int flags, void* stream);
+
+/* FoV mask + angle_span/n_proj scale (fbp.py:246-251) applied to unscaled
+ * partial sums vol (n_rows, ny, nx): the TF_BP_FINALIZE epilogue as a pass. */
+TF_API int tf_bp_finalize(const tf_bp_plan* plan, float* vol, int n_rows, void* stream);
 
 /* Shared-memory bytes the selected K2 variant gathers per voxel x projection
  * update for these flags (8 = 2-tap, 6 = x-pair 3-tap, 4 = 2x2 4-tap): the

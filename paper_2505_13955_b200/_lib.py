@@ -51,6 +51,8 @@ SIGNATURES = {
     "tf_bp_stage": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
     "tf_backproject": (_i, [_vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp]),
     "tf_bp_smem_bytes_per_update": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_double)]),
+    "tf_backproject_reduce": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp, _i, _vp]),
+    "tf_bp_finalize": (_i, [_vp, _vp, _i, _vp]),
     "tf_bp_kernel_info": (_i, [_vp, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]),
     "tf_quantize": (_i, [_vp, _i, _vp, _i64, _d, _d, _vp]),
     "tf_phantom_sinogram": (_i, [_pg, _i, _i, _i, _i, _d, _d, _vp, _vp]),

@@ -92,6 +92,12 @@ struct BPArgs {
     int flags;
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
+    // TF_BP_REDUCE: row z's partial sums are added (red.global.add) into the
+    // slab owning it, rdst[s] + (z - rrow0[s]) * plane (peer memory allowed)
+    int a_base;  // first angle held in the staging buffer (0: it holds all n_proj)
+    int n_rslabs;
+    int rrow0[9];
+    float* rdst[8];
 };
 
 __device__ __forceinline__ bool outside_fov(int x, int y, const BPArgs& a) {
@@ -227,7 +233,7 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
                 mbar_arrive_expect_tx(&full[s], box_bytes * (uint32_t)na);
                 for (int a = 0; a < na; ++a)
                     tma_load_3d(ring + (size_t)(s * APS + a) * args.slot_bytes, &map, &full[s], 0, c_lo[a],
-                                (kb + a) * args.nzb + zb);
+                                (kb + a - args.a_base) * args.nzb + zb);
             }
         }
         return;
@@ -415,6 +421,27 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
         }
     }
 
+    if (args.flags & TF_BP_REDUCE) {
+        // angle-split partials: fire-and-forget adds into each row's owner
+        // (NVLink peer stores when the owner is another GPU); the reduction IS
+        // this kernel's epilogue, overlapped with the other tiles' angle loops
+#pragma unroll
+        for (int j = 0; j < ZT; ++j) {
+            if (j >= nz) break;
+            const int z = zrow0 + j;
+            float* base = nullptr;
+#pragma unroll
+            for (int s = 0; s < 8; ++s)  // constant indices: no local copy of the table
+                if (s < args.n_rslabs && z >= args.rrow0[s] && z < args.rrow0[s + 1])
+                    base = args.rdst[s] + (size_t)(z - args.rrow0[s]) * plane;
+#pragma unroll
+            for (int v = 0; v < VX * VY; ++v) {
+                const int x = X0 + dx0 + (v % VX), y = Y0 + dy0 + (v / VX);
+                if (x >= ux0 && x < ux1 && y >= uy0 && y < uy1) atomicAdd(base + (size_t)y * args.nx + x, acc[v][j]);
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int v = 0; v < VX * VY; ++v) {
         const int x = X0 + dx0 + (v % VX), y = Y0 + dy0 + (v / VX);
@@ -702,8 +729,16 @@ extern "C" int tf_bp_stage(const tf_bp_plan* p, const float* sino, int rows_per_
     return check_launch("stage_kernel");
 }
 
-extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows, float* vol, int a0, int a1,
-                              int x0, int x1, int y0, int y1, int flags, void* stream) {
+namespace tf {
+namespace {
+struct ReduceMap {
+    int n;
+    int row0[9];
+    float* dst[8];
+};
+
+int backproject_impl(const tf_bp_plan* p, const void* stage, int n_rows, float* vol, int a0, int a1, int x0,
+                     int x1, int y0, int y1, int flags, void* stream, const ReduceMap* rm, int a_base = 0) {
     if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null bp plan");
     const tf_geometry& g = p->g;
     if (!(0 <= a0 && a0 <= a1 && a1 <= g.n_proj))
@@ -712,7 +747,7 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
         return set_error(TF_ERR_INVALID_ARGUMENT, "tile (%d, %d, %d, %d) out of bounds", x0, x1, y0, y1);
     if (n_rows < 0) return set_error(TF_ERR_INVALID_ARGUMENT, "n_rows must be >= 0");
     if (n_rows == 0 || x0 == x1 || y0 == y1) return TF_OK;
-    if (!stage || !vol) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    if (!stage || (!vol && !rm)) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
     const int nzb = (n_rows + kZB - 1) / kZB;
     if (a0 == a1 && !(flags & TF_BP_FINALIZE)) return TF_OK;
 
@@ -727,7 +762,7 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     PFN_encodeTiled_t enc = encode_fn();
     if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     CUtensorMap map;
-    cuuint64_t dims[3] = {(cuuint64_t)kZP, (cuuint64_t)g.n_chan, (cuuint64_t)g.n_proj * (cuuint64_t)nzb};
+    cuuint64_t dims[3] = {(cuuint64_t)kZP, (cuuint64_t)g.n_chan, (cuuint64_t)(g.n_proj - a_base) * (cuuint64_t)nzb};
     cuuint64_t strides[2] = {(cuuint64_t)kRowBytes, (cuuint64_t)kRowBytes * (cuuint64_t)g.n_chan};
     cuuint32_t box[3] = {(cuuint32_t)kZP, (cuuint32_t)W, 1u};
     cuuint32_t estr[3] = {1u, 1u, 1u};
@@ -762,6 +797,12 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     a.R2 = p->R2;
     a.sc2 = p->sc2;
     a.angle_wf = p->angle_wf;
+    a.a_base = a_base;
+    if (rm) {
+        a.n_rslabs = rm->n;
+        for (int s = 0; s <= rm->n; ++s) a.rrow0[s] = rm->row0[s];
+        for (int s = 0; s < rm->n; ++s) a.rdst[s] = rm->dst[s];
+    }
     const int nty = (g.ny + TYv - 1) / TYv;
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)nzb);
     int st;
@@ -781,6 +822,13 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
     if (st) return st;
     return check_launch("bp_kernel");
 }
+}  // namespace
+}  // namespace tf
+
+extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows, float* vol, int a0, int a1,
+                              int x0, int x1, int y0, int y1, int flags, void* stream) {
+    return backproject_impl(p, stage, n_rows, vol, a0, a1, x0, x1, y0, y1, flags & ~TF_BP_REDUCE, stream, nullptr);
+}
 
 extern "C" int tf_bp_kernel_info(const tf_bp_plan* p, int flags, int n_rows, int a0, int a1, double* bytes,
                                  int64_t* executed_updates) {
@@ -799,4 +847,54 @@ extern "C" int tf_bp_smem_bytes_per_update(const tf_bp_plan* p, int flags, doubl
     const int v = select_variant(p, flags);
     *bytes = v == 0 ? 8.0 : ((v >= 5 && v <= 7) ? 6.0 : 4.0);
     return TF_OK;
+}
+
+namespace tf {
+namespace {
+// FoV mask + angle weight of fbp.py:247-251 on unscaled partial sums (the
+// TF_BP_FINALIZE epilogue as a separate pass, for reduced angle-split sums)
+__global__ void finalize_kernel(float* __restrict__ vol, long long n, int nx, int ny, double cx, double cy,
+                                double sc2, double R2, float wf) {
+    const long long plane = (long long)nx * ny;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i % plane;
+        const int x = (int)(r % nx), y = (int)(r / nx);
+        const double dx = __dsub_rn((double)x, cx), dy = __dsub_rn((double)y, cy);
+        const double rr = __dmul_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), sc2);
+        vol[i] = rr > R2 ? 0.f : vol[i] * wf;
+    }
+}
+}  // namespace
+}  // namespace tf
+
+extern "C" int tf_bp_finalize(const tf_bp_plan* p, float* vol, int n_rows, void* stream) {
+    if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null bp plan");
+    if (n_rows < 0) return set_error(TF_ERR_INVALID_ARGUMENT, "n_rows must be >= 0");
+    if (n_rows == 0) return TF_OK;
+    if (!vol) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    const long long n = (long long)n_rows * p->g.nx * p->g.ny;
+    const int grid = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    finalize_kernel<<<grid, 256, 0, as_stream(stream)>>>(vol, n, p->g.nx, p->g.ny, p->cx, p->cy, p->sc2, p->R2,
+                                                          p->angle_wf);
+    return check_launch("finalize_kernel");
+}
+
+extern "C" int tf_backproject_reduce(const tf_bp_plan* p, const void* stage, int n_rows, int a0, int a1, int n_slabs,
+                                     const int32_t* slab_row0, void* const* slab_dst, int flags, void* stream) {
+    if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null bp plan");
+    if (n_slabs < 1 || n_slabs > 8 || !slab_row0 || !slab_dst)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "invalid slab map");
+    if (slab_row0[0] != 0 || slab_row0[n_slabs] != n_rows)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "slab rows must cover [0, n_rows)");
+    for (int s = 0; s < n_slabs; ++s) {
+        if (slab_row0[s + 1] < slab_row0[s]) return set_error(TF_ERR_INVALID_ARGUMENT, "slab rows must ascend");
+        if (!slab_dst[s] && slab_row0[s + 1] > slab_row0[s])
+            return set_error(TF_ERR_INVALID_ARGUMENT, "null slab destination");
+    }
+    ReduceMap rm;
+    rm.n = n_slabs;
+    for (int s = 0; s <= n_slabs; ++s) rm.row0[s] = slab_row0[s];
+    for (int s = 0; s < n_slabs; ++s) rm.dst[s] = static_cast<float*>(slab_dst[s]);
+    return backproject_impl(p, stage, n_rows, nullptr, a0, a1, 0, p->g.nx, 0, p->g.ny,
+                            (flags & TF_BP_KERNEL_V1) | TF_BP_REDUCE, stream, &rm, a0);
 }

@@ -218,3 +218,113 @@ class ZSlabReconstructor:
         if self.mode == "allgather":
             return int(np.prod(self.chunk_shape())) * 4 * (self.world - 1)
         return sum(s for i, s in enumerate(self.out_splits) if i != self.rank) * 4
+
+
+class AngleSplitReconstructor:
+    """P_proj partitioning: angle-parallel partial volumes, reduced onto the
+    z-slab owners (the reference's projection split with
+    `Fabric.reduce_scatter_block`, pipeline.py:239-275 / fabric.py:67-101).
+
+    Rank g filters and back-projects ONLY its angle chunk
+    `split_range(n_proj, N)[g]`, over every row of the volume, and ends up
+    owning rows `split_range(n_rows, N)[g]` summed over all ranks' angles,
+    then finalized (FoV mask + angle weight).  Worth it when z-slabs run
+    short (n_rows < N x 32-row blocks), where z-slabs would leave z-blocks
+    half empty; otherwise `ZSlabReconstructor` moves far fewer bytes.
+
+    reduce="p2p" (default): every rank's slab is symmetric memory mapped over
+        NVLink and K2's epilogue adds each row's partial sums straight into
+        the owner's slab (tf_backproject_reduce) -- the reduce-scatter is the
+        back-projection's store stream, overlapped with the other tiles'
+        angle loops.  Two symmetric-memory barriers order a step.
+    reduce="nccl": K2 writes the full partial volume (owner-padded layout),
+        then one `reduce_scatter_tensor` (sum).
+
+    Summation order across ranks differs from the 1-GPU ascending order, so
+    results agree with it to fp32 rounding (not bitwise, unlike z-slabs).
+    """
+
+    def __init__(self, params: AcquisitionParams, dims: VolumeDims, spec: FilterSpec | None = None,
+                 i0: float = 1e5, feather_band: int = 32, reduce: str = "p2p", group=None, device=None):
+        import torch
+        import torch.distributed as dist
+
+        from .fbp import bp_plan, filter_plan
+
+        if reduce not in ("p2p", "nccl"):
+            raise ValueError(f"unknown reduce mode {reduce!r}")
+        self.torch = torch
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world > 8:
+            raise ValueError("angle-split reduction supports at most 8 ranks")
+        self.mode = reduce
+        self.params, self.dims = params, dims
+        self.spec = spec if spec is not None else FilterSpec()
+        self.i0 = float(i0)
+        self.device = torch.device(device if device is not None else "cuda")
+        self.slabs = split_range(params.n_rows, self.world)
+        self.chunks = split_range(params.n_proj, self.world)
+        self.a0, self.a1 = self.chunks[self.rank]
+        self.r0, self.r1 = self.slabs[self.rank]
+        self.kmax = max(e - s for s, e in self.slabs)
+        n_rows, n_chan, plane = params.n_rows, params.n_chan, dims.nx * dims.ny
+        with torch.cuda.device(self.device):
+            self.fplan = filter_plan(n_chan, self.spec, params.pixel_pitch)
+            self.bplan = bp_plan(params, dims, feather_band)
+        A = self.a1 - self.a0
+        nzb = -(-n_rows // ZB)
+        self.angle_bytes = nzb * n_chan * ZP * 4
+        self.stage = torch.empty(max(A, 1) * self.angle_bytes, dtype=torch.uint8, device=self.device)
+        row0 = [s for s, _ in self.slabs] + [n_rows]
+        self._row0 = (ctypes.c_int32 * len(row0))(*row0)
+        if reduce == "p2p":
+            import torch.distributed._symmetric_memory as symm
+
+            self.slab = symm.empty((self.kmax, dims.ny, dims.nx), dtype=torch.float32, device=self.device)
+            self.symm = symm.rendezvous(self.slab, group if group is not None else dist.group.WORLD)
+            dst = [int(self.symm.buffer_ptrs[s]) for s in range(self.world)]
+            self.partial = None
+        else:
+            self.symm = None
+            self.slab = torch.empty((self.kmax, dims.ny, dims.nx), dtype=torch.float32, device=self.device)
+            self.partial = torch.empty((self.world * self.kmax, dims.ny, dims.nx), dtype=torch.float32,
+                                       device=self.device)
+            base = self.partial.data_ptr()
+            dst = [base + s * self.kmax * plane * 4 for s in range(self.world)]
+        self._dst = (ctypes.c_void_p * self.world)(*dst)
+
+    def chunk_shape(self):
+        return (self.a1 - self.a0, self.params.n_rows, self.params.n_chan)
+
+    def _s(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def run(self, raw_chunk):
+        """raw_chunk: device (A, n_rows, n_chan) fp32 counts of this rank's
+        angles -> this rank's finalized volume slab (k, ny, nx)."""
+        import torch.distributed as dist
+
+        p = self.params
+        n_lines = raw_chunk.numel() // p.n_chan
+        check(lib().tf_filter_stage(self.fplan.handle, self.bplan.handle, ctypes.c_void_p(raw_chunk.data_ptr()),
+                                    ctypes.c_void_p(self.stage.data_ptr()), n_lines, self.i0, p.n_rows, 0, None,
+                                    None, self._s()))
+        if self.mode == "p2p":
+            self.slab.zero_()
+            self.symm.barrier(channel=0)  # every owner zeroed (and done reading the last step)
+        else:
+            self.partial.zero_()
+        check(lib().tf_backproject_reduce(self.bplan.handle, ctypes.c_void_p(self.stage.data_ptr()), p.n_rows, self.a0, self.a1, self.world,
+                                          self._row0, self._dst, 0, self._s()))
+        if self.mode == "p2p":
+            self.symm.barrier(channel=0)  # every rank's adds have landed
+        else:
+            dist.reduce_scatter_tensor(self.slab, self.partial, group=self.group)
+        k = self.r1 - self.r0
+        check(lib().tf_bp_finalize(self.bplan.handle, ctypes.c_void_p(self.slab.data_ptr()), k, self._s()))
+        return self.slab[:k]
+
+    def updates(self) -> int:
+        return (self.a1 - self.a0) * self.params.n_rows * self.dims.nx * self.dims.ny

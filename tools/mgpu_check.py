@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import torch.distributed as dist
 
-from paper_2505_13955_b200.distributed import ZSlabReconstructor
+from paper_2505_13955_b200.distributed import AngleSplitReconstructor, ZSlabReconstructor
 from paper_2505_13955_b200.engine import SlabReconstructor, phantom_raw
 from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
 
@@ -26,7 +26,10 @@ rank, world = dist.get_rank(), dist.get_world_size()
 n, n_proj, rows = 128, 120 * world, 96  # rows not a multiple of the slab size on purpose
 p = AcquisitionParams(n_proj=n_proj, n_rows=rows, n_chan=n, pixel_pitch=12.0)
 d = VolumeDims(n, n, rows, voxel_pitch=12.0)
-z = ZSlabReconstructor(p, d, i0=1e5, exchange_mode=args.exchange, device=dev)
+if args.exchange.startswith("angles-"):
+    z = AngleSplitReconstructor(p, d, i0=1e5, reduce=args.exchange[len("angles-"):], device=dev)
+else:
+    z = ZSlabReconstructor(p, d, i0=1e5, exchange_mode=args.exchange, device=dev)
 chunk = torch.empty(z.chunk_shape(), device=dev)
 phantom_raw(p, d, chunk, a0=z.a0, a1=z.a1)
 vol = z.run(chunk)
@@ -43,9 +46,11 @@ if rank == 0:
     ref = SlabReconstructor(p, d, i0=1e5).run(full_raw)
     got = torch.cat([g[: e - s] for g, (s, e) in zip(gathered, z.slabs)])
     same = torch.equal(got, ref)
-    print(f"rank0 world={world} exchange={args.exchange} bitwise_equal={same} "
+    rel = float((got - ref).norm() / ref.norm())
+    print(f"rank0 world={world} exchange={args.exchange} bitwise_equal={same} rel_l2={rel:.3e} "
           f"max_diff={float((got - ref).abs().max()):.3e}")
-    if same:
+    # z-slabs are bitwise; angle-split sums in a different order (fp32 rounding)
+    if same or (args.exchange.startswith("angles-") and rel < 1e-6):
         print("MGPU_OK")
 dist.barrier()
 dist.destroy_process_group()
