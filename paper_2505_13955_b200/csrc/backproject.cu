@@ -12,7 +12,7 @@
 //   * warp 8 is a TMA producer: per angle it computes, in fp64, the channel
 //     window [c_lo, c_lo+W) the tile's rays hit, and issues one
 //     cp.async.bulk.tensor box {36, W, 1} into a 3-stage x 4-angle smem ring
-//     (mbarrier full/empty pipeline).  Out-of-detector channels come back as
+//     (mbarrier 'full' barriers; consumers hand slots back on named barriers).  Out-of-detector channels come back as
 //     zeros from the TMA OOB fill -- the reference's zero guard.
 //   * warps 0-7 each own 32 voxel columns x 32 rows in registers; per angle a
 //     thread forms t in fp32 *relative to the tile origin* (origin and window
@@ -36,8 +36,8 @@ struct tf_bp_plan {
     double2* d_trig;  // (cos, sin) of k * (span / n_proj), fp64 libm, per angle
     float* d_w;       // feather weights (fp32, as numpy casts them)
     double ext;       // max channel extent of a tile's rays over all angles
-    int* d_order[2];  // launch order of the tiles (Morton, FoV-active first) per tile shape
-    int n_active[2];
+    int* d_order[4];  // launch order of the tiles (Morton, FoV-active first) per tile shape
+    int n_active[4];
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
 };
@@ -56,7 +56,7 @@ namespace {
 //       two live taps and 0 elsewhere, so the FMA sequence -- and the result
 //       -- is bit-identical to V1.
 template <int VX, int VY, int NT, int ZT, int STAGES_ = 3, int APS_ = 4, bool PIPE_ = false, int MINB_ = 2,
-          int PW_ = 4, bool ROLE_ = false, int TX_ = 16, int TY_ = 16>
+          int PW_ = 4, bool ROLE_ = false, int TX_ = 16, int TY_ = 16, bool XR_ = false>
 struct Layout {
     static constexpr int TX = TX_, TY = TY_;  // voxel columns per CTA tile
     // ROLE (2x2, 4 taps): per angle the block voxel with the smallest t is
@@ -66,6 +66,13 @@ struct Layout {
     // exact {1-f, f} weights (bit-identical to the 2-tap kernel).  The voxel
     // -> role map depends on the signs of cos/sin (warp-uniform per angle).
     static constexpr bool ROLE = ROLE_;
+    // XR (VX x 1, VX + 1 taps): a run of VX voxels along x; the run's rays
+    // span <= (VX-1)*|cos|*scale <= VX-1 channels, so VX + 1 taps cover it.
+    // The end voxel with the smaller t (by the sign of cos, warp-uniform) is
+    // the base (taps 0,1); the voxel r steps away needs taps 0..r+1.  With
+    // VX = 3: 4 taps / 3 voxels = 5.33 B of smem and 3 FMA per update, exact
+    // {1-f, f} weights (bit-identical to the 2-tap kernel).
+    static constexpr bool XR = XR_;
     static constexpr int PW = PW_, PH = 8 / PW_;  // one 8-lane LDS.128 phase = PW x PH blocks
     static constexpr int STAGES = STAGES_, APS = APS_, RING = STAGES_ * APS_;  // smem ring of angle slots
     static constexpr bool PIPE = PIPE_;  // software-pipeline the next angle's setup under this angle's FMAs
@@ -141,10 +148,32 @@ __device__ __forceinline__ void accumulate_roles(float (&acc)[4][ZT], const floa
     }
 }
 
+template <int C, int VXn, int ZT>
+__device__ __forceinline__ void accumulate_xrun(float (&acc)[VXn][ZT], const float* p0, const float (&w)[VXn][VXn + 1]) {
+#pragma unroll
+    for (int c = 0; c < ZT / 4; ++c) {
+        float4 T[VXn + 1];
+#pragma unroll
+        for (int j = 0; j <= VXn; ++j) T[j] = *reinterpret_cast<const float4*>(p0 + j * kZP + 4 * c);
+#pragma unroll
+        for (int v = 0; v < VXn; ++v) {
+            const int r = C ? VXn - 1 - v : v;  // steps from the base voxel
+            float2 a01 = make_float2(acc[v][4 * c + 0], acc[v][4 * c + 1]);
+            float2 a23 = make_float2(acc[v][4 * c + 2], acc[v][4 * c + 3]);
+#pragma unroll
+            for (int j = 0; j < r + 2; ++j) fma4(a01, a23, T[j], w[v][j]);
+            acc[v][4 * c + 0] = a01.x;
+            acc[v][4 * c + 1] = a01.y;
+            acc[v][4 * c + 2] = a23.x;
+            acc[v][4 * c + 3] = a23.y;
+        }
+    }
+}
+
 template <class L>
 struct Setup;
 
-template <class L>
+template <class L, bool RED = false>  // RED: TF_BP_REDUCE epilogue (own instantiation: no register cost elsewhere)
 __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     bp_kernel(const __grid_constant__ CUtensorMap map, const BPArgs args) {
     constexpr int VX = L::VX_, VY = L::VY_, NT = L::NT_, ZT = L::ZT_;
@@ -192,13 +221,11 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     uint8_t* ring = smem;
     float4* prm = reinterpret_cast<float4*>(smem + STAGES * APS * args.slot_bytes);
     uint64_t* full = reinterpret_cast<uint64_t*>(prm + STAGES * APS);
-    uint64_t* empty = full + STAGES;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], L::NCW);
         }
         fence_barrier_init();
     }
@@ -208,15 +235,17 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     const int n_it = (n_ang + APS - 1) / APS;
 
     if (warp == L::NCW) {
-        // ================= TMA producer (one thread)
-        if (lane == 0) {
-            tma_prefetch_desc(&map);
-            const double dX = (double)X0 - args.cx, dY = (double)Y0 - args.cy;
-            const uint32_t box_bytes = (uint32_t)(kZP * 4 * args.W);
-            for (int it = 0; it < n_it; ++it) {
-                const int s = it % STAGES;
-                const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
-                mbar_wait_parked(&empty[s], ph ^ 1u);
+        // ================= TMA producer (lane 0 issues; the warp waits)
+        // A ring slot is refilled once every consumer thread has arrived on
+        // the slot's named barrier: bar.sync parks the warp in hardware (a
+        // polled mbarrier kept ~20% of the SM's issue slots busy spinning).
+        if (lane == 0) tma_prefetch_desc(&map);
+        const double dX = (double)X0 - args.cx, dY = (double)Y0 - args.cy;
+        const uint32_t box_bytes = (uint32_t)(kZP * 4 * args.W);
+        for (int it = 0; it < n_it; ++it) {
+            const int s = it % STAGES;
+            if (it >= STAGES) named_bar_sync(1 + s, L::NTHREADS);  // round it-STAGES consumed
+            if (lane == 0) {
                 const int kb = args.a0 + it * APS;
                 const int na = min(APS, args.a1 - kb);
                 int c_lo[APS];
@@ -235,6 +264,7 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
                     tma_load_3d(ring + (size_t)(s * APS + a) * args.slot_bytes, &map, &full[s], 0, c_lo[a],
                                 (kb + a - args.a_base) * args.nzb + zb);
             }
+            __syncwarp();
         }
         return;
     }
@@ -301,6 +331,24 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
                 w[r][3] = o == 2.f ? f : 0.f;
             }
             p0 = reinterpret_cast<const float*>(base + (int)fb * kRowBytes);
+        } else if constexpr (L::XR) {
+            static_assert(VY == 1 && NT == VX + 1, "x-run kernel is VX x 1 with VX + 1 taps");
+            cls = p.y < 0.f ? 1 : 0;  // t falls along the run: the last voxel is the base
+            float t[VX];
+#pragma unroll
+            for (int v = 0; v < VX; ++v)
+                t[v] = fmaxf(fmaf((float)dy0, p.z, fmaf((float)(dx0 + v), p.y, p.x)), 0.f);
+            const float fb = floorf(cls ? t[VX - 1] : t[0]);  // smallest t (monotone rounding)
+#pragma unroll
+            for (int v = 0; v < VX; ++v) {
+                const float fl = floorf(t[v]);
+                const float f = t[v] - fl;
+                const float g0 = 1.f - f;
+                const float o = fl - fb;
+#pragma unroll
+                for (int j = 0; j < NT; ++j) w[v][j] = o == (float)j ? g0 : (o == (float)(j - 1) ? f : 0.f);
+            }
+            p0 = reinterpret_cast<const float*>(base + (int)fb * kRowBytes);
         } else if constexpr (NT == 2) {
             float t = fmaf((float)dy0, p.z, fmaf((float)dx0, p.y, p.x));
             t = fmaxf(t, 0.f);
@@ -351,6 +399,11 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
         }
     };
     auto accumulate = [&](const float* p0, const float (&w)[VX * VY][NT], int cls) {
+        if constexpr (L::XR) {
+            if (cls) accumulate_xrun<1, VX, ZT>(acc, p0, w);  // warp-uniform: sign of cos
+            else accumulate_xrun<0, VX, ZT>(acc, p0, w);
+            return;
+        }
         if constexpr (L::ROLE) {
             switch (cls) {  // warp-uniform: depends on the angle only
                 case 0: accumulate_roles<0, ZT>(acc, p0, w); break;
@@ -383,8 +436,8 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
         mbar_wait(&full[it % STAGES], (uint32_t)(it / STAGES) & 1u);
     };
     auto release = [&](int g) {  // last angle of a stage (or of the launch)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[(g / APS) % STAGES]);
+        const int it = g / APS;
+        if (it + STAGES < n_it) named_bar_arrive(1 + it % STAGES, L::NTHREADS);  // the producer refills it
     };
 
     if constexpr (!L::PIPE) {
@@ -421,7 +474,7 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
         }
     }
 
-    if (args.flags & TF_BP_REDUCE) {
+    if constexpr (RED) {
         // angle-split partials: fire-and-forget adds into each row's owner
         // (NVLink peer stores when the owner is another GPU); the reduction IS
         // this kernel's epilogue, overlapped with the other tiles' angle loops
@@ -536,12 +589,17 @@ using Q4Cfg9 = Layout<2, 2, 4, 16, 8, 2, false, 3, 2, true>;
 // 2x2 role kernel with a full 32-row column per thread (128 accumulators) on
 // a 32x16 tile: setup amortised over 128 updates, 4 B smem + 3 FMA per update
 using Q4Cfg10 = Layout<2, 2, 4, 32, 8, 2, true, 2, 2, true, 32, 16>;
+// x-run of 3 voxels, 4 taps, 16 rows per thread, 24x16 tiles (5.33 B/update)
+using X3Cfg11 = Layout<3, 1, 4, 16, 8, 2, false, 2, 2, false, 24, 16, true>;
+using X3Cfg12 = Layout<3, 1, 4, 16, 8, 2, true, 2, 2, false, 24, 16, true>;
+using X3Cfg13 = Layout<3, 1, 4, 16, 8, 2, false, 3, 2, false, 24, 8, true>;
+using X3Cfg14 = Layout<3, 1, 4, 16, 8, 2, true, 3, 2, false, 24, 8, true>;
 
 int default_variant() {
     static int v = [] {
         const char* e = getenv("TF_BP_VARIANT");  // benchmarking knob: 1..4
         int x = e ? atoi(e) : 0;
-        return (x >= 1 && x <= 10) ? x : 6;
+        return (x >= 1 && x <= 14) ? x : 6;
     }();
     return v;
 }
@@ -555,21 +613,31 @@ bool tile_order_enabled() {
 }
 
 // tile shapes (TX, TY) with a launch order each; variant -> shape
-constexpr int kTileShape[2][2] = {{16, 16}, {32, 16}};
-int variant_shape(int v) { return v == 10 ? 1 : 0; }
+constexpr int kNumShapes = 4;
+constexpr int kTileShape[kNumShapes][2] = {{16, 16}, {32, 16}, {24, 16}, {24, 8}};
+int variant_shape(int v) { return v == 10 ? 1 : (v >= 13 ? 3 : (v >= 11 ? 2 : 0)); }
+
+// smem bytes gathered per update: 16 B per LDS.128 of 4 rows, taps / voxels
+double bytes_per_update(int v) {
+    if (v == 0) return 8.0;
+    if (v >= 5 && v <= 7) return 6.0;
+    if (v >= 11) return 16.0 / 3.0;
+    return 4.0;
+}
 
 int select_variant(const tf_bp_plan* p, int flags) {
-    int variant = (flags & TF_BP_KERNEL_V1) ? 0 : default_variant();
-    if (variant >= 5 && variant <= 7 && p->scale > 1.0) variant = 0;  // x-pairs need |cos|*scale <= 1 (3 taps)
+    int variant = (flags & TF_BP_KERNEL_V1) ? 0 : ((flags & TF_BP_REDUCE) ? 6 : default_variant());
+    if (((variant >= 5 && variant <= 7) || variant >= 11) && p->scale > 1.0)
+        variant = 0;  // x-runs need |cos|*scale <= 1 (VX + 1 taps)
     if (variant >= 1 && p->scale > 1.4) variant = 0;  // 2x2 blocks need sqrt(2)*scale < 2 (4 taps)
     return variant;
 }
 
-template <class L>
+template <class L, bool RED = false>
 int launch_bp(const CUtensorMap& map, const BPArgs& a, dim3 grid, void* stream) {
     const int smem = bp_smem_bytes<L>(a.slot_bytes);
-    TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    bp_kernel<L><<<grid, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
+    TF_CUDA_TRY(cudaFuncSetAttribute(bp_kernel<L, RED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    bp_kernel<L, RED><<<grid, L::NTHREADS, smem, as_stream(stream)>>>(map, a);
     return TF_OK;
 }
 }  // namespace
@@ -641,8 +709,8 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     p->angle_wf = (float)step;
     // tile launch order per tile shape: FoV-active tiles (same fp64 test as
     // the kernel's early-out) in Morton order, then the inactive ones
-    std::vector<int> orders[2];
-    for (int shape = 0; shape < 2; ++shape) {
+    std::vector<int> orders[kNumShapes];
+    for (int shape = 0; shape < kNumShapes; ++shape) {
         const int TXs = kTileShape[shape][0], TYs = kTileShape[shape][1];
         const int ntx = (g->nx + TXs - 1) / TXs, nty = (g->ny + TYs - 1) / TYs;
         std::vector<int> act, inact;
@@ -681,7 +749,7 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     std::vector<float> wf(g->n_chan);
     for (int i = 0; i < g->n_chan; ++i) wf[i] = (float)w[i];
     cudaError_t e = cudaMalloc(&p->d_trig, sizeof(double2) * g->n_proj);
-    for (int s = 0; s < 2 && e == cudaSuccess; ++s) {
+    for (int s = 0; s < kNumShapes && e == cudaSuccess; ++s) {
         e = cudaMalloc(&p->d_order[s], sizeof(int) * orders[s].size());
         if (e == cudaSuccess)
             e = cudaMemcpy(p->d_order[s], orders[s].data(), sizeof(int) * orders[s].size(), cudaMemcpyHostToDevice);
@@ -702,7 +770,7 @@ extern "C" int tf_bp_plan_destroy(tf_bp_plan* p) {
     if (!p) return TF_OK;
     cudaFree(p->d_trig);
     cudaFree(p->d_w);
-    for (int s = 0; s < 2; ++s) cudaFree(p->d_order[s]);
+    for (int s = 0; s < kNumShapes; ++s) cudaFree(p->d_order[s]);
     delete p;
     return TF_OK;
 }
@@ -806,6 +874,11 @@ int backproject_impl(const tf_bp_plan* p, const void* stage, int n_rows, float* 
     const int nty = (g.ny + TYv - 1) / TYv;
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)nzb);
     int st;
+    if (flags & TF_BP_REDUCE) {  // reduce epilogue: the default pair kernel, or V1 (select_variant maps others)
+        st = variant == 0 ? launch_bp<V1Cfg, true>(map, a, grid, stream) : launch_bp<P3Cfg6, true>(map, a, grid, stream);
+        if (st) return st;
+        return check_launch("bp_kernel");
+    }
     switch (variant) {
         case 0: st = launch_bp<V1Cfg>(map, a, grid, stream); break;
         case 1: st = launch_bp<V4Cfg1>(map, a, grid, stream); break;
@@ -817,7 +890,11 @@ int backproject_impl(const tf_bp_plan* p, const void* stage, int n_rows, float* 
         case 7: st = launch_bp<P3Cfg7>(map, a, grid, stream); break;
         case 8: st = launch_bp<Q4Cfg8>(map, a, grid, stream); break;
         case 9: st = launch_bp<Q4Cfg9>(map, a, grid, stream); break;
-        default: st = launch_bp<Q4Cfg10>(map, a, grid, stream); break;
+        case 10: st = launch_bp<Q4Cfg10>(map, a, grid, stream); break;
+        case 11: st = launch_bp<X3Cfg11>(map, a, grid, stream); break;
+        case 12: st = launch_bp<X3Cfg12>(map, a, grid, stream); break;
+        case 13: st = launch_bp<X3Cfg13>(map, a, grid, stream); break;
+        default: st = launch_bp<X3Cfg14>(map, a, grid, stream); break;
     }
     if (st) return st;
     return check_launch("bp_kernel");
@@ -834,7 +911,7 @@ extern "C" int tf_bp_kernel_info(const tf_bp_plan* p, int flags, int n_rows, int
                                  int64_t* executed_updates) {
     if (!p || !bytes || !executed_updates) return set_error(TF_ERR_INVALID_ARGUMENT, "null argument");
     const int v = select_variant(p, flags);
-    *bytes = v == 0 ? 8.0 : ((v >= 5 && v <= 7) ? 6.0 : 4.0);
+    *bytes = bytes_per_update(v);
     const int shape = variant_shape(v);
     const int64_t tile_vox = kTileShape[shape][0] * kTileShape[shape][1];
     const int64_t rows = (int64_t)((n_rows + kZB - 1) / kZB) * kZB;
@@ -845,7 +922,7 @@ extern "C" int tf_bp_kernel_info(const tf_bp_plan* p, int flags, int n_rows, int
 extern "C" int tf_bp_smem_bytes_per_update(const tf_bp_plan* p, int flags, double* bytes) {
     if (!p || !bytes) return set_error(TF_ERR_INVALID_ARGUMENT, "null argument");
     const int v = select_variant(p, flags);
-    *bytes = v == 0 ? 8.0 : ((v >= 5 && v <= 7) ? 6.0 : 4.0);
+    *bytes = bytes_per_update(v);
     return TF_OK;
 }
 
