@@ -73,6 +73,38 @@ def test_ramp_filter_long_lines(F, golden):
     assert rel_l2(got, g["rf_300"]) < 2e-6
 
 
+@pytest.mark.parametrize("n", [100, 129, 300, 700, 1024, 1500, 2048, 2500, 4096, 5000])
+@pytest.mark.parametrize("mode", ["2", "1", "0"])
+def test_ramp_filter_sizes_and_modes_vs_direct_convolution(F, n, mode, monkeypatch):
+    """K1 at every transform length of the radix-8 kernel (P = 256..16384,
+    with and without a radix-2/4 tail pass, n below and at P/2) and in all
+    three K1 modes, fused Beer-Lambert on, odd line count (a lone last line):
+    equals the C oracle's O(n^2) direct convolution (test_fbp.py:66-97)."""
+    import ctypes
+
+    import torch
+
+    from oracle import c_oracle as C
+    from paper_2505_13955_b200 import fbp as G
+    from paper_2505_13955_b200._lib import check, lib
+
+    monkeypatch.setenv("TF_FILTER_MODE", mode)
+    G._filter_plan.cache_clear()
+    try:
+        rng = np.random.default_rng(n)
+        raw = rng.uniform(2e4, 1e5, size=(3, n)).astype(np.float32)
+        ref = C.ramp_filter(C.preprocess(raw.astype(np.float64)[None], 1e5)[0], "ramlak", 12.0)
+        plan = G.filter_plan(n, F.FilterSpec(), 12.0)
+        x = torch.from_numpy(raw).cuda()
+        out = torch.empty_like(x)
+        check(lib().tf_filter(plan.handle, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), 3, 1e5,
+                              0, 0, None, None, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        got = out.cpu().numpy().astype(np.float64)
+        assert rel_l2(got, ref) < 3e-6, (n, mode, rel_l2(got, ref))
+    finally:
+        G._filter_plan.cache_clear()
+
+
 def test_preprocess_matches_reference(F, golden):
     g, _ = golden
     got = F.preprocess(g["pre_raw"], 1e5)
