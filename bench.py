@@ -6,8 +6,9 @@
     torchrun --nproc-per-node N bench.py --gpus N ...           # z-slab multi-GPU
 
 A step = one complete reconstruction of the volume: raw counts (resident in
-HBM) -> K1 Beer-Lambert + ramp filter -> [row-slab exchange over NCCL] ->
-z-block staging -> K2 back-projection -> fp32 volume.  `value` is whole-job
+HBM) -> K1 Beer-Lambert + ramp filter -> [N>1: row-slab exchange, by
+default K1's own stores into the owner GPU over NVLink] -> z-block staging
+-> K2 back-projection -> fp32 volume.  `value` is whole-job
 GUPS (voxel x projection updates / s, N_p*N^3 convention of
 pipeline.py:225-227) over the max-over-ranks device time; `e2e` is the same
 through host pinned buffers (H2D of the raw counts + D2H of the volume inside
@@ -45,6 +46,18 @@ TX = TY = 16   # BP tile (csrc/backproject.cu)
 ZB = 32
 
 
+EXCHANGE_STEP = {
+    "": "K1 Beer-Lambert+ramp+feather -> z-blocked staging -> K2 back-projection",
+    "alltoall": "K1 Beer-Lambert+ramp+feather -> z-blocked staging per owner slab -> NCCL row-slab all-to-all "
+                "landing in the owner's staging buffer -> K2 back-projection",
+    "p2p": "K1 Beer-Lambert+ramp -> natural rows stored straight into the owner GPU's buffer over NVLink "
+           "(symmetric memory; the all-to-all is K1's store stream) -> owner stages (feather) -> K2",
+    "p2p-zblocked": "K1 Beer-Lambert+ramp+feather -> z-blocked rows stored straight into the owner's staging "
+                    "buffer over NVLink -> K2",
+    "allgather": "K1 Beer-Lambert+ramp -> NCCL all-gather of natural rows -> owner stages its rows -> K2",
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -52,8 +65,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--exchange", default="alltoall",
-                    choices=["alltoall", "allgather", "p2p", "angles-p2p", "angles-nccl"])
+    ap.add_argument("--exchange", default="p2p",
+                    choices=["alltoall", "allgather", "p2p", "p2p-zblocked", "angles-p2p", "angles-nccl"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--slab-rows", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")
@@ -406,7 +419,14 @@ def main():
     elif world > 1:
         from paper_2505_13955_b200.distributed import ZSlabReconstructor
 
-        eng = ZSlabReconstructor(p, d, i0=I0, exchange_mode=args.exchange, device=dev)
+        try:
+            eng = ZSlabReconstructor(p, d, i0=I0, exchange_mode=args.exchange, device=dev)
+        except Exception as e:  # symmetric memory unavailable: same z-slab path, NCCL all-to-all
+            if not args.exchange.startswith("p2p"):
+                raise
+            print(f"p2p exchange unavailable ({e}); using alltoall", file=sys.stderr)
+            args.exchange = "alltoall"
+            eng = ZSlabReconstructor(p, d, i0=I0, exchange_mode=args.exchange, device=dev)
         raw = torch.empty(eng.chunk_shape(), dtype=torch.float32, device=dev)
         phantom_raw(p, d, raw, a0=eng.a0, a1=eng.a1)
         slab = eng.local
@@ -612,8 +632,7 @@ def main():
                             "rank's angles over the whole volume, epilogue adds into each row's owner "
                             "(NVLink peer memory, or + NCCL reduce-scatter) -> FoV/scale finalize"
                             if angle_split else
-                            "K1 Beer-Lambert+ramp+feather -> z-blocked staging -> [NCCL row-slab all-to-all "
-                            "landing in the owner's staging buffer] -> K2 back-projection")},
+                            EXCHANGE_STEP.get(args.exchange if world > 1 else "", EXCHANGE_STEP[""]))},
         "roofline": {
             "bound": "smem",
             "kernel": "bp_kernel (K2)",
@@ -640,7 +659,9 @@ def main():
             "hbm_peak_measured": peaks.get("hbm_gbs"),
         },
         "clocks": clk,
-        "gpu_launches": (3 if (world > 1 and args.exchange in ("allgather",) or angle_split) else 2) * args.steps,
+        # our kernels per step: K1 + K2, + tf_bp_stage (allgather, p2p) or + tf_bp_finalize (angle split)
+        "gpu_launches": (3 if (world > 1 and (args.exchange in ("allgather", "p2p") or angle_split)) else 2)
+        * args.steps,
     }
     if e2e is not None:
         line["e2e"] = e2e

@@ -126,6 +126,15 @@ TF_API int tf_filter_stage_peers(const tf_filter_plan* plan, const tf_bp_plan* b
                                  float i0, int rows_per_angle, int n_slabs, const int32_t* slab_row0,
                                  void* const* slab_dst, void* stream);
 
+/* Fused filter + exchange, natural rows: slab s's rows of every line
+ * (angle-major, [angle][row - slab_row0[s]][chan], like tf_filter's slab map)
+ * are written to the device pointer slab_dst[s], typically the owner GPU's
+ * receive buffer over NVLink.  Each line is one contiguous run, so the remote
+ * stores are fully coalesced; the owner stages its rows locally
+ * (tf_bp_stage) after a cross-GPU barrier. */
+TF_API int tf_filter_peers(const tf_filter_plan* plan, const float* in, int64_t n_lines, float i0, int rows_per_angle,
+                           int n_slabs, const int32_t* slab_row0, void* const* slab_dst, void* stream);
+
 /* Beer-Lambert only (fbp.py:75-83): fp32 or fp64 counts -> fp64 depth
  * (the reference's output dtype), computed in fp64. */
 TF_API int tf_preprocess(const void* raw, int raw_dtype, double* out, int64_t n, double i0, void* stream);

@@ -43,6 +43,7 @@ SIGNATURES = {
     "tf_filter_plan_destroy": (_i, [_vp]),
     "tf_filter": (_i, [_vp, _vp, _vp, _i64, _f, _i, _i, _vp, _vp, _vp]),
     "tf_filter_stage": (_i, [_vp, _vp, _vp, _vp, _i64, _f, _i, _i, _vp, _vp, _vp]),
+    "tf_filter_peers": (_i, [_vp, _vp, ctypes.c_int64, ctypes.c_float, _i, _i, _vp, _vp, _vp]),
     "tf_filter_stage_peers": (_i, [_vp, _vp, _vp, _i64, _f, _i, _i, _vp, _vp, _vp]),
     "tf_preprocess": (_i, [_vp, _i, _vp, _i64, _d, _vp]),
     "tf_bp_plan_create": (_i, [_pg, _i, ctypes.POINTER(_vp)]),

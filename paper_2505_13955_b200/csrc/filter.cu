@@ -948,6 +948,21 @@ extern "C" int tf_filter_stage_peers(const tf_filter_plan* p, const tf_bp_plan* 
     return launch_filter(p, in, map.dst[0], n_lines, i0, map, stream);
 }
 
+extern "C" int tf_filter_peers(const tf_filter_plan* p, const float* in, int64_t n_lines, float i0,
+                               int rows_per_angle, int n_slabs, const int32_t* slab_row0, void* const* slab_dst,
+                               void* stream) {
+    if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null plan");
+    if (n_lines < 0 || rows_per_angle < 1 || n_slabs < 1) return set_error(TF_ERR_INVALID_ARGUMENT, "invalid line counts");
+    if (n_lines == 0) return TF_OK;
+    if (!in || !slab_dst) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    OutMap map{};
+    int st = build_map(map, nullptr, n_lines, rows_per_angle, n_slabs, slab_row0, nullptr, slab_dst);
+    if (st) return st;
+    map.zblocked = 0;  // natural rows: each line one contiguous run (coalesced NVLink stores)
+    map.w = nullptr;
+    return launch_filter(p, in, map.dst[0], n_lines, i0, map, stream);
+}
+
 extern "C" int tf_preprocess(const void* raw, int raw_dtype, double* out, int64_t n, double i0, void* stream) {
     if (!(i0 > 0)) return set_error(TF_ERR_INVALID_ARGUMENT, "i0 must be positive, got %g", i0);
     if (n < 0 || (raw_dtype != TF_F32 && raw_dtype != TF_F64)) return set_error(TF_ERR_INVALID_ARGUMENT, "bad arguments");

@@ -15,12 +15,17 @@ devices:
       K2's z-blocked staging layout, grouped per destination slab, so a
       single `all_to_all_single` lands every owner's rows angle-ordered
       directly in its staging buffer (no separate staging pass);
-    - "p2p" (fused compute + exchange): every rank's staging buffer is
+    - "p2p" (fused compute + exchange): every rank's receive buffer is
       symmetric memory mapped over NVLink; K1's epilogue stores each
-      destination slab's rows straight into the owner's staging buffer
-      (tf_filter_stage_peers), so the all-to-all IS the filter's store
-      stream.  Two symmetric-memory barriers per step order it (previous
-      back-projection done before overwrite; all stores landed before K2);
+      destination slab's rows, natural layout, straight into the owner's
+      buffer (tf_filter_peers, one contiguous run per line: coalesced
+      NVLink stores), so the all-to-all IS the filter's store stream; the
+      owner then stages its rows locally (tf_bp_stage).  Two symmetric-
+      memory barriers per step order it (previous step's staging done
+      before overwrite; all stores landed before staging);
+    - "p2p-zblocked": as "p2p" but K1 stores straight into the owner's
+      staging layout (tf_filter_stage_peers): no staging pass, but 8-byte
+      scattered remote stores;
     - "allgather" (north_star's literal variant): `all_gather_into_tensor`
       of the natural-layout chunks, N x the bytes, owners stage their rows.
 """
@@ -127,24 +132,31 @@ class ZSlabReconstructor:
             sizes = {e - s for s, e in self.chunks}
             if len(sizes) != 1:
                 raise ValueError("allgather exchange needs n_proj divisible by the world size")
-        elif exchange_mode not in ("alltoall", "p2p"):
+        elif exchange_mode not in ("alltoall", "p2p", "p2p-zblocked"):
             raise ValueError(f"unknown exchange mode {exchange_mode!r}")
         A = self.a1 - self.a0
         self.symm = None
+        self.recv = None
         stage = None
-        if exchange_mode == "p2p":
+        if exchange_mode.startswith("p2p"):
             import torch.distributed._symmetric_memory as symm
 
-            zper = [_rows_elems(e - s, n_chan, True) for s, e in self.slabs]  # floats per angle per slab
-            stage = symm.empty(n_proj * max(zper), dtype=torch.float32, device=self.device)
-            self.symm = symm.rendezvous(stage, group if group is not None else dist.group.WORLD)
-            # slab s's rows of my angles go to rank s's staging buffer at angle a0
-            dst = [int(self.symm.buffer_ptrs[s]) + self.a0 * zper[s] * 4 for s in range(self.world)]
+            zb = exchange_mode == "p2p-zblocked"
+            per = [_rows_elems(e - s, n_chan, zb) for s, e in self.slabs]  # floats per angle per slab
+            buf = symm.empty(n_proj * max(per), dtype=torch.float32, device=self.device)
+            self.symm = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
+            # slab s's rows of my angles go to rank s's buffer at angle a0
+            dst = [int(self.symm.buffer_ptrs[s]) + self.a0 * per[s] * 4 for s in range(self.world)]
             self._dst = (ctypes.c_void_p * self.world)(*dst)
+            if zb:
+                stage = buf  # lands directly in the owner's staging layout
+            else:
+                k = self.r1 - self.r0
+                self.recv = buf[: n_proj * k * n_chan].view(n_proj, k, n_chan)
         # local slab engine; its staging buffer is the exchange landing zone
         self.local = SlabReconstructor(params, dims, spec, i0, feather_band, rows=(self.r0, self.r1),
                                        device=self.device, stage=stage)
-        if exchange_mode == "p2p":
+        if exchange_mode.startswith("p2p"):
             self.send = None
         else:
             self.send = torch.empty(sum(self.in_splits) if exchange_mode == "alltoall" else A * n_rows * n_chan,
@@ -169,12 +181,17 @@ class ZSlabReconstructor:
         (allgather)."""
         p = self.params
         n_lines = raw_chunk.numel() // p.n_chan
-        if self.mode == "p2p":
+        if self.mode.startswith("p2p"):
             row0, _ = self._map
-            self.symm.barrier(channel=0)  # owners finished reading their staging (previous step)
-            check(lib().tf_filter_stage_peers(self.local.fplan.handle, self.local.bplan.handle,
-                                              ctypes.c_void_p(raw_chunk.data_ptr()), n_lines, self.local.i0,
-                                              p.n_rows, self.world, row0, self._dst, self._s()))
+            self.symm.barrier(channel=0)  # owners finished reading their buffer (previous step)
+            if self.mode == "p2p":
+                check(lib().tf_filter_peers(self.local.fplan.handle, ctypes.c_void_p(raw_chunk.data_ptr()),
+                                            n_lines, self.local.i0, p.n_rows, self.world, row0, self._dst,
+                                            self._s()))
+            else:
+                check(lib().tf_filter_stage_peers(self.local.fplan.handle, self.local.bplan.handle,
+                                                  ctypes.c_void_p(raw_chunk.data_ptr()), n_lines, self.local.i0,
+                                                  p.n_rows, self.world, row0, self._dst, self._s()))
             return
         if self._map is None:
             check(lib().tf_filter(self.local.fplan.handle, ctypes.c_void_p(raw_chunk.data_ptr()),
@@ -189,7 +206,7 @@ class ZSlabReconstructor:
     def exchange(self):
         import torch.distributed as dist
 
-        if self.mode == "p2p":  # the stores already landed; wait until every peer's have
+        if self.mode.startswith("p2p"):  # the stores already landed; wait until every peer's have
             self.symm.barrier(channel=0)
             return
         if self.mode == "allgather":
@@ -201,6 +218,8 @@ class ZSlabReconstructor:
     def stage(self):
         if self.mode == "allgather":
             self.local.stage_rows(self.gathered, rows_per_angle=self.params.n_rows, r0=self.r0)
+        elif self.mode == "p2p":
+            self.local.stage_rows(self.recv, rows_per_angle=self.r1 - self.r0, r0=0)
 
     def run(self, raw_chunk):
         """raw_chunk: device (A, n_rows, n_chan) fp32 counts of this rank's

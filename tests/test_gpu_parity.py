@@ -450,7 +450,7 @@ def test_multi_gpu_zslab_bitwise(F):
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for i, mode in enumerate(("alltoall", "allgather", "p2p")):
+    for i, mode in enumerate(("alltoall", "allgather", "p2p", "p2p-zblocked")):
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
                "--master-addr", "127.0.0.1", "--master-port", str(29500 + i),
                os.path.join(root, "tools", "mgpu_check.py"), "--exchange", mode]
