@@ -34,6 +34,7 @@ struct tf_filter_plan {
     const void* kernel;  // ramp_filter_kernel instantiation for this P
     bool fused;          // fused-I/O FFT path
     int mode;            // 0 generic, 1 fused radix-16, 2 fused radix-8
+    int run;             // mode 2: consecutive line pairs per CTA turn (TF_FILTER_RUN)
 };
 
 namespace tf {
@@ -502,6 +503,18 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kerne
 // over GF(2), so for an index a | c with disjoint bit fields
 // sw8(a | c) = sw8(a) ^ sw8(c): per butterfly leg sw8(c) is a constant, and
 // an immediate address offset wherever it cannot overlap sw8(a)'s bits.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_f2_evict_last(float* p, float a, float b, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(a), "f"(b), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_f1_evict_last(float* p, float a, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(a), "l"(pol) : "memory");
+}
+
 __host__ __device__ constexpr int sw8(int i) { return i ^ ((i >> 4) & 7) ^ (((i >> 6) & 1) << 3); }
 
 // a_sw = sw8(a) for an index a confined to the bits of `amask`; c a constant
@@ -634,7 +647,7 @@ template <int LOG2P>
 __global__ void __launch_bounds__(R8Plan<LOG2P>::T, 1024 / R8Plan<LOG2P>::T)
     ramp_filter_r8(const float* __restrict__ in, float* out, long long n_lines, int n, int, int,
                    const float2* __restrict__ tw_g, const float* __restrict__ mult, const float* __restrict__,
-                   int, float i0, OutMap map, int n_tw) {
+                   int run, float i0, OutMap map, int n_tw) {  // `run` rides in ramp_filter_kernel's blur-radius slot
     constexpr int P = 1 << LOG2P;
     extern __shared__ float2 sbuf[];  // [2][P] ping-pong lines, then the twiddle tables
     __shared__ int32_t s_row0[9];
@@ -652,6 +665,7 @@ __global__ void __launch_bounds__(R8Plan<LOG2P>::T, 1024 / R8Plan<LOG2P>::T)
     const long long n_pairs = (n_lines + 1) / 2;
     const bool log_in = i0 > 0.f;
     const NoIO none;
+    const uint64_t pol = policy_evict_last();
     // raw inputs of this thread's 4 first-pass legs (m = tid + r P/8, r < 4),
     // loaded one pair ahead so the loads overlap the previous pair's inverse
     float2 pf[4];
@@ -667,8 +681,19 @@ __global__ void __launch_bounds__(R8Plan<LOG2P>::T, 1024 / R8Plan<LOG2P>::T)
             if (m < n) pf[r] = make_float2(__ldcs(pa + m), hb ? __ldcs(pa + n + m) : 0.f);
         }
     };
-    prefetch(blockIdx.x);
-    for (long long pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+    // CTA b takes runs of kRun consecutive line pairs: pairs kRun*(b + i*grid) + j.
+    // Consecutive pairs are neighbouring rows of one z-block, so one CTA
+    // completes each 32-B staging sector (8 rows of a channel) within a few
+    // pairs instead of 4 CTAs scattering 8-B pieces of it across L2.
+    const int kRun = run;
+    auto pair_of = [&](long long it) { return kRun * (blockIdx.x + (it / kRun) * gridDim.x) + it % kRun; };
+    prefetch(pair_of(0));
+    for (long long it = 0;; ++it) {
+        const long long pair = pair_of(it);
+        if (pair >= n_pairs) {
+            if (it % kRun == 0) break;  // past the end
+            continue;                   // ragged last run
+        }
         const long long la = 2 * pair;
         const bool has_b = la + 1 < n_lines;
         {
@@ -685,7 +710,7 @@ __global__ void __launch_bounds__(R8Plan<LOG2P>::T, 1024 / R8Plan<LOG2P>::T)
             __syncthreads();  // the previous pair's last pass may still read buffer 0
             r8_run<LOG2P, 0, 0>(sbuf, tws, tid, n, load, mult, none);
         }
-        prefetch(pair + gridDim.x);
+        prefetch(pair_of(it + 1) < n_pairs ? pair_of(it + 1) : pair_of(it + kRun - it % kRun));
         // output pointers resolved after the forward half (fewer live registers)
         int za, zb = 0;
         float* oa = out_ptr(la, n, map, s_row0, s_dst, za);
@@ -702,11 +727,13 @@ __global__ void __launch_bounds__(R8Plan<LOG2P>::T, 1024 / R8Plan<LOG2P>::T)
             }
             const float wm = w ? __ldg(&w[m]) : 1.f;  // feather after the filter (fbp.py:242)
             const float va = y.x * wm, vb = -y.y * wm;
+            // evict_last: a staging line is completed by 16 line pairs; keep the
+            // partial line in L2 until then (the raw input streams evict-first)
             if (pairwise) {
-                *reinterpret_cast<float2*>(oa + (size_t)m * kZP) = make_float2(va, vb);
+                st_f2_evict_last(oa + (size_t)m * kZP, va, vb, pol);
             } else {
-                oa[(size_t)m * kZP] = va;
-                if (has_b) ob[(size_t)m * kZP] = vb;
+                st_f1_evict_last(oa + (size_t)m * kZP, va, pol);
+                if (has_b) st_f1_evict_last(ob + (size_t)m * kZP, vb, pol);
             }
         };
         r8_run<LOG2P, 0, 1>(sbuf, tws, tid, n, none, mult, store);
@@ -767,6 +794,8 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
         if (want == 0 || (want == 1 && p->log2P >= 8) || (want == 2 && P >= 256 && P <= 8192)) p->mode = want;
     }
     p->fused = p->mode != 0;
+    const char* fr = getenv("TF_FILTER_RUN");
+    p->run = fr ? std::max(1, std::min(64, atoi(fr))) : 8;
     if (p->mode == 2) p->threads = std::max(32, P / 8);
     std::vector<float2> tw =
         twiddle_tables(p->mode == 2 ? radix_plan8(p->log2P) : radix_plan(p->log2P, p->mode == 1));
@@ -884,9 +913,10 @@ int build_map(OutMap& map, float* out, int64_t n_lines, int rows_per_angle, int 
 int launch_filter(const tf_filter_plan* p, const float* in, float* out, int64_t n_lines, float i0,
                   const OutMap& map, void* stream) {
     const long long pairs = (n_lines + 1) / 2;
-    const unsigned grid = (unsigned)std::min<long long>(pairs, p->max_grid);
+    const long long units = p->mode == 2 ? (pairs + p->run - 1) / p->run : pairs;  // r8: runs of `run` pairs
+    const unsigned grid = (unsigned)std::min<long long>(units, p->max_grid);
     long long nl = n_lines;
-    int n = p->n, P = p->P, l2 = p->log2P, rad = p->blur_radius;
+    int n = p->n, P = p->P, l2 = p->log2P, rad = p->mode == 2 ? p->run : p->blur_radius;
     const float2* tw = p->d_tw;
     const float* mult = p->d_mult;
     const float* blur = p->d_blur;
