@@ -163,24 +163,31 @@ class StreamedReconstructor:
             self.s_d2h = torch.cuda.Stream(self.device)
 
     def sub_slabs(self, R0, R1):
-        """Sub-slab boundaries: full `slab_rows` slabs in the middle, with the
-        first and last slab cut to a quarter (32-row aligned) so that the
-        un-overlapped pipeline fill (first H2D) and drain (last D2H) are short."""
+        """Sub-slab boundaries: full `slab_rows` slabs in the middle and a
+        geometric ramp at both ends (32, 64, 128, ... rows) so that the
+        un-overlapped pipeline fill (first H2D) and drain (last D2H) are one
+        32-row slab each, while every next slab's H2D still hides under the
+        current slab's compute (compute per row > copy per row)."""
         S = self.slab_rows
-        edge = max(32, (S // 4) // 32 * 32) if S >= 64 else S
+        ramp = []
+        e = 32
+        while e < S:
+            ramp.append(e)
+            e *= 2
+        if R1 - R0 < 2 * sum(ramp) + S:
+            ramp = []
         cuts, r = [], R0
-        if R1 - R0 > 2 * S:
-            cuts.append((r, r + edge))
-            r += edge
-            tail = R1 - edge
-            while r < tail:
-                cuts.append((r, min(r + S, tail)))
-                r = cuts[-1][1]
-            cuts.append((r, R1))
-        else:
-            while r < R1:
-                cuts.append((r, min(r + S, R1)))
-                r = cuts[-1][1]
+        for e in ramp:
+            cuts.append((r, r + e))
+            r += e
+        tail = R1 - sum(ramp)
+        while r < tail:
+            cuts.append((r, min(r + S, tail)))
+            r = cuts[-1][1]
+        for e in reversed(ramp):
+            cuts.append((r, r + e))
+            r += e
+        assert r == R1
         return cuts
 
     def _copy2d(self, dst, dpitch, src, spitch, width, height, stream):
