@@ -350,3 +350,26 @@ def test_cli_error_mapping(tmp_path):
     bad.write_bytes(b"nonsense")
     assert main(["reconstruct", str(bad), "--out", str(tmp_path / "o")]) == 2
     assert main(["reconstruct", str(tmp_path / "missing.sino"), "--out", str(tmp_path / "o")]) == 2
+
+
+@pytest.mark.parametrize("R0,R1,S", [(0, 2048, 256), (0, 1024, 256), (0, 1100, 256), (512, 1024, 256),
+                                     (0, 300, 256), (0, 96, 256), (0, 4096, 128), (7, 999, 64)])
+def test_streamed_sub_slabs_cover_rows_once(R0, R1, S):
+    """engine.StreamedReconstructor.sub_slabs: contiguous, disjoint, in order,
+    covering [R0, R1); never longer than slab_rows; with a ramp, the first and
+    last slabs are 32 rows and each next slab at most doubles (so its H2D
+    hides under the current slab's compute)."""
+    from paper_2505_13955_b200.engine import StreamedReconstructor
+
+    class Cfg:
+        slab_rows = S
+
+    cuts = StreamedReconstructor.sub_slabs(Cfg(), R0, R1)
+    assert cuts[0][0] == R0 and cuts[-1][1] == R1
+    assert all(a < b for a, b in cuts)
+    assert all(cuts[i][1] == cuts[i + 1][0] for i in range(len(cuts) - 1))
+    sizes = [b - a for a, b in cuts]
+    assert max(sizes) <= S
+    if R1 - R0 >= 2 * (S - 32) + S and S > 32:
+        assert sizes[0] == 32 and sizes[-1] == 32
+        assert all(sizes[i + 1] <= 2 * sizes[i] for i in range(len(sizes) // 2))
