@@ -6,10 +6,15 @@
 // band-limited ramp kernel (fbp.py:86-116) and keeps the first n samples.
 // Because the multiplier is real and even, two real lines are filtered by one
 // complex FFT (line a in the real part, line b in the imaginary part).  The
-// FFT is a shared-memory Stockham transform, radix 16/8/4/2, one CTA per
-// line pair, fp32 with fp64-derived twiddles.  Output equals the linear
-// convolution with taps |d| <= n-1 for any pad >= 2n, so the transform
-// always runs at next_pow2(2n) whatever FilterSpec.padding says.
+// FFT is a shared-memory Stockham transform in persistent CTAs (one line pair
+// at a time per CTA), fp32 with fp64-derived twiddles:
+//   mode 2 (default, 256 <= P <= 8192): ramp_filter_r8<log2 P>, radix 8, all
+//          shapes compile-time, ping-pong buffers, XOR swizzle, prefetch;
+//   mode 1 (P = 16384): radix 16 with fused I/O;
+//   mode 0 (blur, P < 256): generic passes plus the Gaussian blur.
+// Output equals the linear convolution with taps |d| <= n-1 for any pad
+// >= 2n, so the transform always runs at next_pow2(2n) whatever
+// FilterSpec.padding says.
 #include <cmath>
 #include <complex>
 #include <cstring>
@@ -247,10 +252,11 @@ __device__ __forceinline__ void fft_pass(float2* buf, const float2* tw, int P, i
 }
 
 // Radix sequences.  Generic path: radix-16 passes, remainder (2/4/8) last.
-// Fused path (P >= 256, no blur): radix 16, then the remainder, then radix
-// 16 -- so the first pass (global input, pruned zero half) and the last
-// pass (global output, pruned half) are always radix 16.
-std::vector<int> radix_plan8(int log2P) {  // fused radix-8 path: 8, remainder, 8, 8, ...
+// Fused radix-16 path (mode 1): radix 16, then the remainder, then radix 16
+// -- so the first pass (global input, pruned zero half) and the last pass
+// (global output, pruned half) are always radix 16.  Radix-8 path (mode 2):
+// 8, remainder, 8, 8, ... (R8Plan mirrors it at compile time).
+std::vector<int> radix_plan8(int log2P) {
     std::vector<int> rs{8};
     const int tail = log2P % 3;
     if (tail) rs.push_back(1 << tail);
