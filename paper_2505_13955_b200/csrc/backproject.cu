@@ -8,19 +8,26 @@
 // below are conflict-free without a swizzle).  Feather weights
 // (fbp.py:242) are folded in while staging.
 //
-// Kernel structure (one CTA = 16x16 voxel columns x one 32-row z-block):
-//   * warp 8 is a TMA producer: per angle it computes, in fp64, the channel
-//     window [c_lo, c_lo+W) the tile's rays hit, and issues one
-//     cp.async.bulk.tensor box {36, W, 1} into a 3-stage x 4-angle smem ring
-//     (mbarrier 'full' barriers; consumers hand slots back on named barriers).  Out-of-detector channels come back as
-//     zeros from the TMA OOB fill -- the reference's zero guard.
-//   * warps 0-7 each own 32 voxel columns x 32 rows in registers; per angle a
-//     thread forms t in fp32 *relative to the tile origin* (origin and window
-//     offset in fp64: |error| ~1e-6 channels even at 8192 channels, where a
-//     plain fp32 t would be off by ~5e-4), then gathers the two taps for all
-//     32 rows with 2x8 LDS.128 and accumulates with 64 FFMA.
+// Kernel structure (default variant: one CTA = 16x16 voxel columns x one
+// 32-row z-block, 4 consumer warps + 1 producer warp, 3 CTAs per SM):
+//   * the producer warp: per angle lane 0 computes, in fp64, the channel
+//     window [c_lo, c_lo+W) the tile's rays hit and issues one
+//     cp.async.bulk.tensor box {36, W, 1} into an 8-stage x 2-angle smem ring
+//     (an mbarrier per slot, completed by the TMA transaction count).  It
+//     refills a slot once every consumer has arrived on the slot's named
+//     barrier (bar.sync parks the warp; no polling).  Out-of-detector
+//     channels come back as zeros from the TMA OOB fill -- the reference's
+//     zero guard.
+//   * each consumer thread owns a pair of voxels along x x 32 rows (64
+//     accumulators); per angle it forms t in fp32 *relative to the tile
+//     origin* (origin and window offset in fp64: |error| ~1e-6 channels even
+//     at 8192 channels, where a plain fp32 t would be off by ~5e-4), reads
+//     the pair's 3 taps for all 32 rows with 3x8 LDS.128 (6 B of shared
+//     memory per update) and accumulates with 96 packed FFMA2 using the
+//     exact two-tap weights of each voxel (bit-identical to the 2-tap V1).
 //   * epilogue: FoV mask evaluated in fp64 exactly as fbp.py:247-250, scale by
-//     float32(angle_span / n_proj) (fbp.py:251), coalesced stores.
+//     float32(angle_span / n_proj) (fbp.py:251), coalesced stores -- or, for
+//     angle-split partials (RED), adds into each row's owner slab.
 // Tiles wholly outside the field of view skip the angle loop.
 #include <algorithm>
 #include <cmath>
