@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
     // per-angle setup: detector coordinates -> tap row + interpolation weights
     const uint8_t* ring_z = ring + zg * ZT * 4;
     auto setup = [&](int g, const float*& p0, float (&w)[VX * VY][NT], int& cls) {
-        const int slot = g & (L::RING - 1);
+        const int slot = g % L::RING;  // RING need not be a power of 2
         const float4 p = prm[slot];
         const uint8_t* base = ring_z + slot * args.slot_bytes;
         cls = 0;
