@@ -520,36 +520,63 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
 }
 
 // ---- staging: angle-major rows -> z-blocked, feather-weighted ------------
+// One block turn = 32 rows x 64 channels of one (angle, z-block): float4
+// loads along channels (coalesced rows), transposed through shared memory,
+// written back as 64 contiguous 144-B channel rows (fully coalesced float4
+// stores, pad floats zeroed).
 __global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ sino, float* __restrict__ stage,
                                                     const float* __restrict__ w, int n_proj, int n_chan,
                                                     int rows_per_angle, int r0, int n_rows, int nzb) {
-    __shared__ float tile[kZB][33];
-    const int nch = (n_chan + 31) / 32;
+    constexpr int CB = 64;                    // channels per turn
+    __shared__ float tile[kZB][CB + 1];       // +1: conflict-light column reads
+    const int nch = (n_chan + CB - 1) / CB;
     const long long total = (long long)n_proj * nzb * nch;
+    const bool vec = (n_chan % 4) == 0 && (reinterpret_cast<uintptr_t>(sino) & 15) == 0;  // float4-aligned rows
     for (long long blk = blockIdx.x; blk < total; blk += gridDim.x) {
         const int cb = (int)(blk % nch);
         const long long kz = blk / nch;
         const int zb = (int)(kz % nzb);
         const int k = (int)(kz / nzb);
-        const int c0 = cb * 32;
-        // load 32 rows x 32 channels (coalesced along channels)
-        for (int i = threadIdx.x; i < kZB * 32; i += 256) {
-            const int zi = i >> 5, c = i & 31;
+        const int c0 = cb * CB;
+        // load 32 rows x 64 channels: 512 float4, 2 per thread, both in flight
+        float4 v[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int i = threadIdx.x + u * 256;
+            const int zi = i >> 4, c = (i & 15) * 4;
             const int row = zb * kZB + zi;
-            float v = 0.f;
-            if (row < n_rows && c0 + c < n_chan)
-                v = sino[((size_t)k * rows_per_angle + r0 + row) * n_chan + c0 + c] * w[c0 + c];
-            tile[zi][c] = v;
+            const size_t off = ((size_t)k * rows_per_angle + r0 + row) * n_chan + c0 + c;
+            v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (row < n_rows) {
+                if (vec && c0 + c + 3 < n_chan) {
+                    v[u] = __ldcs(reinterpret_cast<const float4*>(sino + off));
+                } else {
+                    if (c0 + c + 0 < n_chan) v[u].x = sino[off + 0];
+                    if (c0 + c + 1 < n_chan) v[u].y = sino[off + 1];
+                    if (c0 + c + 2 < n_chan) v[u].z = sino[off + 2];
+                    if (c0 + c + 3 < n_chan) v[u].w = sino[off + 3];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int i = threadIdx.x + u * 256;
+            const int zi = i >> 4, c = (i & 15) * 4;
+            // feather after the filter (fbp.py:242), fp32 product
+            tile[zi][c + 0] = v[u].x * (c0 + c + 0 < n_chan ? w[c0 + c + 0] : 0.f);
+            tile[zi][c + 1] = v[u].y * (c0 + c + 1 < n_chan ? w[c0 + c + 1] : 0.f);
+            tile[zi][c + 2] = v[u].z * (c0 + c + 2 < n_chan ? w[c0 + c + 2] : 0.f);
+            tile[zi][c + 3] = v[u].w * (c0 + c + 3 < n_chan ? w[c0 + c + 3] : 0.f);
         }
         __syncthreads();
-        // write 32 channels x 36 floats, contiguous
+        // write 64 channels x 36 floats = 576 contiguous float4
         float* dst = stage + (((size_t)k * nzb + zb) * n_chan + c0) * kZP;
-        const int nc = min(32, n_chan - c0);
+        const int nc = min(CB, n_chan - c0);
         for (int i = threadIdx.x; i < nc * (kZP / 4); i += 256) {
             const int c = i / (kZP / 4), z4 = (i % (kZP / 4)) * 4;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (z4 < kZB) v = make_float4(tile[z4][c], tile[z4 + 1][c], tile[z4 + 2][c], tile[z4 + 3][c]);
-            *reinterpret_cast<float4*>(dst + (size_t)c * kZP + z4) = v;
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (z4 < kZB) o = make_float4(tile[z4][c], tile[z4 + 1][c], tile[z4 + 2][c], tile[z4 + 3][c]);
+            *reinterpret_cast<float4*>(dst + (size_t)c * kZP + z4) = o;
         }
         __syncthreads();
     }
@@ -797,7 +824,7 @@ extern "C" int tf_bp_stage(const tf_bp_plan* p, const float* sino, int rows_per_
     if (n_rows == 0) return TF_OK;
     if (!sino || !stage) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
     const int nzb = (n_rows + kZB - 1) / kZB;
-    const long long total = (long long)p->g.n_proj * nzb * ((p->g.n_chan + 31) / 32);
+    const long long total = (long long)p->g.n_proj * nzb * ((p->g.n_chan + 63) / 64);
     const int grid = (int)std::min<long long>(total, 148LL * 16);
     stage_kernel<<<grid, 256, 0, as_stream(stream)>>>(sino, static_cast<float*>(stage), p->d_w, p->g.n_proj,
                                                       p->g.n_chan, rows_per_angle, r0, n_rows, nzb);
