@@ -435,6 +435,13 @@ def test_filter_slab_map_matches_host_restatement(F):
                           chunk.numel() // 40, 1e5, 22, world, r0, b0,
                           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
     assert torch.equal(send, slab_major(natural, slabs))
+    # tf_filter_peers (the p2p exchange's store stream) with every destination
+    # slab a local pointer: the same rows, slab by slab
+    send2 = torch.full_like(send, float("nan"))
+    dst = (ctypes.c_void_p * world)(*[send2.data_ptr() + 4 * b for b in base])
+    check(lib().tf_filter_peers(eng.fplan.handle, ctypes.c_void_p(chunk.data_ptr()), chunk.numel() // 40, 1e5, 22,
+                                world, r0, dst, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    assert torch.equal(send2, send)
 
 
 def test_multi_gpu_zslab_bitwise(F):
