@@ -579,7 +579,9 @@ __device__ __forceinline__ void dft8_ip(float2 (&v)[8]) {
 __host__ __device__ constexpr int dft8_pos(int k) { return (k & 1) * 4 + k / 2; }
 
 // One Stockham pass (radix R, input stride NS) of a P-point line: src -> dst.
-template <int LOG2P, int R, int NS, int IN, int OUT, class Load, class Store>
+// FULL: n == P/2 (power-of-two line length), so every first-pass input leg is
+// inside the line and exactly the last pass's legs r < R/2 are stored.
+template <int LOG2P, int R, int NS, int IN, int OUT, bool FULL, class Load, class Store>
 __device__ __forceinline__ void r8_pass(const float2* src, float2* dst, const float2* tw, int tid, int n,
                                         const Load& load, const float* __restrict__ mult, const Store& store) {
     constexpr int P = 1 << LOG2P, T = P / 8, NB = 8 / R, STRIDE = P / R;
@@ -626,14 +628,14 @@ __device__ __forceinline__ void r8_pass(const float2* src, float2* dst, const fl
                 dst[sw8_join(b_sw, BMASK, r * NS)] = make_float2(x.x * g, -x.y * g);
             } else {
                 const int m = base + r * NS;
-                if (m < n) store(m, x);
+                if (FULL ? r < R / 2 : m < n) store(m, x);
             }
         }
     }
 }
 
 // Passes I.. of one direction; pass G = DIR * NP + I writes buffer G % 2.
-template <int LOG2P, int I, int DIR, class Load, class Store>
+template <int LOG2P, int I, int DIR, bool FULL, class Load, class Store>
 __device__ __forceinline__ void r8_run(float2* bufs, const float2* tw, int tid, int n, const Load& load,
                                        const float* mult, const Store& store) {
     using PL = R8Plan<LOG2P>;
@@ -641,35 +643,25 @@ __device__ __forceinline__ void r8_run(float2* bufs, const float2* tw, int tid, 
         constexpr int G = DIR * PL::NP + I;
         constexpr int IN = (DIR == 0 && I == 0) ? IN_GLOBAL : IN_SMEM;
         constexpr int OUT = I == PL::NP - 1 ? (DIR == 0 ? OUT_MULT : OUT_GLOBAL) : OUT_SMEM;
-        r8_pass<LOG2P, PL::radix(I), PL::ns(I), IN, OUT>(bufs + ((G + 1) % 2) * PL::P, bufs + (G % 2) * PL::P,
-                                                         tw + PL::twoff(I), tid, n, load, mult, store);
+        r8_pass<LOG2P, PL::radix(I), PL::ns(I), IN, OUT, FULL>(bufs + ((G + 1) % 2) * PL::P,
+                                                               bufs + (G % 2) * PL::P, tw + PL::twoff(I), tid, n,
+                                                               load, mult, store);
         if constexpr (OUT != OUT_GLOBAL) __syncthreads();
-        r8_run<LOG2P, I + 1, DIR>(bufs, tw, tid, n, load, mult, store);
+        r8_run<LOG2P, I + 1, DIR, FULL>(bufs, tw, tid, n, load, mult, store);
     }
 }
 
-// Same arguments as ramp_filter_kernel (blur/radius unused: no blur in mode 2).
-template <int LOG2P>
-__global__ void __launch_bounds__(R8Plan<LOG2P>::T, 1024 / R8Plan<LOG2P>::T)
-    ramp_filter_r8(const float* __restrict__ in, float* out, long long n_lines, int n, int, int,
-                   const float2* __restrict__ tw_g, const float* __restrict__ mult, const float* __restrict__,
-                   int run, float i0, OutMap map, int n_tw) {  // `run` rides in ramp_filter_kernel's blur-radius slot
+// The persistent line-pair loop of ramp_filter_r8.
+template <int LOG2P, bool FULL>
+__device__ __forceinline__ void r8_pairs(const float* __restrict__ in, long long n_lines, int n,
+                                         const float* __restrict__ mult, float i0, const OutMap& map, int run,
+                                         float2* sbuf, const float2* tws, const int32_t* s_row0,
+                                         float* const* s_dst) {
     constexpr int P = 1 << LOG2P;
-    extern __shared__ float2 sbuf[];  // [2][P] ping-pong lines, then the twiddle tables
-    __shared__ int32_t s_row0[9];
-    __shared__ float* s_dst[8];
     const int tid = threadIdx.x;
-    if (tid == 0) {
-#pragma unroll
-        for (int s = 0; s < 9; ++s) s_row0[s] = map.row0[s];
-#pragma unroll
-        for (int s = 0; s < 8; ++s) s_dst[s] = map.dst[s];
-    }
-    float2* tws = sbuf + 2 * P;
-    for (int m = tid; m < n_tw; m += R8Plan<LOG2P>::T) tws[m] = tw_g[m];
-    __syncthreads();
     const long long n_pairs = (n_lines + 1) / 2;
     const bool log_in = i0 > 0.f;
+    const float inv_i0 = 1.f / i0;
     const NoIO none;
     const uint64_t pol = policy_evict_last();
     // raw inputs of this thread's 4 first-pass legs (m = tid + r P/8, r < 4),
@@ -684,7 +676,7 @@ __global__ void __launch_bounds__(R8Plan<LOG2P>::T, 1024 / R8Plan<LOG2P>::T)
         for (int r = 0; r < 4; ++r) {
             const int m = tid + r * (P / 8);
             pf[r] = make_float2(0.f, 0.f);
-            if (m < n) pf[r] = make_float2(__ldcs(pa + m), hb ? __ldcs(pa + n + m) : 0.f);
+            if (FULL || m < n) pf[r] = make_float2(__ldcs(pa + m), hb ? __ldcs(pa + n + m) : 0.f);
         }
     };
     // CTA b takes runs of kRun consecutive line pairs: pairs kRun*(b + i*grid) + j.
@@ -705,20 +697,20 @@ __global__ void __launch_bounds__(R8Plan<LOG2P>::T, 1024 / R8Plan<LOG2P>::T)
         {
             // the two lines as one complex line, Beer-Lambert fused (fbp.py:80-83)
             auto load = [&](int r, int m) -> float2 {
-                if (m >= n) return make_float2(0.f, 0.f);
+                if (!FULL && m >= n) return make_float2(0.f, 0.f);
                 float a = pf[r].x, b = pf[r].y;
                 if (log_in) {  // -ln(max(raw, 1) / i0)
                     // MUFU.LG2-based log of the ratio (in (0, 1]): |error| < 4e-7 for
                     // ratios in [0.5, 1], ~1 ulp relative below -- far inside the fp32
                     // filter's own error, and 8 logs per thread per pair were ~8% of
                     // K1's instructions with the polynomial logf
-                    a = -__logf(__fdiv_rn(fmaxf(a, 1.f), i0));
-                    b = has_b ? -__logf(__fdiv_rn(fmaxf(b, 1.f), i0)) : 0.f;
+                    a = -__logf(fmaxf(a, 1.f) * inv_i0);
+                    b = has_b ? -__logf(fmaxf(b, 1.f) * inv_i0) : 0.f;
                 }
                 return make_float2(a, b);
             };
             __syncthreads();  // the previous pair's last pass may still read buffer 0
-            r8_run<LOG2P, 0, 0>(sbuf, tws, tid, n, load, mult, none);
+            r8_run<LOG2P, 0, 0, FULL>(sbuf, tws, tid, n, load, mult, none);
         }
         prefetch(pair_of(it + 1) < n_pairs ? pair_of(it + 1) : pair_of(it + kRun - it % kRun));
         // output pointers resolved after the forward half (fewer live registers)
@@ -746,8 +738,32 @@ __global__ void __launch_bounds__(R8Plan<LOG2P>::T, 1024 / R8Plan<LOG2P>::T)
                 if (has_b) st_f1_evict_last(ob + (size_t)m * kZP, vb, pol);
             }
         };
-        r8_run<LOG2P, 0, 1>(sbuf, tws, tid, n, none, mult, store);
+        r8_run<LOG2P, 0, 1, FULL>(sbuf, tws, tid, n, none, mult, store);
     }
+}
+
+// Same arguments as ramp_filter_kernel (blur/radius unused: no blur in mode 2).
+template <int LOG2P>
+__global__ void __launch_bounds__(R8Plan<LOG2P>::T, 1024 / R8Plan<LOG2P>::T)
+    ramp_filter_r8(const float* __restrict__ in, float* out, long long n_lines, int n, int, int,
+                   const float2* __restrict__ tw_g, const float* __restrict__ mult, const float* __restrict__,
+                   int run, float i0, OutMap map, int n_tw) {  // `run` rides in ramp_filter_kernel's blur-radius slot
+    constexpr int P = 1 << LOG2P;
+    extern __shared__ float2 sbuf[];  // [2][P] ping-pong lines, then the twiddle tables
+    __shared__ int32_t s_row0[9];
+    __shared__ float* s_dst[8];
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < 9; ++s) s_row0[s] = map.row0[s];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) s_dst[s] = map.dst[s];
+    }
+    float2* tws = sbuf + 2 * P;
+    for (int m = tid; m < n_tw; m += R8Plan<LOG2P>::T) tws[m] = tw_g[m];
+    __syncthreads();
+    if (2 * n == P) r8_pairs<LOG2P, true>(in, n_lines, n, mult, i0, map, run, sbuf, tws, s_row0, s_dst);
+    else r8_pairs<LOG2P, false>(in, n_lines, n, mult, i0, map, run, sbuf, tws, s_row0, s_dst);
 }
 
 template <typename T>
