@@ -109,6 +109,22 @@ class SlabReconstructor:
         self.filter_stage(raw, stream=stream)
         return self.backproject(stream=stream)
 
+    def capture(self, raw):
+        """Record run(raw) -- K1 into staging, K2 into self.vol -- as a CUDA
+        graph and return it; `graph.replay()` re-runs the step on whatever
+        `raw` holds then, with one launch from the host.  The library call
+        path allocates nothing, so it is capture-safe."""
+        torch = self.torch
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            self.run(raw)  # warm-up outside the graph (kernel attributes, tensor-map encoder)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self.run(raw)
+        return graph
+
     def updates(self) -> int:
         """Voxel x projection updates of one run (pipeline.py:225-227 convention)."""
         return self.params.n_proj * self.k * self.dims.nx * self.dims.ny
