@@ -10,7 +10,6 @@ the reference's prefixes and exit code 2 (cli.py:264-285).
 from __future__ import annotations
 
 import argparse
-import os
 import sys
 from pathlib import Path
 

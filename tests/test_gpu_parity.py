@@ -11,7 +11,7 @@ import math
 import numpy as np
 import pytest
 
-from conftest import oracle_geom, ref_objects, rel_l2
+from conftest import ref_objects, rel_l2
 
 pytestmark = pytest.mark.gpu
 

@@ -1,8 +1,7 @@
 """Micro-benchmark of K1 (dev tool): natural vs fused z-blocked output."""
-import argparse, json, os, sys, ctypes
+import argparse, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from paper_2505_13955_b200._lib import check, lib
 from paper_2505_13955_b200.engine import SlabReconstructor, phantom_raw
 from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
 
