@@ -179,19 +179,30 @@ class StreamedReconstructor:
             self.s_d2h = torch.cuda.Stream(self.device)
 
     def sub_slabs(self, R0, R1):
-        """Sub-slab boundaries: full `slab_rows` slabs in the middle and a
-        geometric ramp at both ends (32, 64, 128, ... rows) so that the
-        un-overlapped pipeline fill (first H2D) and drain (last D2H) are one
-        32-row slab each, while every next slab's H2D still hides under the
-        current slab's compute (compute per row > copy per row)."""
+        """Sub-slab boundaries: full slabs in the middle and a geometric ramp
+        at both ends (32, 64, 128, ... rows) so that the un-overlapped
+        pipeline fill (first H2D) and drain (last D2H) are one 32-row slab
+        each, while every next slab's H2D still hides under the current
+        slab's compute (compute per row > copy per row).  When the range is
+        too short for the ramp up to `slab_rows` (a z-slab of one GPU among
+        several: 512 rows at N=4), the middle slab size halves until the ramp
+        fits, instead of falling back to two un-overlapped full slabs."""
         S = self.slab_rows
+
+        def ramp_to(s):
+            r, e = [], 32
+            while e < s:
+                r.append(e)
+                e *= 2
+            return r
+
         ramp = []
-        e = 32
-        while e < S:
-            ramp.append(e)
-            e *= 2
-        if R1 - R0 < 2 * sum(ramp) + S:
-            ramp = []
+        s = S
+        while s >= 64:
+            if R1 - R0 >= 2 * sum(ramp_to(s)) + s:
+                S, ramp = s, ramp_to(s)
+                break
+            s //= 2
         cuts, r = [], R0
         for e in ramp:
             cuts.append((r, r + e))
