@@ -395,6 +395,11 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        from paper_2505_13955_b200.hostnuma import bind_to_device
+
+        numa = bind_to_device(local)  # pinned e2e buffers on the GPU's node (no-op on 1-node hosts)
+    else:
+        numa = None
     p, d = geometry(cfg)
     n, n_proj = cfg["n"], cfg["n_proj"]
     total_updates = n_proj * n * n * n
@@ -567,7 +572,8 @@ def main():
                "s_per_volume": round(e2e_ms / 1e3, 4), "steps": ke,
                "path": f"engine.StreamedReconstructor: pinned host sinogram -> {args.slab_rows}-row z-sub-slabs, "
                        "H2D / kernels / D2H on 3 streams (double-buffered); bytes are per rank",
-               "matches_device_resident_volume": same}
+               "matches_device_resident_volume": same,
+               "host_numa": numa}
         del streamed
 
     # ---- parity spot check on the bench data (rank 0): 2 rows x 256^2 centre tile vs the C oracle

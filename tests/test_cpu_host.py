@@ -375,3 +375,12 @@ def test_streamed_sub_slabs_cover_rows_once(R0, R1, S):
     if R1 - R0 >= 128 and S >= 64:  # the ramp fits once the middle slab may shrink to 64 rows
         assert sizes[0] == 32 and sizes[-1] == 32
         assert all(sizes[i + 1] <= 2 * sizes[i] for i in range(len(sizes) // 2))
+
+
+def test_hostnuma_cpulist_parse():
+    """hostnuma._parse_cpulist reads sysfs local_cpulist syntax."""
+    from paper_2505_13955_b200.hostnuma import _parse_cpulist
+
+    assert _parse_cpulist("0-3,8,10-11\n") == {0, 1, 2, 3, 8, 10, 11}
+    assert _parse_cpulist("5") == {5}
+    assert _parse_cpulist("") == set()
