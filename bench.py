@@ -41,7 +41,9 @@ CONFIGS = {
 PITCH = 12.0   # um (config.py:40,47)
 I0 = 1e5       # config.py:59
 SM_COUNT = 148
-SMEM_BYTES_PER_CLK = 128  # per SM
+# per SM per clock, measured: conflict-free LDS.128 over all 148 SMs, each SM timed on its own
+# clock64 (tools/micro/smem_rate.cu -> profiles/r01_smem_rate.jsonl; nominal 128)
+SMEM_BYTES_PER_CLK = 127.69
 TX = TY = 16   # BP tile (csrc/backproject.cu)
 ZB = 32
 
@@ -648,7 +650,8 @@ def main():
             "frac": round(smem_achieved / smem_peak, 4),
             "traffic": traffic["bytes_per_launch"] if traffic else None,
             "traffic_detail": traffic,
-            "peak_source": "derived: 128 B/clk/SM x 148 SMs x measured median SM clock "
+            "peak_source": "measured 127.69 B/clk/SM (conflict-free LDS.128, tools/micro/smem_rate.cu, "
+                           "profiles/r01_smem_rate.jsonl) x 148 SMs x measured median SM clock "
                            "(shared-memory data path; no tensor-core or HBM bound applies, SURVEY 8d)",
             "roof_updates_per_s_e9": round(smem_peak / bytes_per_update, 1),
             "algorithmic_bytes_per_update": bytes_per_update,
