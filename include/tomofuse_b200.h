@@ -202,6 +202,26 @@ TF_API int tf_bp_smem_bytes_per_update(const tf_bp_plan* plan, int flags, double
 TF_API int tf_bp_kernel_info(const tf_bp_plan* plan, int flags, int n_rows, int a0, int a1, double* bytes,
                              int64_t* executed_updates);
 
+/* ---- tensor-core back-projection (K2-TC, same contract as tf_backproject) --
+ * The same sum as tf_backproject (fbp.py:186-252) computed as per-angle GEMMs
+ * D[voxel][row] += W[voxel][chan] * T[chan][row] on tcgen05 (fp16 hi/lo split
+ * operands, fp32 TMEM accumulation): 16 x 8 voxel tiles, exact two-tap
+ * weights.  Not bitwise equal to the CUDA-core kernels (different summation
+ * order); within the fp32 tolerance of the reference float64 output.
+ * 1. tf_bp_tc_prepare converts angles [a0, a1) of a z-blocked staging buffer
+ *    (tf_filter_stage / tf_bp_stage output for n_rows rows) into `ws`
+ *    (tf_bp_tc_workspace_bytes): fp16 hi/lo taps scaled by a device-chosen
+ *    power of two, stream-ordered, no host sync.
+ * 2. tf_backproject_tc back-projects angles [a0, a1) within the prepared
+ *    [ws_a0, ws_a1), flags as tf_backproject (TF_BP_ACCUMULATE/FINALIZE).
+ * Requires voxel_pitch / pixel_pitch <= 1.5 (tf_bp_tc_supported). */
+TF_API int tf_bp_tc_supported(const tf_bp_plan* plan);
+TF_API int64_t tf_bp_tc_workspace_bytes(const tf_bp_plan* plan, int n_rows, int a0, int a1);
+TF_API int tf_bp_tc_prepare(const tf_bp_plan* plan, const void* stage, int n_rows, int a0, int a1, void* ws,
+                            void* stream);
+TF_API int tf_backproject_tc(const tf_bp_plan* plan, const void* ws, int ws_a0, int ws_a1, int n_rows, float* vol,
+                             int a0, int a1, int x0, int x1, int y0, int y1, int flags, void* stream);
+
 /* ---- quantize (fbp.py:255-259) ------------------------------------------ */
 /* vol is fp32 or fp64 (vol_dtype); arithmetic is fp64, round-half-even,
  * bit-identical to numpy for the same input values. */

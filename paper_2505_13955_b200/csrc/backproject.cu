@@ -34,6 +34,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "internal.hpp"
 
@@ -43,8 +45,8 @@ struct tf_bp_plan {
     double2* d_trig;  // (cos, sin) of k * (span / n_proj), fp64 libm, per angle
     float* d_w;       // feather weights (fp32, as numpy casts them)
     double ext;       // max channel extent of a tile's rays over all angles
-    int* d_order[4];  // launch order of the tiles (Morton, FoV-active first) per tile shape
-    int n_active[4];
+    int* d_order[5];  // launch order of the tiles (Morton, FoV-active first) per tile shape
+    int n_active[5];
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
 };
@@ -647,8 +649,9 @@ bool tile_order_enabled() {
 }
 
 // tile shapes (TX, TY) with a launch order each; variant -> shape
-constexpr int kNumShapes = 4;
-constexpr int kTileShape[kNumShapes][2] = {{16, 16}, {32, 16}, {24, 16}, {24, 8}};
+constexpr int kNumShapes = 5;
+// shape 4 (16 x 8 = 128 voxels, the MMA M) is the tensor-core kernel's tile (backproject_tc below)
+constexpr int kTileShape[kNumShapes][2] = {{16, 16}, {32, 16}, {24, 16}, {24, 8}, {16, 8}};
 int variant_shape(int v) { return v == 10 ? 1 : (v >= 13 ? 3 : (v >= 11 ? 2 : 0)); }
 
 // smem bytes gathered per update: 16 B per LDS.128 of 4 rows, taps / voxels
@@ -1008,4 +1011,527 @@ extern "C" int tf_backproject_reduce(const tf_bp_plan* p, const void* stage, int
     for (int s = 0; s < n_slabs; ++s) rm.dst[s] = static_cast<float*>(slab_dst[s]);
     return backproject_impl(p, stage, n_rows, nullptr, a0, a1, 0, p->g.nx, 0, p->g.ny,
                             (flags & TF_BP_KERNEL_V1) | TF_BP_REDUCE, stream, &rm, a0);
+}
+
+// ============================================================================
+// K2-TC: back-projection on the 5th-generation tensor cores (tcgen05).
+//
+// For one angle, a tile of M = 128 voxel columns (16 x 8) and N detector rows,
+// back-projection is a small GEMM: D[m][z] += sum_k W[m][k] * T[k][z], with
+// T the filtered taps of the tile's channel window [c_lo, c_lo + 32) and W the
+// interpolation matrix -- row m holds voxel m's exact two-tap weights
+// {1 - f, f} at k = floor(t) - c_lo and k + 1, zeros elsewhere (fbp.py:237-245).
+// Summed over all angles, D is the unscaled back-projection.  The tensor core
+// runs at 8192 FLOP/clk/SM (128 x 256 x 16 fp16 MMA in 128 clk, measured,
+// tools/micro/umma_probe.cu), so even at 2 x 32 FLOP per update it outruns the
+// shared-memory gather of the CUDA-core kernel.
+//
+// Precision: fp32 operands are split into fp16 pairs (hi + lo, 22 significant
+// bits) and D accumulates W_hi T_hi + W_lo T_hi + W_hi T_lo in fp32 TMEM (the
+// dropped W_lo T_lo term is < 2^-22 relative).  The taps are scaled by a
+// power of two 2^e (from the data's max |T|, computed on the device) so they
+// sit in fp16's normal range; the epilogue multiplies by 2^-e exactly.
+//
+// Roles per CTA (192 threads, one CTA per SM):
+//   warp 0  TMA producer: per angle the fp64 window origin (same operations as
+//           bp_kernel) and two TMA loads (T_hi, T_lo boxes of N rows x 32
+//           channels, MN-major canonical layout) into a 6-stage ring; the OOB
+//           zero fill is the reference's zero guard for off-detector taps.
+//   warp 1  TMEM owner + MMA issuer (one thread): 6 tcgen05.mma per angle
+//           (2 K-steps x 3 split products) into one fp32 accumulator of N
+//           TMEM columns, tcgen05.commit frees the stage.
+//   warps 2-5  one voxel per thread: fp32 t relative to the fp64 window
+//           origin (as bp_kernel), the weights as fp16 hi/lo K-major rows of
+//           the W tile; after the last angle the epilogue: tcgen05.ld of the
+//           voxel's N rows, x 2^-e, FoV mask and angle weight (fbp.py:247-251).
+// ============================================================================
+namespace tf {
+namespace {
+constexpr int kTcTX = 16, kTcTY = 8, kTcM = kTcTX * kTcTY;  // voxels per CTA = MMA M
+constexpr int kTcK = 32;                                     // channel window (2 MMA K-steps of 16)
+constexpr int kTcStages = 6;
+constexpr int kTcThreads = 192;
+constexpr int kTcShape = 4;                                  // kTileShape[4] = {16, 8}
+constexpr int kTcHeader = 256;                               // workspace header: absmax bits, exponent
+
+struct TCArgs {
+    const double2* trig;
+    const int* order;
+    const int* d_exp;  // power-of-2 exponent of the fp16 tap scale (workspace header)
+    float* vol;
+    int a0, a1, ws_a0, n_rows, nx, ny, n_chan;
+    int x0, x1, y0, y1;
+    int ntx, N, flags;
+    double cx, cy, scale, axis, R2, sc2;
+    float angle_wf;
+};
+
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (sm_100); SWIZZLE_NONE, base offset 0
+    return d;
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_h2(__half lo, __half hi) {
+    return (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+}
+
+// the tile's channel window for angle k: fp64, same operation order as bp_kernel's producer
+struct TcWin {
+    int c_lo;
+    float F0, B, C;
+};
+__device__ __forceinline__ TcWin tc_window(double dX, double dY, double2 cs, const TCArgs& a) {
+    double t0 = __dadd_rn(__dmul_rn(dX, cs.x), __dmul_rn(dY, cs.y));
+    t0 = __dadd_rn(__dmul_rn(t0, a.scale), a.axis);
+    const double B = cs.x * a.scale, C = cs.y * a.scale;
+    const double tmin = t0 + fmin(0.0, B * (kTcTX - 1)) + fmin(0.0, C * (kTcTY - 1));
+    TcWin w;
+    w.c_lo = (int)floor(tmin);
+    w.F0 = (float)(t0 - (double)w.c_lo);
+    w.B = (float)B;
+    w.C = (float)C;
+    return w;
+}
+
+__device__ __forceinline__ bool tc_outside_fov(int x, int y, const TCArgs& a) {
+    double dx = __dsub_rn((double)x, a.cx), dy = __dsub_rn((double)y, a.cy);
+    double rr = __dmul_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), a.sc2);
+    return rr > a.R2;
+}
+
+// 32 consecutive angles' windows, one per lane (g0 + lane); read back with tc_bcast
+__device__ __forceinline__ TcWin tc_window_lane(int g0, int n_ang, double dX, double dY, const TCArgs& a) {
+    const int lane = threadIdx.x & 31;
+    const int g = min(g0 + lane, n_ang - 1);
+    return tc_window(dX, dY, a.trig[a.a0 + g], a);
+}
+__device__ __forceinline__ TcWin tc_bcast(const TcWin& w, int src) {
+    TcWin r;
+    r.c_lo = __shfl_sync(0xffffffffu, w.c_lo, src);
+    r.F0 = __shfl_sync(0xffffffffu, w.F0, src);
+    r.B = __shfl_sync(0xffffffffu, w.B, src);
+    r.C = __shfl_sync(0xffffffffu, w.C, src);
+    return r;
+}
+
+#define TC_LD32(ta, v)                                                                                            \
+    asm volatile(                                                                                                 \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"  \
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                         \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),          \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),    \
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),  \
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])   \
+        : "r"(ta))
+#define TC_ST32(ta, v)                                                                                            \
+    asm volatile(                                                                                                 \
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"  \
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta),                              \
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),         \
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), \
+        "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]),           \
+        "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])                                     \
+        : "memory")
+
+// TMEM columns: two MMA accumulators (ping-pong per block of kTcP angles) and
+// the round-to-nearest master sum, N = 128 columns each.
+constexpr int kTcN = 128;  // rows per CTA (MMA N)
+constexpr int kTcP = 16;   // angles per accumulator block (the tensor core's fp32 accumulation truncates:
+                           // its bias grows with the count, so blocks are re-added in RN fp32 by threads)
+
+__global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_constant__ CUtensorMap map, const TCArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
+    const int tx = tile % a.ntx, ty = tile / a.ntx;
+    const int X0 = tx * kTcTX, Y0 = ty * kTcTY;
+    const int zr0 = blockIdx.y * kTcN;
+    const int xe = min(X0 + kTcTX, a.nx), ye = min(Y0 + kTcTY, a.ny);
+    const int ux0 = max(X0, a.x0), ux1 = min(xe, a.x1);
+    const int uy0 = max(Y0, a.y0), uy1 = min(ye, a.y1);
+    if (ux0 >= ux1 || uy0 >= uy1) return;
+    const size_t plane = (size_t)a.nx * a.ny;
+    {
+        int nxv = (int)fmin(fmax(rint(a.cx), (double)X0), (double)(xe - 1));
+        int nyv = (int)fmin(fmax(rint(a.cy), (double)Y0), (double)(ye - 1));
+        bool all_out = true;
+        for (int ddx = -1; ddx <= 1; ++ddx)
+            for (int ddy = -1; ddy <= 1; ++ddy) {
+                int xx = min(max(nxv + ddx, X0), xe - 1), yy = min(max(nyv + ddy, Y0), ye - 1);
+                all_out = all_out && tc_outside_fov(xx, yy, a);
+            }
+        if (all_out) {
+            if (a.flags & TF_BP_FINALIZE) {
+                const int nz = min(kTcN, a.n_rows - zr0);
+                for (int i = threadIdx.x; i < kTcM * nz; i += blockDim.x) {
+                    int z = i / kTcM, r = i % kTcM;
+                    int x = X0 + (r % kTcTX), y = Y0 + (r / kTcTX);
+                    if (x >= ux0 && x < ux1 && y >= uy0 && y < uy1) a.vol[(size_t)(zr0 + z) * plane + (size_t)y * a.nx + x] = 0.f;
+                }
+            }
+            return;
+        }
+    }
+
+    constexpr uint32_t bbytes = kTcN * kTcK * 2;   // one split of the tap box
+    constexpr uint32_t abytes = kTcM * kTcK * 2;   // one split of the weight tile
+    constexpr uint32_t stage_bytes = 2 * bbytes + 2 * abytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * stage_bytes);
+    uint64_t* afull = full + kTcStages;
+    uint64_t* empty = afull + kTcStages;
+    uint64_t* accfull = empty + kTcStages;  // [2]: MMA block done -> flush
+    uint64_t* accfree = accfull + 2;        // [2]: flushed -> MMA may overwrite
+    uint64_t* done = accfree + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&afull[s], 4);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&accfull[b], 1);
+            mbar_init(&accfree[b], 4);
+        }
+        mbar_init(done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "n"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;  // columns [0,128) acc0, [128,256) acc1, [256,384) master
+    const int n_ang = a.a1 - a.a0;
+    const int n_blk = (n_ang + kTcP - 1) / kTcP;
+    const double dX = (double)X0 - a.cx, dY = (double)Y0 - a.cy;
+
+    if (warp == 0) {
+        // ---- TMA producer: windows for 32 angles per batch, one per lane
+        if (lane == 0) tma_prefetch_desc(&map);
+        for (int g0 = 0; g0 < n_ang; g0 += 32) {
+            const TcWin wl = tc_window_lane(g0, n_ang, dX, dY, a);
+            const int gn = min(32, n_ang - g0);
+            for (int i = 0; i < gn; ++i) {
+                const int c_lo = __shfl_sync(0xffffffffu, wl.c_lo, i);
+                const int g = g0 + i;
+                if (lane == 0) {
+                    const int s = g % kTcStages;
+                    if (g >= kTcStages) mbar_wait(&empty[s], (uint32_t)((g / kTcStages) - 1) & 1u);
+                    uint8_t* st = smem + s * stage_bytes;
+                    mbar_arrive_expect_tx(&full[s], 2 * bbytes);
+                    const int ka = 2 * (a.a0 + g - a.ws_a0);
+                    tma_load_3d(st, &map, &full[s], 8 * c_lo, zr0 / 8, ka);
+                    tma_load_3d(st + bbytes, &map, &full[s], 8 * c_lo, zr0 / 8, ka + 1);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && n_ang > 0) {
+            // D f32, A/B f16, A K-major, B MN-major, N = 128, M = 128
+            constexpr uint32_t idesc = (1u << 4) | (1u << 16) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+            const uint32_t base = smem_u32(smem);
+            for (int g = 0; g < n_ang; ++g) {
+                const int s = g % kTcStages;
+                const uint32_t ph = (uint32_t)(g / kTcStages) & 1u;
+                const int blk = g / kTcP, b = blk & 1;
+                const bool first = (g % kTcP) == 0;
+                if (first && blk >= 2) mbar_wait(&accfree[b], (uint32_t)((blk / 2) - 1) & 1u);
+                mbar_wait(&full[s], ph);
+                mbar_wait(&afull[s], ph);
+                tc_fence_after();
+                const uint32_t bh = base + s * stage_bytes, bl = bh + bbytes, ah = bh + 2 * bbytes, al = ah + abytes;
+                const uint32_t td = tmem + (uint32_t)(b * kTcN);
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    // A: LBO = 128 voxels x 16 B between 8-channel chunks, SBO = 128 B between 8-voxel groups
+                    // B: LBO = 128 B between 8-channel chunks, SBO = 32 ch x 16 B between 8-row groups
+                    const uint64_t dah = umma_sdesc(ah + ks * 4096, kTcM * 16, 128);
+                    const uint64_t dal = umma_sdesc(al + ks * 4096, kTcM * 16, 128);
+                    const uint64_t dbh = umma_sdesc(bh + ks * 256, 128, kTcK * 16);
+                    const uint64_t dbl = umma_sdesc(bl + ks * 256, 128, kTcK * 16);
+                    umma_f16(td, dah, dbh, idesc, (first && ks == 0) ? 0u : 1u);
+                    umma_f16(td, dal, dbh, idesc, 1u);
+                    umma_f16(td, dah, dbl, idesc, 1u);
+                }
+                umma_commit(&empty[s]);
+                if (g % kTcP == kTcP - 1 || g == n_ang - 1) umma_commit(&accfull[b]);
+            }
+        }
+    } else {
+        // ---- weight producers (one voxel per thread; TMEM lane quadrant = warp % 4) + RN flush + epilogue
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const int vx = m % kTcTX, vy = m / kTcTX;
+        const float fdx = (float)vx, fdy = (float)vy;
+        const uint32_t rowoff = (uint32_t)((m % 8) * 16 + (m / 8) * 128);
+        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);  // this warp's TMEM lanes
+        auto flush = [&](int blk) {  // master (+)= acc[blk & 1], round to nearest
+            const int b = blk & 1;
+            mbar_wait(&accfull[b], (uint32_t)(blk / 2) & 1u);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < kTcN; c += 32) {
+                uint32_t v[32], u[32];
+                TC_LD32(tl + (uint32_t)(b * kTcN + c), v);
+                if (blk > 0) TC_LD32(tl + (uint32_t)(2 * kTcN + c), u);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (blk > 0) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__fadd_rn(__uint_as_float(u[j]), __uint_as_float(v[j])));
+                }
+                TC_ST32(tl + (uint32_t)(2 * kTcN + c), v);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&accfree[b]);
+        };
+        for (int g0 = 0; g0 < n_ang; g0 += 32) {
+            const TcWin wl = tc_window_lane(g0, n_ang, dX, dY, a);
+            const int gn = min(32, n_ang - g0);
+            for (int i = 0; i < gn; ++i) {
+                const int g = g0 + i;
+                const TcWin w = tc_bcast(wl, i);
+                const int s = g % kTcStages;
+                if (g >= kTcStages) mbar_wait(&empty[s], (uint32_t)((g / kTcStages) - 1) & 1u);
+                const float t = fmaxf(fmaf(fdy, w.C, fmaf(fdx, w.B, w.F0)), 0.f);
+                const float fl = floorf(t);
+                const float f = t - fl;
+                const float g0w = 1.f - f;
+                const int o = (int)fl;
+                const __half h0 = __float2half_rn(g0w), h1 = __float2half_rn(f);
+                const __half l0 = __float2half_rn(g0w - __half2float(h0)), l1 = __float2half_rn(f - __half2float(h1));
+                const __half z = __ushort_as_half(0);
+                const bool odd = o & 1;
+                const int jo = o >> 1;
+                const uint32_t Xh = odd ? pack_h2(z, h0) : pack_h2(h0, h1), Yh = odd ? pack_h2(h1, z) : 0u;
+                const uint32_t Xl = odd ? pack_h2(z, l0) : pack_h2(l0, l1), Yl = odd ? pack_h2(l1, z) : 0u;
+                uint8_t* ah = smem + s * stage_bytes + 2 * bbytes;
+                uint8_t* al = ah + abytes;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t vh[4], vl[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int j = 4 * c + k;
+                        vh[k] = j == jo ? Xh : (j == jo + 1 ? Yh : 0u);
+                        vl[k] = j == jo ? Xl : (j == jo + 1 ? Yl : 0u);
+                    }
+                    *reinterpret_cast<uint4*>(ah + rowoff + c * (kTcM * 16)) = make_uint4(vh[0], vh[1], vh[2], vh[3]);
+                    *reinterpret_cast<uint4*>(al + rowoff + c * (kTcM * 16)) = make_uint4(vl[0], vl[1], vl[2], vl[3]);
+                }
+                fence_proxy_async();  // generic-proxy stores -> visible to the tensor core (async proxy)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&afull[s]);
+                // the block before the one just started is complete once its last MMAs retire
+                if (g % kTcP == 0 && g >= kTcP) flush(g / kTcP - 1);
+            }
+        }
+        // ---- epilogue: master + last block -> volume
+        const int x = X0 + vx, y = Y0 + vy;
+        const bool inside = x >= ux0 && x < ux1 && y >= uy0 && y < uy1;
+        const bool fin = (a.flags & TF_BP_FINALIZE) != 0, accum = (a.flags & TF_BP_ACCUMULATE) != 0;
+        const bool zero = fin && tc_outside_fov(x, y, a);
+        const float sc = n_ang > 0 ? ldexpf(1.f, -*a.d_exp) : 0.f;
+        const int lb = n_blk - 1;
+        if (n_ang > 0) mbar_wait(&accfull[lb & 1], (uint32_t)(lb / 2) & 1u);
+        tc_fence_after();
+        float* out = a.vol + (size_t)y * a.nx + x;
+        for (int c = 0; c < kTcN; c += 32) {
+            uint32_t v[32], u[32];
+            TC_LD32(tl + (uint32_t)((lb & 1) * kTcN + c), v);
+            TC_LD32(tl + (uint32_t)(2 * kTcN + c), u);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (inside) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int zz = zr0 + c + j;
+                    if (zz < a.n_rows) {
+                        float sum = lb > 0 ? __fadd_rn(__uint_as_float(u[j]), __uint_as_float(v[j])) : __uint_as_float(v[j]);
+                        float val = n_ang > 0 ? sum * sc : 0.f;
+                        float* p = out + (size_t)zz * plane;
+                        if (accum) val += *p;
+                        if (fin) val = zero ? 0.f : val * a.angle_wf;
+                        *p = val;
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+// |T| max over the staged taps (non-negative floats order as their bit patterns)
+__global__ void tc_absmax_kernel(const float* __restrict__ st, long long n, unsigned* __restrict__ out) {
+    float mx = 0.f;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const float v = fabsf(st[i]);
+        if (v <= 3.0e38f) mx = fmaxf(mx, v);  // skip inf/nan
+    }
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(out, __float_as_uint(mx));
+}
+
+// z-blocked fp32 staging [k][zb][c][36] -> fp16 pairs [k][hi,lo][zb*4+g][c][8] scaled by 2^e
+__global__ void tc_convert_kernel(const float* __restrict__ st, __half* __restrict__ ws, const unsigned* __restrict__ hdr,
+                                  int* __restrict__ exp_out, long long n_items, int nzb, int n_chan, int a0) {
+    const float mx = __uint_as_float(hdr[0]);
+    const int e = mx > 0.f ? 14 - ilogbf(mx) : 0;  // max |T| * 2^e in [2^14, 2^15)
+    if (blockIdx.x == 0 && threadIdx.x == 0) *exp_out = e;
+    const float s = ldexpf(1.f, e);
+    const int R8 = nzb * 4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_items; i += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(i % n_chan);
+        long long r = i / n_chan;
+        const int g8 = (int)(r % R8);  // 8-row group
+        const long long k = r / R8;    // angle relative to a0
+        const int zb = g8 >> 2, g = g8 & 3;
+        const float* src = st + (((size_t)(a0 + k) * nzb + zb) * n_chan + c) * kZP + 8 * g;
+        const float4 u = *reinterpret_cast<const float4*>(src), v = *reinterpret_cast<const float4*>(src + 4);
+        const float x[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float p0 = x[2 * j] * s, p1 = x[2 * j + 1] * s;
+            const __half h0 = __float2half_rn(p0), h1 = __float2half_rn(p1);
+            const __half l0 = __float2half_rn(p0 - __half2float(h0)), l1 = __float2half_rn(p1 - __half2float(h1));
+            hw[j] = pack_h2(h0, h1);
+            lw[j] = pack_h2(l0, l1);
+        }
+        const size_t plane8 = (size_t)R8 * n_chan * 8;  // halves per split per angle
+        __half* dh = ws + (size_t)k * 2 * plane8 + ((size_t)g8 * n_chan + c) * 8;
+        *reinterpret_cast<uint4*>(dh) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(dh + plane8) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+}
+}  // namespace
+}  // namespace tf
+
+extern "C" int tf_bp_tc_supported(const tf_bp_plan* p) {
+    // a 16 x 8 tile's rays span <= sqrt(15^2 + 7^2) * scale + 2 taps; the window holds 32
+    return p && p->scale <= 1.5 ? 1 : 0;
+}
+
+extern "C" int64_t tf_bp_tc_workspace_bytes(const tf_bp_plan* p, int n_rows, int a0, int a1) {
+    if (!p || n_rows < 0 || a0 < 0 || a1 < a0) return -1;
+    const int64_t nzb = (n_rows + kZB - 1) / kZB;
+    return kTcHeader + (int64_t)(a1 - a0) * 2 * (nzb * 4) * p->g.n_chan * 8 * 2;
+}
+
+extern "C" int tf_bp_tc_prepare(const tf_bp_plan* p, const void* stage, int n_rows, int a0, int a1, void* ws,
+                                void* stream) {
+    if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null bp plan");
+    if (!tf_bp_tc_supported(p))
+        return set_error(TF_ERR_UNSUPPORTED, "tensor-core back-projection needs voxel/pixel pitch <= 1.5");
+    if (!(0 <= a0 && a0 <= a1 && a1 <= p->g.n_proj) || n_rows < 0)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "invalid rows/angles");
+    if (!stage || !ws) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    cudaStream_t s = as_stream(stream);
+    unsigned* hdr = static_cast<unsigned*>(ws);
+    TF_CUDA_TRY(cudaMemsetAsync(hdr, 0, kTcHeader, s));
+    if (n_rows == 0 || a0 == a1) return TF_OK;
+    const int nzb = (n_rows + kZB - 1) / kZB;
+    const long long per_angle = (long long)nzb * p->g.n_chan * kZP;
+    const float* st = static_cast<const float*>(stage);
+    tc_absmax_kernel<<<148 * 8, 256, 0, s>>>(st + (size_t)a0 * per_angle, (long long)(a1 - a0) * per_angle, hdr);
+    TF_CUDA_TRY(cudaGetLastError());
+    const long long items = (long long)(a1 - a0) * nzb * 4 * p->g.n_chan;
+    __half* data = reinterpret_cast<__half*>(static_cast<uint8_t*>(ws) + kTcHeader);
+    tc_convert_kernel<<<148 * 16, 256, 0, s>>>(st, data, hdr, reinterpret_cast<int*>(hdr + 1), items, nzb, p->g.n_chan,
+                                               a0);
+    return check_launch("tc_convert_kernel");
+}
+
+extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* ws, int ws_a0, int ws_a1, int n_rows, float* vol,
+                                 int a0, int a1, int x0, int x1, int y0, int y1, int flags, void* stream) {
+    if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null bp plan");
+    const tf_geometry& g = p->g;
+    if (!tf_bp_tc_supported(p))
+        return set_error(TF_ERR_UNSUPPORTED, "tensor-core back-projection needs voxel/pixel pitch <= 1.5");
+    if (!(ws_a0 <= a0 && a0 <= a1 && a1 <= ws_a1 && 0 <= ws_a0 && ws_a1 <= g.n_proj))
+        return set_error(TF_ERR_INVALID_ARGUMENT, "angle range (%d, %d) outside the prepared (%d, %d)", a0, a1, ws_a0,
+                         ws_a1);
+    if (!(0 <= x0 && x0 <= x1 && x1 <= g.nx && 0 <= y0 && y0 <= y1 && y1 <= g.ny))
+        return set_error(TF_ERR_INVALID_ARGUMENT, "tile (%d, %d, %d, %d) out of bounds", x0, x1, y0, y1);
+    if (n_rows < 0) return set_error(TF_ERR_INVALID_ARGUMENT, "n_rows must be >= 0");
+    if (n_rows == 0 || x0 == x1 || y0 == y1) return TF_OK;
+    if (!ws || !vol) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    if (a0 == a1 && !(flags & TF_BP_FINALIZE)) return TF_OK;
+    const int nzb = (n_rows + kZB - 1) / kZB;
+    const int R8 = nzb * 4;
+    const int N = kTcN;  // rows per CTA
+
+    PFN_encodeTiled_t enc = encode_fn();
+    if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    CUtensorMap map;
+    void* data = static_cast<uint8_t*>(const_cast<void*>(ws)) + kTcHeader;
+    // dim 0 = (channel, row-in-group) flattened: a box row is 32 channels x 8 rows = 512 contiguous
+    // bytes (one L2 request of 16 sectors, not 32 requests of 16 B); channel c_lo starts at element 8 c_lo
+    cuuint64_t dims[3] = {(cuuint64_t)8 * g.n_chan, (cuuint64_t)R8, (cuuint64_t)(2 * (ws_a1 - ws_a0))};
+    cuuint64_t strides[2] = {(cuuint64_t)g.n_chan * 16u, (cuuint64_t)R8 * g.n_chan * 16u};
+    cuuint32_t box[3] = {(cuuint32_t)(8 * kTcK), (cuuint32_t)(N / 8), 1u};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, data, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+
+    TCArgs a{};
+    a.trig = p->d_trig;
+    a.order = tile_order_enabled() ? p->d_order[kTcShape] : nullptr;
+    a.d_exp = reinterpret_cast<const int*>(static_cast<const uint8_t*>(ws) + 4);
+    a.vol = vol;
+    a.a0 = a0;
+    a.a1 = a1;
+    a.ws_a0 = ws_a0;
+    a.n_rows = n_rows;
+    a.nx = g.nx;
+    a.ny = g.ny;
+    a.n_chan = g.n_chan;
+    a.x0 = x0;
+    a.x1 = x1;
+    a.y0 = y0;
+    a.y1 = y1;
+    a.ntx = (g.nx + kTcTX - 1) / kTcTX;
+    a.N = N;
+    a.flags = flags;
+    a.cx = p->cx;
+    a.cy = p->cy;
+    a.scale = p->scale;
+    a.axis = p->axis;
+    a.R2 = p->R2;
+    a.sc2 = p->sc2;
+    a.angle_wf = p->angle_wf;
+    const int nty = (g.ny + kTcTY - 1) / kTcTY;
+    const int smem = kTcStages * (2 * N * kTcK * 2 + 2 * kTcM * kTcK * 2) + (3 * kTcStages + 5) * 8 + 16;
+    TF_CUDA_TRY(cudaFuncSetAttribute(bp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    dim3 grid((unsigned)(a.ntx * nty), (unsigned)((nzb * kZB + N - 1) / N));
+    bp_tc_kernel<<<grid, kTcThreads, smem, as_stream(stream)>>>(map, a);
+    return check_launch("bp_tc_kernel");
 }
