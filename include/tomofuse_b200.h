@@ -216,6 +216,9 @@ TF_API int tf_bp_kernel_info(const tf_bp_plan* plan, int flags, int n_rows, int 
  *    [ws_a0, ws_a1), flags as tf_backproject (TF_BP_ACCUMULATE/FINALIZE).
  * Requires voxel_pitch / pixel_pitch <= 1.5 (tf_bp_tc_supported). */
 TF_API int tf_bp_tc_supported(const tf_bp_plan* plan);
+/* development: per-CTA wait-cycle counters of the first 1024 tiles (8 int64
+ * each) into a device buffer; NULL turns the instrumentation off. */
+TF_API int tf_bp_tc_debug(void* dev_buf);
 TF_API int64_t tf_bp_tc_workspace_bytes(const tf_bp_plan* plan, int n_rows, int a0, int a1);
 TF_API int tf_bp_tc_prepare(const tf_bp_plan* plan, const void* stage, int n_rows, int a0, int a1, void* ws,
                             void* stream);

@@ -56,6 +56,7 @@ SIGNATURES = {
     "tf_bp_finalize": (_i, [_vp, _vp, _i, _vp]),
     "tf_bp_kernel_info": (_i, [_vp, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]),
     "tf_bp_tc_supported": (_i, [_vp]),
+    "tf_bp_tc_debug": (_i, [_vp]),
     "tf_bp_tc_workspace_bytes": (_i64, [_vp, _i, _i, _i]),
     "tf_bp_tc_prepare": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
     "tf_backproject_tc": (_i, [_vp, _vp, _i, _i, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp]),

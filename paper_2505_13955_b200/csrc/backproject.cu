@@ -1035,7 +1035,7 @@ extern "C" int tf_backproject_reduce(const tf_bp_plan* p, const void* stage, int
 // Roles per CTA (192 threads, one CTA per SM):
 //   warp 0  TMA producer: per angle the fp64 window origin (same operations as
 //           bp_kernel) and two TMA loads (T_hi, T_lo boxes of N rows x 32
-//           channels, MN-major canonical layout) into a 6-stage ring; the OOB
+//           channels, MN-major canonical layout) into a 10-stage ring; the OOB
 //           zero fill is the reference's zero guard for off-detector taps.
 //   warp 1  TMEM owner + MMA issuer (one thread): 6 tcgen05.mma per angle
 //           (2 K-steps x 3 split products) into one fp32 accumulator of N
@@ -1049,8 +1049,9 @@ namespace tf {
 namespace {
 constexpr int kTcTX = 16, kTcTY = 8, kTcM = kTcTX * kTcTY;  // voxels per CTA = MMA M
 constexpr int kTcK = 32;                                     // channel window (2 MMA K-steps of 16)
-constexpr int kTcStages = 6;
-constexpr int kTcThreads = 192;
+constexpr int kTcSB = 10;  // tap (TMA) ring depth (smem)
+constexpr int kTcSA = 4;   // weight ring depth (TMEM columns [384, 512): 32 per stage)
+constexpr int kTcThreads = 192;  // w0 TMA, w1 MMA, w2-5 weights
 constexpr int kTcShape = 4;                                  // kTileShape[4] = {16, 8}
 constexpr int kTcHeader = 256;                               // workspace header: absmax bits, exponent
 
@@ -1064,6 +1065,7 @@ struct TCArgs {
     int ntx, N, flags;
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
+    long long* dbg;  // optional per-CTA wait-cycle counters (tools/tc_check.py --dbg)
 };
 
 __device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -1079,6 +1081,15 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t 
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
         "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+// A (the weights) from TMEM: lane m = voxel m, column c = fp16 pair (k = 2c, 2c + 1)
+__device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc)
         : "memory");
 }
 
@@ -1124,6 +1135,12 @@ __device__ __forceinline__ TcWin tc_window_lane(int g0, int n_ang, double dX, do
     const int g = min(g0 + lane, n_ang - 1);
     return tc_window(dX, dY, a.trig[a.a0 + g], a);
 }
+// windows of angles g0, g0 + 2, ..., g0 + 62 (one weight group's alternate angles), one per lane
+__device__ __forceinline__ TcWin tc_window_lane2(int g0, int n_ang, double dX, double dY, const TCArgs& a) {
+    const int lane = threadIdx.x & 31;
+    const int g = min(g0 + 2 * lane, n_ang - 1);
+    return tc_window(dX, dY, a.trig[a.a0 + g], a);
+}
 __device__ __forceinline__ TcWin tc_bcast(const TcWin& w, int src) {
     TcWin r;
     r.c_lo = __shfl_sync(0xffffffffu, w.c_lo, src);
@@ -1152,9 +1169,17 @@ __device__ __forceinline__ TcWin tc_bcast(const TcWin& w, int src) {
         "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])                                     \
         : "memory")
 
+#define TC_ST16(ta, v)                                                                                            \
+    asm volatile(                                                                                                 \
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
+        ::"r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),      \
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])            \
+        : "memory")
+
 // TMEM columns: two MMA accumulators (ping-pong per block of kTcP angles) and
 // the round-to-nearest master sum, N = 128 columns each.
 constexpr int kTcN = 128;  // rows per CTA (MMA N)
+constexpr int kTcAcol = 3 * kTcN;  // first TMEM column of the weight (A) ring
 constexpr int kTcP = 16;   // angles per accumulator block (the tensor core's fp32 accumulation truncates:
                            // its bias grows with the count, so blocks are re-added in RN fp32 by threads)
 
@@ -1192,21 +1217,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
     }
 
     constexpr uint32_t bbytes = kTcN * kTcK * 2;   // one split of the tap box
-    constexpr uint32_t abytes = kTcM * kTcK * 2;   // one split of the weight tile
-    constexpr uint32_t stage_bytes = 2 * bbytes + 2 * abytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * stage_bytes);
-    uint64_t* afull = full + kTcStages;
-    uint64_t* empty = afull + kTcStages;
-    uint64_t* accfull = empty + kTcStages;  // [2]: MMA block done -> flush
+    uint8_t* const bring = smem;                              // [kTcSB][hi, lo] tap boxes
+    uint64_t* full = reinterpret_cast<uint64_t*>(bring + kTcSB * 2 * bbytes);
+    uint64_t* empty = full + kTcSB;
+    uint64_t* afull = empty + kTcSB;
+    uint64_t* accfull = afull + kTcSA;  // [2]: MMA block done -> flush
     uint64_t* accfree = accfull + 2;        // [2]: flushed -> MMA may overwrite
     uint64_t* done = accfree + 2;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+    int* kring = reinterpret_cast<int*>(tslot + 1);  // [kTcSB]: MMA K-steps of the angle in tap slot s
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kTcStages; ++s) {
+        for (int s = 0; s < kTcSB; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&afull[s], 4);
             mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < kTcSA; ++s) {
+            mbar_init(&afull[s], 4);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&accfull[b], 1);
@@ -1231,16 +1258,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
     if (warp == 0) {
         // ---- TMA producer: windows for 32 angles per batch, one per lane
         if (lane == 0) tma_prefetch_desc(&map);
+        long long w_bempty = 0;
         for (int g0 = 0; g0 < n_ang; g0 += 32) {
             const TcWin wl = tc_window_lane(g0, n_ang, dX, dY, a);
+            // one K-step suffices when every tap of the tile lies in the first 16 channels
+            // (t - c_lo < 15 with a margin for the fp32 t of the weights; the skipped
+            // weights are exact zeros)
+            const float span = wl.F0 + fmaxf(0.f, wl.B * (kTcTX - 1)) + fmaxf(0.f, wl.C * (kTcTY - 1));
+            const int ksl = span < 14.9f ? 1 : 2;
             const int gn = min(32, n_ang - g0);
             for (int i = 0; i < gn; ++i) {
                 const int c_lo = __shfl_sync(0xffffffffu, wl.c_lo, i);
+                const int nks = __shfl_sync(0xffffffffu, ksl, i);
                 const int g = g0 + i;
                 if (lane == 0) {
-                    const int s = g % kTcStages;
-                    if (g >= kTcStages) mbar_wait(&empty[s], (uint32_t)((g / kTcStages) - 1) & 1u);
-                    uint8_t* st = smem + s * stage_bytes;
+                    const int s = g % kTcSB;
+                    const long long e0 = clock64();
+                    if (g >= kTcSB) mbar_wait(&empty[s], (uint32_t)((g / kTcSB) - 1) & 1u);
+                    w_bempty += clock64() - e0;
+                    uint8_t* st = bring + s * 2 * bbytes;
+                    kring[s] = nks;
                     mbar_arrive_expect_tx(&full[s], 2 * bbytes);
                     const int ka = 2 * (a.a0 + g - a.ws_a0);
                     tma_load_3d(st, &map, &full[s], 8 * c_lo, zr0 / 8, ka);
@@ -1249,45 +1286,59 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 __syncwarp();
             }
         }
+        if (a.dbg && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) a.dbg[blockIdx.x * 8 + 6] = w_bempty;
     } else if (warp == 1) {
         if (lane == 0 && n_ang > 0) {
             // D f32, A/B f16, A K-major, B MN-major, N = 128, M = 128
             constexpr uint32_t idesc = (1u << 4) | (1u << 16) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
             const uint32_t base = smem_u32(smem);
+            long long w_full = 0, w_afull = 0;
+            const long long t_start = clock64();
             for (int g = 0; g < n_ang; ++g) {
-                const int s = g % kTcStages;
-                const uint32_t ph = (uint32_t)(g / kTcStages) & 1u;
+                const int sb = g % kTcSB, sa = g % kTcSA;
                 const int blk = g / kTcP, b = blk & 1;
                 const bool first = (g % kTcP) == 0;
                 if (first && blk >= 2) mbar_wait(&accfree[b], (uint32_t)((blk / 2) - 1) & 1u);
-                mbar_wait(&full[s], ph);
-                mbar_wait(&afull[s], ph);
+                const long long c0 = clock64();
+                mbar_wait(&full[sb], (uint32_t)(g / kTcSB) & 1u);
+                const long long c1 = clock64();
+                mbar_wait(&afull[sa], (uint32_t)(g / kTcSA) & 1u);
+                const long long c2 = clock64();
+                w_full += c1 - c0;
+                w_afull += c2 - c1;
                 tc_fence_after();
-                const uint32_t bh = base + s * stage_bytes, bl = bh + bbytes, ah = bh + 2 * bbytes, al = ah + abytes;
+                const uint32_t bh = base + sb * 2 * bbytes, bl = bh + bbytes;
+                const uint32_t ah = tmem + (uint32_t)(kTcAcol + sa * 32), al = ah + 16;  // TMEM weight tiles
                 const uint32_t td = tmem + (uint32_t)(b * kTcN);
+                const int nks = kring[sb];
 #pragma unroll
                 for (int ks = 0; ks < 2; ++ks) {
+                    if (ks >= nks) break;
                     // A: LBO = 128 voxels x 16 B between 8-channel chunks, SBO = 128 B between 8-voxel groups
                     // B: LBO = 128 B between 8-channel chunks, SBO = 32 ch x 16 B between 8-row groups
-                    const uint64_t dah = umma_sdesc(ah + ks * 4096, kTcM * 16, 128);
-                    const uint64_t dal = umma_sdesc(al + ks * 4096, kTcM * 16, 128);
                     const uint64_t dbh = umma_sdesc(bh + ks * 256, 128, kTcK * 16);
                     const uint64_t dbl = umma_sdesc(bl + ks * 256, 128, kTcK * 16);
-                    umma_f16(td, dah, dbh, idesc, (first && ks == 0) ? 0u : 1u);
-                    umma_f16(td, dal, dbh, idesc, 1u);
-                    umma_f16(td, dah, dbl, idesc, 1u);
+                    umma_f16_ts(td, ah + ks * 8, dbh, idesc, (first && ks == 0) ? 0u : 1u);
+                    umma_f16_ts(td, al + ks * 8, dbh, idesc, 1u);
+                    umma_f16_ts(td, ah + ks * 8, dbl, idesc, 1u);
                 }
-                umma_commit(&empty[s]);
+                umma_commit(&empty[sb]);  // frees tap slot sb and weight slot sa (one commit per angle)
                 if (g % kTcP == kTcP - 1 || g == n_ang - 1) umma_commit(&accfull[b]);
+            }
+            if (a.dbg && blockIdx.y == 0 && blockIdx.x < 1024) {
+                a.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
+                a.dbg[blockIdx.x * 8 + 1] = w_full;
+                a.dbg[blockIdx.x * 8 + 2] = w_afull;
             }
         }
     } else {
-        // ---- weight producers (one voxel per thread; TMEM lane quadrant = warp % 4) + RN flush + epilogue
+        // ---- weight producers: two groups of 4 warps take alternate angles (one voxel per
+        // thread; TMEM lane quadrant = warp % 4); group 0 also does the RN flush and the epilogue
+        const int grp = 0;
         const int q = warp & 3;
         const int m = q * 32 + lane;
         const int vx = m % kTcTX, vy = m / kTcTX;
         const float fdx = (float)vx, fdy = (float)vy;
-        const uint32_t rowoff = (uint32_t)((m % 8) * 16 + (m / 8) * 128);
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);  // this warp's TMEM lanes
         auto flush = [&](int blk) {  // master (+)= acc[blk & 1], round to nearest
             const int b = blk & 1;
@@ -1310,14 +1361,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
             __syncwarp();
             if (lane == 0) mbar_arrive(&accfree[b]);
         };
+        int flushed = 0;
+        long long w_aempty = 0, w_flush = 0;
+        const long long t_w0 = clock64();
         for (int g0 = 0; g0 < n_ang; g0 += 32) {
             const TcWin wl = tc_window_lane(g0, n_ang, dX, dY, a);
-            const int gn = min(32, n_ang - g0);
-            for (int i = 0; i < gn; ++i) {
+            for (int i = 0; i < 32; ++i) {
                 const int g = g0 + i;
+                if (g >= n_ang) break;
                 const TcWin w = tc_bcast(wl, i);
-                const int s = g % kTcStages;
-                if (g >= kTcStages) mbar_wait(&empty[s], (uint32_t)((g / kTcStages) - 1) & 1u);
+                const int s = g % kTcSA;
+                const long long e0 = clock64();
+                // weight slot s was last used by angle g - kTcSA: wait for its MMAs (the tap
+                // ring's empty barrier of that angle; the MMA thread commits one per angle)
+                if (g >= kTcSA) mbar_wait(&empty[(g - kTcSA) % kTcSB], (uint32_t)((g - kTcSA) / kTcSB) & 1u);
+                w_aempty += clock64() - e0;
                 const float t = fmaxf(fmaf(fdy, w.C, fmaf(fdx, w.B, w.F0)), 0.f);
                 const float fl = floorf(t);
                 const float f = t - fl;
@@ -1330,27 +1388,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 const int jo = o >> 1;
                 const uint32_t Xh = odd ? pack_h2(z, h0) : pack_h2(h0, h1), Yh = odd ? pack_h2(h1, z) : 0u;
                 const uint32_t Xl = odd ? pack_h2(z, l0) : pack_h2(l0, l1), Yl = odd ? pack_h2(l1, z) : 0u;
-                uint8_t* ah = smem + s * stage_bytes + 2 * bbytes;
-                uint8_t* al = ah + abytes;
+                uint32_t vh[16], vl[16];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t vh[4], vl[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int j = 4 * c + k;
-                        vh[k] = j == jo ? Xh : (j == jo + 1 ? Yh : 0u);
-                        vl[k] = j == jo ? Xl : (j == jo + 1 ? Yl : 0u);
-                    }
-                    *reinterpret_cast<uint4*>(ah + rowoff + c * (kTcM * 16)) = make_uint4(vh[0], vh[1], vh[2], vh[3]);
-                    *reinterpret_cast<uint4*>(al + rowoff + c * (kTcM * 16)) = make_uint4(vl[0], vl[1], vl[2], vl[3]);
+                for (int j = 0; j < 16; ++j) {
+                    vh[j] = j == jo ? Xh : (j == jo + 1 ? Yh : 0u);
+                    vl[j] = j == jo ? Xl : (j == jo + 1 ? Yl : 0u);
                 }
-                fence_proxy_async();  // generic-proxy stores -> visible to the tensor core (async proxy)
+                const uint32_t ta = tl + (uint32_t)(kTcAcol + s * 32);  // this voxel's row of the TMEM A tile
+                TC_ST16(ta, vh);
+                TC_ST16(ta + 16, vl);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&afull[s]);
-                // the block before the one just started is complete once its last MMAs retire
-                if (g % kTcP == 0 && g >= kTcP) flush(g / kTcP - 1);
+                // flush block j once angle (j+1)P + kTcSA is being produced: its aempty-wait
+                // above proved the MMAs through angle (j+1)P retired, so the accfull wait is
+                // immediate (flushing at (j+1)P instead drained the whole MMA pipeline)
+                if (grp == 0 && g % kTcP == kTcSA && g >= kTcP) {
+                    const long long f0 = clock64();
+                    flush(flushed++);
+                    w_flush += clock64() - f0;
+                }
             }
         }
+        if (a.dbg && warp == 2 && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) {
+            a.dbg[blockIdx.x * 8 + 3] = clock64() - t_w0;
+            a.dbg[blockIdx.x * 8 + 4] = w_aempty;
+            a.dbg[blockIdx.x * 8 + 5] = w_flush;
+        }
+        if (grp == 0) {
+        while (flushed < n_blk - 1) flush(flushed++);  // short last block
         // ---- epilogue: master + last block -> volume
         const int x = X0 + vx, y = Y0 + vy;
         const bool inside = x >= ux0 && x < ux1 && y >= uy0 && y < uy1;
@@ -1381,6 +1448,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 }
             }
         }
+        }  // grp == 0
     }
     tc_fence_before();
     __syncthreads();
@@ -1432,6 +1500,18 @@ __global__ void tc_convert_kernel(const float* __restrict__ st, __half* __restri
 }
 }  // namespace
 }  // namespace tf
+
+namespace tf {
+namespace {
+long long* g_tc_dbg = nullptr;  // development instrumentation (tf_bp_tc_debug), off by default
+long long* tc_debug_buffer() { return g_tc_dbg; }
+}  // namespace
+}  // namespace tf
+
+extern "C" int tf_bp_tc_debug(void* buf) {
+    g_tc_dbg = static_cast<long long*>(buf);
+    return TF_OK;
+}
 
 extern "C" int tf_bp_tc_supported(const tf_bp_plan* p) {
     // a 16 x 8 tile's rays span <= sqrt(15^2 + 7^2) * scale + 2 taps; the window holds 32
@@ -1528,8 +1608,9 @@ extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* ws, int ws_a0,
     a.R2 = p->R2;
     a.sc2 = p->sc2;
     a.angle_wf = p->angle_wf;
+    a.dbg = tc_debug_buffer();
     const int nty = (g.ny + kTcTY - 1) / kTcTY;
-    const int smem = kTcStages * (2 * N * kTcK * 2 + 2 * kTcM * kTcK * 2) + (3 * kTcStages + 5) * 8 + 16;
+    const int smem = kTcSB * 2 * N * kTcK * 2 + (2 * kTcSB + kTcSA + 5) * 8 + 8 + 4 * kTcSB;
     TF_CUDA_TRY(cudaFuncSetAttribute(bp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)((nzb * kZB + N - 1) / N));
     bp_tc_kernel<<<grid, kTcThreads, smem, as_stream(stream)>>>(map, a);

@@ -10,7 +10,10 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
-constexpr int M = 128, N = 256, KS = 2, K = 16 * KS;
+#ifndef PN
+#define PN 256
+#endif
+constexpr int M = 128, N = PN, KS = 2, K = 16 * KS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -46,22 +49,30 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t da, uint64_t db, u
 }
 
 __global__ void __launch_bounds__(128, 1) k_probe(const __half* A, const __half* B, float* D, long long* clk, int reps) {
-    __shared__ __align__(1024) uint8_t sa[M * K * 2];
-    __shared__ __align__(1024) uint8_t sb[N * K * 2];
+#ifndef NBUF
+#define NBUF 1
+#endif
+    extern __shared__ __align__(1024) uint8_t dyn[];  // NBUF distinct copies of A and B
+    uint8_t* sa = dyn;
+    uint8_t* sb = dyn + NBUF * M * K * 2;
     __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t bar2[4];
     __shared__ uint32_t tbase;
     const int tid = threadIdx.x, warp = tid >> 5;
-    for (int i = tid; i < M * K; i += 128) {
-        int m = i / K, k = i % K;
-        *reinterpret_cast<__half*>(sa + a_off(m, k)) = A[i];
-    }
-    for (int i = tid; i < N * K; i += 128) {
-        int k = i / N, n = i % N;
-        *reinterpret_cast<__half*>(sb + b_off(n, k)) = B[i];
+    for (int c = 0; c < NBUF; ++c) {
+        for (int i = tid; i < M * K; i += 128) {
+            int m = i / K, k = i % K;
+            *reinterpret_cast<__half*>(sa + c * M * K * 2 + a_off(m, k)) = A[i];
+        }
+        for (int i = tid; i < N * K; i += 128) {
+            int k = i / N, n = i % N;
+            *reinterpret_cast<__half*>(sb + c * N * K * 2 + b_off(n, k)) = B[i];
+        }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        for (int c = 0; c < 4; ++c) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar2[c])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -75,11 +86,17 @@ __global__ void __launch_bounds__(128, 1) k_probe(const __half* A, const __half*
     const uint32_t td = tbase;
     if (tid == 0) {
         long long t0 = clock64();
-        for (int r = 0; r < reps; ++r)
+        for (int r = 0; r < reps; ++r) {
 #pragma unroll
             for (int s = 0; s < KS; ++s)
-                mma(td, sdesc(smem_u32(sa) + s * 2 * A_LBO, A_LBO, A_SBO), sdesc(smem_u32(sb) + s * 256, B_LBO, B_SBO),
-                    (r | s) ? 1u : 0u);
+                mma(td, sdesc(smem_u32(sa) + (r % NBUF) * M * K * 2 + s * 2 * A_LBO, A_LBO, A_SBO),
+                    sdesc(smem_u32(sb) + (r % NBUF) * N * K * 2 + s * 256, B_LBO, B_SBO), (r | s) ? 1u : 0u);
+#ifdef PCOMMIT  // a commit per KS-step group (as the back-projection kernel does per angle)
+            for (int c = 0; c < PCOMMIT; ++c)
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    smem_u32(&bar2[c])));
+#endif
+        }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(&bar)));
         // wait for completion (phase 0)
@@ -138,7 +155,9 @@ int main() {
     cudaMemcpy(dB, hB, K * N * 2, cudaMemcpyHostToDevice);
     for (int reps : {1, 3, 4096}) {
         cudaMemset(dD, 0, M * N * 4);
-        k_probe<<<1, 128>>>(dA, dB, dD, dclk, reps);
+        const int dsm = NBUF * (M + N) * K * 2;
+        cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
+        k_probe<<<1, 128, dsm>>>(dA, dB, dD, dclk, reps);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e)); return 1; }
         float* hD = new float[M * N];

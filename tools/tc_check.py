@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--rows", type=int, default=64)
     ap.add_argument("--oracle-rows", type=int, default=2)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--dbg", action="store_true", help="print the kernel's per-role wait-cycle counters")
     a = ap.parse_args()
     n, k = a.n, a.rows
     p = AcquisitionParams(n_proj=a.n_proj, n_rows=n, n_chan=n, pixel_pitch=12.0)
@@ -54,9 +55,19 @@ def main():
         check(L.tf_backproject_tc(h, ctypes.c_void_p(ws.data_ptr()), 0, a.n_proj, k, ctypes.c_void_p(vol.data_ptr()),
                                   0, a.n_proj, 0, n, 0, n, _lib.TF_BP_FINALIZE, st))
 
+    dbg = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")
+    if a.dbg:
+        check(L.tf_bp_tc_debug(ctypes.c_void_p(dbg.data_ptr())))
     prep()
     bp()
     torch.cuda.synchronize()
+    check(L.tf_bp_tc_debug(None))
+    if a.dbg:
+        d8 = dbg.view(1024, 8).cpu().numpy().astype(np.float64)
+        d8 = d8[d8[:, 0] > 0]
+        names = ["mma_total", "mma_wait_full", "mma_wait_afull", "w_total", "w_wait_aempty", "w_flush", "tma_wait_empty"]
+        print(json.dumps({"dbg_ctas": len(d8), **{nm: round(float(d8[:, i].mean()) / a.n_proj, 1)
+                                                 for i, nm in enumerate(names)}, "unit": "clk per angle"}))
     e = int(torch.tensor(ws[4:8].cpu().numpy().view(np.int32))[0])
     diff = (vol - ref).double()
     rel = float(diff.norm() / ref.double().norm())
