@@ -1093,6 +1093,14 @@ __device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, ui
         : "memory");
 }
 
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -1258,7 +1266,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
     if (warp == 0) {
         // ---- TMA producer: windows for 32 angles per batch, one per lane
         if (lane == 0) tma_prefetch_desc(&map);
-        long long w_bempty = 0;
         for (int g0 = 0; g0 < n_ang; g0 += 32) {
             const TcWin wl = tc_window_lane(g0, n_ang, dX, dY, a);
             // one K-step suffices when every tap of the tile lies in the first 16 channels
@@ -1273,9 +1280,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 const int g = g0 + i;
                 if (lane == 0) {
                     const int s = g % kTcSB;
-                    const long long e0 = clock64();
                     if (g >= kTcSB) mbar_wait(&empty[s], (uint32_t)((g / kTcSB) - 1) & 1u);
-                    w_bempty += clock64() - e0;
                     uint8_t* st = bring + s * 2 * bbytes;
                     kring[s] = nks;
                     mbar_arrive_expect_tx(&full[s], 2 * bbytes);
@@ -1286,50 +1291,43 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 __syncwarp();
             }
         }
-        if (a.dbg && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) a.dbg[blockIdx.x * 8 + 6] = w_bempty;
     } else if (warp == 1) {
-        if (lane == 0 && n_ang > 0) {
-            // D f32, A/B f16, A K-major, B MN-major, N = 128, M = 128
+        // ---- MMA issue: the whole warp runs the loop (waits are warp-uniform) and one elected
+        // lane issues, so the tcgen05 ops are not wrapped in per-thread issue loops
+        if (n_ang > 0) {
+            // D f32, A/B f16, A K-major (TMEM), B MN-major, N = 128, M = 128
             constexpr uint32_t idesc = (1u << 4) | (1u << 16) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
-            const uint32_t base = smem_u32(smem);
-            long long w_full = 0, w_afull = 0;
-            const long long t_start = clock64();
+            // B: LBO = 128 B between 8-channel chunks, SBO = 32 ch x 16 B between 8-row groups; the
+            // start-address field (bits 0-13, addr >> 4) is advanced by adding offsets >> 4
+            const uint64_t db0 = umma_sdesc(smem_u32(smem), 128, kTcK * 16);
+            long long t_start = a.dbg ? clock64() : 0;
             for (int g = 0; g < n_ang; ++g) {
                 const int sb = g % kTcSB, sa = g % kTcSA;
                 const int blk = g / kTcP, b = blk & 1;
                 const bool first = (g % kTcP) == 0;
                 if (first && blk >= 2) mbar_wait(&accfree[b], (uint32_t)((blk / 2) - 1) & 1u);
-                const long long c0 = clock64();
                 mbar_wait(&full[sb], (uint32_t)(g / kTcSB) & 1u);
-                const long long c1 = clock64();
                 mbar_wait(&afull[sa], (uint32_t)(g / kTcSA) & 1u);
-                const long long c2 = clock64();
-                w_full += c1 - c0;
-                w_afull += c2 - c1;
                 tc_fence_after();
-                const uint32_t bh = base + sb * 2 * bbytes, bl = bh + bbytes;
-                const uint32_t ah = tmem + (uint32_t)(kTcAcol + sa * 32), al = ah + 16;  // TMEM weight tiles
-                const uint32_t td = tmem + (uint32_t)(b * kTcN);
                 const int nks = kring[sb];
-#pragma unroll
-                for (int ks = 0; ks < 2; ++ks) {
-                    if (ks >= nks) break;
-                    // A: LBO = 128 voxels x 16 B between 8-channel chunks, SBO = 128 B between 8-voxel groups
-                    // B: LBO = 128 B between 8-channel chunks, SBO = 32 ch x 16 B between 8-row groups
-                    const uint64_t dbh = umma_sdesc(bh + ks * 256, 128, kTcK * 16);
-                    const uint64_t dbl = umma_sdesc(bl + ks * 256, 128, kTcK * 16);
-                    umma_f16_ts(td, ah + ks * 8, dbh, idesc, (first && ks == 0) ? 0u : 1u);
-                    umma_f16_ts(td, al + ks * 8, dbh, idesc, 1u);
-                    umma_f16_ts(td, ah + ks * 8, dbl, idesc, 1u);
+                if (elect_one()) {
+                    const uint64_t dbh = db0 + (uint64_t)((sb * 2 * bbytes) >> 4), dbl = dbh + (bbytes >> 4);
+                    const uint32_t ah = tmem + (uint32_t)(kTcAcol + sa * 32), al = ah + 16;  // TMEM weight tiles
+                    const uint32_t td = tmem + (uint32_t)(b * kTcN);
+                    umma_f16_ts(td, ah, dbh, idesc, first ? 0u : 1u);
+                    umma_f16_ts(td, al, dbh, idesc, 1u);
+                    umma_f16_ts(td, ah, dbl, idesc, 1u);
+                    if (nks > 1) {  // channels 16..31: +16 ch x 16 B = 256 B
+                        umma_f16_ts(td, ah + 8, dbh + 16, idesc, 1u);
+                        umma_f16_ts(td, al + 8, dbh + 16, idesc, 1u);
+                        umma_f16_ts(td, ah + 8, dbl + 16, idesc, 1u);
+                    }
+                    umma_commit(&empty[sb]);  // frees tap slot sb and weight slot sa (one commit per angle)
+                    if (g % kTcP == kTcP - 1 || g == n_ang - 1) umma_commit(&accfull[b]);
                 }
-                umma_commit(&empty[sb]);  // frees tap slot sb and weight slot sa (one commit per angle)
-                if (g % kTcP == kTcP - 1 || g == n_ang - 1) umma_commit(&accfull[b]);
+                __syncwarp();
             }
-            if (a.dbg && blockIdx.y == 0 && blockIdx.x < 1024) {
-                a.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
-                a.dbg[blockIdx.x * 8 + 1] = w_full;
-                a.dbg[blockIdx.x * 8 + 2] = w_afull;
-            }
+            if (a.dbg && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) a.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
         }
     } else {
         // ---- weight producers: two groups of 4 warps take alternate angles (one voxel per
@@ -1362,8 +1360,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
             if (lane == 0) mbar_arrive(&accfree[b]);
         };
         int flushed = 0;
-        long long w_aempty = 0, w_flush = 0;
-        const long long t_w0 = clock64();
+        const long long t_w0 = a.dbg ? clock64() : 0;
         for (int g0 = 0; g0 < n_ang; g0 += 32) {
             const TcWin wl = tc_window_lane(g0, n_ang, dX, dY, a);
             for (int i = 0; i < 32; ++i) {
@@ -1371,11 +1368,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 if (g >= n_ang) break;
                 const TcWin w = tc_bcast(wl, i);
                 const int s = g % kTcSA;
-                const long long e0 = clock64();
                 // weight slot s was last used by angle g - kTcSA: wait for its MMAs (the tap
                 // ring's empty barrier of that angle; the MMA thread commits one per angle)
                 if (g >= kTcSA) mbar_wait(&empty[(g - kTcSA) % kTcSB], (uint32_t)((g - kTcSA) / kTcSB) & 1u);
-                w_aempty += clock64() - e0;
                 const float t = fmaxf(fmaf(fdy, w.C, fmaf(fdx, w.B, w.F0)), 0.f);
                 const float fl = floorf(t);
                 const float f = t - fl;
@@ -1404,17 +1399,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 // flush block j once angle (j+1)P + kTcSA is being produced: its aempty-wait
                 // above proved the MMAs through angle (j+1)P retired, so the accfull wait is
                 // immediate (flushing at (j+1)P instead drained the whole MMA pipeline)
-                if (grp == 0 && g % kTcP == kTcSA && g >= kTcP) {
-                    const long long f0 = clock64();
-                    flush(flushed++);
-                    w_flush += clock64() - f0;
-                }
+                if (grp == 0 && g % kTcP == kTcSA && g >= kTcP) flush(flushed++);
             }
         }
         if (a.dbg && warp == 2 && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) {
             a.dbg[blockIdx.x * 8 + 3] = clock64() - t_w0;
-            a.dbg[blockIdx.x * 8 + 4] = w_aempty;
-            a.dbg[blockIdx.x * 8 + 5] = w_flush;
         }
         if (grp == 0) {
         while (flushed < n_blk - 1) flush(flushed++);  // short last block

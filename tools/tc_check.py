@@ -65,9 +65,9 @@ def main():
     if a.dbg:
         d8 = dbg.view(1024, 8).cpu().numpy().astype(np.float64)
         d8 = d8[d8[:, 0] > 0]
-        names = ["mma_total", "mma_wait_full", "mma_wait_afull", "w_total", "w_wait_aempty", "w_flush", "tma_wait_empty"]
+        names = ["mma_total", "", "", "w_total"]
         print(json.dumps({"dbg_ctas": len(d8), **{nm: round(float(d8[:, i].mean()) / a.n_proj, 1)
-                                                 for i, nm in enumerate(names)}, "unit": "clk per angle"}))
+                                                 for i, nm in enumerate(names) if nm}, "unit": "clk per angle"}))
     e = int(torch.tensor(ws[4:8].cpu().numpy().view(np.int32))[0])
     diff = (vol - ref).double()
     rel = float(diff.norm() / ref.double().norm())
