@@ -1051,7 +1051,7 @@ constexpr int kTcTX = 16, kTcTY = 8, kTcM = kTcTX * kTcTY;  // voxels per CTA = 
 constexpr int kTcK = 32;                                     // channel window (2 MMA K-steps of 16)
 constexpr int kTcSB = 10;  // tap (TMA) ring depth (smem)
 constexpr int kTcSA = 4;   // weight ring depth (TMEM columns [384, 512): 32 per stage)
-constexpr int kTcThreads = 192;  // w0 TMA, w1 MMA, w2-5 weights
+constexpr int kTcThreads = 320;  // w0 TMA, w1 MMA, w2-5 / w6-9 weight groups (even / odd angles)
 constexpr int kTcShape = 4;                                  // kTileShape[4] = {16, 8}
 constexpr int kTcHeader = 256;                               // workspace header: absmax bits, exponent
 
@@ -1332,7 +1332,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
     } else {
         // ---- weight producers: two groups of 4 warps take alternate angles (one voxel per
         // thread; TMEM lane quadrant = warp % 4); group 0 also does the RN flush and the epilogue
-        const int grp = 0;
+        const int grp = (warp - 2) >> 2;  // kTcSA is even: group 0 owns the even weight slots
         const int q = warp & 3;
         const int m = q * 32 + lane;
         const int vx = m % kTcTX, vy = m / kTcTX;
@@ -1361,10 +1361,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
         };
         int flushed = 0;
         const long long t_w0 = a.dbg ? clock64() : 0;
-        for (int g0 = 0; g0 < n_ang; g0 += 32) {
-            const TcWin wl = tc_window_lane(g0, n_ang, dX, dY, a);
+        for (int g0 = grp; g0 < n_ang; g0 += 64) {
+            const TcWin wl = tc_window_lane2(g0, n_ang, dX, dY, a);
             for (int i = 0; i < 32; ++i) {
-                const int g = g0 + i;
+                const int g = g0 + 2 * i;
                 if (g >= n_ang) break;
                 const TcWin w = tc_bcast(wl, i);
                 const int s = g % kTcSA;
