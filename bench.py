@@ -18,6 +18,7 @@ every timed step).  Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -443,8 +444,9 @@ def main():
             eng.filter(raw)
             eng.exchange()
             eng.stage()
+            eng.prepare_bp()  # tensor-core K2: fp16 hi/lo taps, scale from the all-reduced max |T|
             bp_ev[0].record()
-            eng.local.backproject()
+            eng.local.backproject(prepared=True)
             bp_ev[1].record()
     else:
         eng = slab = SlabReconstructor(p, d, i0=I0, device=dev)
@@ -454,8 +456,10 @@ def main():
 
         def step_parts():
             eng.filter_stage(raw)  # K1 fused: Beer-Lambert + ramp + feather -> z-blocked staging
+            if eng.tensor:
+                eng.prepare_tc()  # fp16 hi/lo taps for the tensor-core K2
             bp_ev[0].record()
-            eng.backproject()
+            eng.backproject(prepared=True)
             bp_ev[1].record()
 
     torch.cuda.synchronize()
@@ -476,12 +480,21 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    tensor = bool(getattr(slab, "tensor", False)) and not angle_split
+    if tensor:  # count the MMA K-steps K2 issues in the timed steps (its FLOPs)
+        from paper_2505_13955_b200._lib import lib as _tl
+
+        kcount = torch.zeros(1, dtype=torch.int64, device=dev)
+        _tl().tf_bp_tc_count(ctypes.c_void_p(kcount.data_ptr()))
     for e in evs:
         bp_ev = [e[1], e[2]]
         e[0].record()
         step_parts()
         e[3].record()
     torch.cuda.synchronize()
+    if tensor:
+        _tl().tf_bp_tc_count(None)
+        ksteps_per_launch = kcount.item() / args.steps
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -498,8 +511,6 @@ def main():
     exec_upd, active_tiles = executed_updates(d, n_proj, k_rows)
     sm_mhz = clk.get("sm_mhz") or 1965.0
     smem_peak = SMEM_BYTES_PER_CLK * SM_COUNT * sm_mhz * 1e6 / 1e9  # GB/s
-    import ctypes
-
     from paper_2505_13955_b200._lib import TF_BP_FINALIZE, lib as _tf_lib
 
     bpu, exe = ctypes.c_double(), ctypes.c_int64()
@@ -566,7 +577,11 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = te.item()
         if world == 1 and rank == 0:  # the host-fed volume must equal the device-resident one
-            same = bool(torch.equal(h_vol[n // 2], slab.vol[n // 2].cpu()))
+            a_, b_ = h_vol[n // 2], slab.vol[n // 2].cpu()
+            if getattr(slab, "tensor", False):  # sub-slabs pick their own fp16 tap scale: fp32 roundoff
+                same = bool(float((a_ - b_).norm() / b_.norm()) < 1e-6)
+            else:
+                same = bool(torch.equal(a_, b_))
         else:
             same = None
         e2e = {"value": round(total_updates / (e2e_ms / 1e3) / 1e9, 3), "unit": "GUPS",
@@ -616,6 +631,36 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return
+    tc_roof = None
+    if tensor:
+        # tensor-core K2: per angle and CTA (128 voxels x 128 rows) 3 fp16 MMAs of 128 x 128 x 16
+        # per K-step (T_hi W_hi + T_hi W_lo + T_lo W_hi), 1 or 2 K-steps by the tile's window
+        flops = ksteps_per_launch * 3 * 2 * 128 * 128 * 16
+        tflops = flops / (bp_avg_ms / 1e3) / 1e12
+        pk = peaks.get("bf16_tflops_sustained") or 1420.9
+        tc_roof = {
+            "bound": "tensor",
+            "kernel": "bp_tc_kernel (K2, tcgen05)",
+            "achieved": round(tflops, 1),
+            "peak": pk,
+            "unit": "TFLOP/s",
+            "frac": round(tflops / pk, 4),
+            "frac_of_burst": round(tflops / (peaks.get("bf16_tflops") or 1684.4), 4),
+            "traffic": None,
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (dense fp16 MMA runs at the bf16 rate; "
+                           "K2 is a 1-2 s kernel inside the step)",
+            "flops_per_launch": flops,
+            "flops_note": "executed MMA FLOPs of the GEMM formulation D[voxel][row] += W[voxel][chan] T[chan][row]: "
+                          "K-steps counted on the device (tf_bp_tc_count) x 3 split products x 2*128*128*16",
+            "mma_ksteps_per_launch": ksteps_per_launch,
+            "bp_ms_per_launch": round(bp_avg_ms, 3),
+            "bp_gups_full_count": round(slab_updates / (bp_avg_ms / 1e3) / 1e9, 1),
+            # per angle and CTA: TMA writes 2 x 128 rows x 32 ch x 2 B = 16 KB, the MMAs read B 3x per
+            # K-step (2 x 12 KB); weights come from TMEM: (16 + 24) KB / 16384 updates
+            "smem_bytes_per_update": 2.5,
+            "hbm_gbs_algorithmic": round(hbm_alg / (bp_avg_ms / 1e3) / 1e9, 1),
+            "hbm_peak_measured": peaks.get("hbm_gbs"),
+        }
     line = {
         "metric": METRIC,
         "value": round(gups, 3),
@@ -641,7 +686,7 @@ def main():
                             "(NVLink peer memory, or + NCCL reduce-scatter) -> FoV/scale finalize"
                             if angle_split else
                             EXCHANGE_STEP.get(args.exchange if world > 1 else "", EXCHANGE_STEP[""]))},
-        "roofline": {
+        "roofline": tc_roof if tensor else {
             "bound": "smem",
             "kernel": "bp_kernel (K2)",
             "achieved": round(smem_achieved, 1),
@@ -669,8 +714,9 @@ def main():
         },
         "clocks": clk,
         # our kernels per step: K1 + K2, + tf_bp_stage (allgather, p2p) or + tf_bp_finalize (angle split)
-        "gpu_launches": (3 if (world > 1 and (args.exchange in ("allgather", "p2p") or angle_split)) else 2)
-        * args.steps,
+        # (+1 with the tensor-core K2: tc_convert_kernel; its scale comes from tap_bound, no absmax pass)
+        "gpu_launches": ((3 if (world > 1 and (args.exchange in ("allgather", "p2p") or angle_split)) else 2)
+                         + (1 if tensor else 0)) * args.steps,
     }
     if e2e is not None:
         line["e2e"] = e2e

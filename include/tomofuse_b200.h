@@ -210,18 +210,26 @@ TF_API int tf_bp_kernel_info(const tf_bp_plan* plan, int flags, int n_rows, int 
  * order); within the fp32 tolerance of the reference float64 output.
  * 1. tf_bp_tc_prepare converts angles [a0, a1) of a z-blocked staging buffer
  *    (tf_filter_stage / tf_bp_stage output for n_rows rows) into `ws`
- *    (tf_bp_tc_workspace_bytes): fp16 hi/lo taps scaled by a device-chosen
- *    power of two, stream-ordered, no host sync.
+ *    (tf_bp_tc_workspace_bytes): fp16 hi/lo taps scaled by 2^e with
+ *    max|T| 2^e < 2^15.  t_bound == 0 takes max|T| from the data on the
+ *    device (no host sync); t_bound > 0 is a caller bound on |T|; t_bound < 0
+ *    uses the max already in ws (tf_bp_tc_absmax, possibly all-reduced over
+ *    the ranks of a z-slab split so every rank uses the same scale).
  * 2. tf_backproject_tc back-projects angles [a0, a1) within the prepared
  *    [ws_a0, ws_a1), flags as tf_backproject (TF_BP_ACCUMULATE/FINALIZE).
  * Requires voxel_pitch / pixel_pitch <= 1.5 (tf_bp_tc_supported). */
 TF_API int tf_bp_tc_supported(const tf_bp_plan* plan);
+/* Adds the MMA K-steps of every later tf_backproject_tc launch to the device
+ * uint64 `counter` (each K-step = 3 MMAs of 128 x 128 x 16); NULL: off. */
+TF_API int tf_bp_tc_count(void* dev_counter);
 /* development: per-CTA wait-cycle counters of the first 1024 tiles (8 int64
  * each) into a device buffer; NULL turns the instrumentation off. */
 TF_API int tf_bp_tc_debug(void* dev_buf);
 TF_API int64_t tf_bp_tc_workspace_bytes(const tf_bp_plan* plan, int n_rows, int a0, int a1);
-TF_API int tf_bp_tc_prepare(const tf_bp_plan* plan, const void* stage, int n_rows, int a0, int a1, void* ws,
-                            void* stream);
+TF_API int tf_bp_tc_prepare(const tf_bp_plan* plan, const void* stage, int n_rows, int a0, int a1, double t_bound,
+                            void* ws, void* stream);
+TF_API int tf_bp_tc_absmax(const tf_bp_plan* plan, const void* stage, int n_rows, int a0, int a1, void* ws,
+                           void* stream);
 TF_API int tf_backproject_tc(const tf_bp_plan* plan, const void* ws, int ws_a0, int ws_a1, int n_rows, float* vol,
                              int a0, int a1, int x0, int x1, int y0, int y1, int flags, void* stream);
 

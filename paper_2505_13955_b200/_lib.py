@@ -58,7 +58,9 @@ SIGNATURES = {
     "tf_bp_tc_supported": (_i, [_vp]),
     "tf_bp_tc_debug": (_i, [_vp]),
     "tf_bp_tc_workspace_bytes": (_i64, [_vp, _i, _i, _i]),
-    "tf_bp_tc_prepare": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
+    "tf_bp_tc_prepare": (_i, [_vp, _vp, _i, _i, _i, _d, _vp, _vp]),
+    "tf_bp_tc_count": (_i, [_vp]),
+    "tf_bp_tc_absmax": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
     "tf_backproject_tc": (_i, [_vp, _vp, _i, _i, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp]),
     "tf_quantize": (_i, [_vp, _i, _vp, _i64, _d, _d, _vp]),
     "tf_phantom_sinogram": (_i, [_pg, _i, _i, _i, _i, _d, _d, _vp, _vp]),

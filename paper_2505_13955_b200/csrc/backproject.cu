@@ -1065,7 +1065,8 @@ struct TCArgs {
     int ntx, N, flags;
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
-    long long* dbg;  // optional per-CTA wait-cycle counters (tools/tc_check.py --dbg)
+    long long* dbg;                // optional per-CTA cycle counters (tools/tc_check.py --dbg)
+    unsigned long long* kcount;    // optional: total MMA K-steps issued (the roofline's FLOP count)
 };
 
 __device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -1301,6 +1302,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
             // start-address field (bits 0-13, addr >> 4) is advanced by adding offsets >> 4
             const uint64_t db0 = umma_sdesc(smem_u32(smem), 128, kTcK * 16);
             long long t_start = a.dbg ? clock64() : 0;
+            int ksum = 0;
             for (int g = 0; g < n_ang; ++g) {
                 const int sb = g % kTcSB, sa = g % kTcSA;
                 const int blk = g / kTcP, b = blk & 1;
@@ -1310,6 +1312,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 mbar_wait(&afull[sa], (uint32_t)(g / kTcSA) & 1u);
                 tc_fence_after();
                 const int nks = kring[sb];
+                ksum += nks;
                 if (elect_one()) {
                     const uint64_t dbh = db0 + (uint64_t)((sb * 2 * bbytes) >> 4), dbl = dbh + (bbytes >> 4);
                     const uint32_t ah = tmem + (uint32_t)(kTcAcol + sa * 32), al = ah + 16;  // TMEM weight tiles
@@ -1328,6 +1331,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 __syncwarp();
             }
             if (a.dbg && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) a.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
+            if (a.kcount && lane == 0) atomicAdd(a.kcount, (unsigned long long)ksum);
         }
     } else {
         // ---- weight producers: two groups of 4 warps take alternate angles (one voxel per
@@ -1444,12 +1448,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
 
-// |T| max over the staged taps (non-negative floats order as their bit patterns)
-__global__ void tc_absmax_kernel(const float* __restrict__ st, long long n, unsigned* __restrict__ out) {
+// |T| max over the staged taps (non-negative floats order as their bit patterns).  Only the
+// n_rows real rows count: the 4 pad floats of each 36-float channel row and the rows past
+// n_rows of a ragged last z-block are never written by K1 (uninitialised memory).
+__global__ void tc_absmax_kernel(const float* __restrict__ st, long long n_items, int nzb, int n_chan, int n_rows,
+                                 unsigned* __restrict__ out) {
     float mx = 0.f;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const float v = fabsf(st[i]);
-        if (v <= 3.0e38f) mx = fmaxf(mx, v);  // skip inf/nan
+    // item = (angle, z-block, channel, 4-row group): one float4
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_items;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int g = (int)(i & 7);
+        const long long row = i >> 3;  // (angle * nzb + zb) * n_chan + c
+        const int zb = (int)((row / n_chan) % nzb);
+        const int z0 = zb * kZB + 4 * g;
+        if (z0 >= n_rows) continue;
+        const float4 v = *reinterpret_cast<const float4*>(st + row * kZP + 4 * g);
+        const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float a = fabsf(e[j]);
+            if (z0 + j < n_rows && a <= 3.0e38f) mx = fmaxf(mx, a);  // skip inf/nan
+        }
     }
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(out, __float_as_uint(mx));
@@ -1457,8 +1476,9 @@ __global__ void tc_absmax_kernel(const float* __restrict__ st, long long n, unsi
 
 // z-blocked fp32 staging [k][zb][c][36] -> fp16 pairs [k][hi,lo][zb*4+g][c][8] scaled by 2^e
 __global__ void tc_convert_kernel(const float* __restrict__ st, __half* __restrict__ ws, const unsigned* __restrict__ hdr,
-                                  int* __restrict__ exp_out, long long n_items, int nzb, int n_chan, int a0) {
-    const float mx = __uint_as_float(hdr[0]);
+                                  int* __restrict__ exp_out, long long n_items, int nzb, int n_chan, int a0,
+                                  float bound) {
+    const float mx = bound > 0.f ? bound : __uint_as_float(hdr[0]);
     const int e = mx > 0.f ? 14 - ilogbf(mx) : 0;  // max |T| * 2^e in [2^14, 2^15)
     if (blockIdx.x == 0 && threadIdx.x == 0) *exp_out = e;
     const float s = ldexpf(1.f, e);
@@ -1494,11 +1514,17 @@ namespace tf {
 namespace {
 long long* g_tc_dbg = nullptr;  // development instrumentation (tf_bp_tc_debug), off by default
 long long* tc_debug_buffer() { return g_tc_dbg; }
+unsigned long long* g_tc_count = nullptr;  // MMA K-step counter (tf_bp_tc_count), off by default
 }  // namespace
 }  // namespace tf
 
 extern "C" int tf_bp_tc_debug(void* buf) {
     g_tc_dbg = static_cast<long long*>(buf);
+    return TF_OK;
+}
+
+extern "C" int tf_bp_tc_count(void* counter) {
+    g_tc_count = static_cast<unsigned long long*>(counter);
     return TF_OK;
 }
 
@@ -1513,11 +1539,38 @@ extern "C" int64_t tf_bp_tc_workspace_bytes(const tf_bp_plan* p, int n_rows, int
     return kTcHeader + (int64_t)(a1 - a0) * 2 * (nzb * 4) * p->g.n_chan * 8 * 2;
 }
 
-extern "C" int tf_bp_tc_prepare(const tf_bp_plan* p, const void* stage, int n_rows, int a0, int a1, void* ws,
-                                void* stream) {
+extern "C" int tf_bp_tc_prepare(const tf_bp_plan* p, const void* stage, int n_rows, int a0, int a1, double t_bound,
+                                void* ws, void* stream) {
     if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null bp plan");
     if (!tf_bp_tc_supported(p))
         return set_error(TF_ERR_UNSUPPORTED, "tensor-core back-projection needs voxel/pixel pitch <= 1.5");
+    if (!(0 <= a0 && a0 <= a1 && a1 <= p->g.n_proj) || n_rows < 0)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "invalid rows/angles");
+    if (!stage || !ws) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    cudaStream_t s = as_stream(stream);
+    unsigned* hdr = static_cast<unsigned*>(ws);
+    // t_bound < 0: hdr[0] already holds the max |T| bits (tf_bp_tc_absmax, e.g. all-reduced over ranks)
+    if (t_bound >= 0) TF_CUDA_TRY(cudaMemsetAsync(hdr, 0, kTcHeader, s));
+    if (n_rows == 0 || a0 == a1) return TF_OK;
+    const int nzb = (n_rows + kZB - 1) / kZB;
+    const long long per_angle = (long long)nzb * p->g.n_chan * kZP;
+    const float* st = static_cast<const float*>(stage);
+    if (t_bound == 0) {  // t_bound > 0: the caller's bound on |T| fixes the scale
+        tc_absmax_kernel<<<148 * 8, 256, 0, s>>>(st + (size_t)a0 * per_angle,
+                                                 (long long)(a1 - a0) * nzb * p->g.n_chan * 8, nzb, p->g.n_chan,
+                                                 n_rows, hdr);
+        TF_CUDA_TRY(cudaGetLastError());
+    }
+    const long long items = (long long)(a1 - a0) * nzb * 4 * p->g.n_chan;
+    __half* data = reinterpret_cast<__half*>(static_cast<uint8_t*>(ws) + kTcHeader);
+    tc_convert_kernel<<<148 * 16, 256, 0, s>>>(st, data, hdr, reinterpret_cast<int*>(hdr + 1), items, nzb, p->g.n_chan,
+                                               a0, t_bound > 0 ? (float)t_bound : 0.f);
+    return check_launch("tc_convert_kernel");
+}
+
+extern "C" int tf_bp_tc_absmax(const tf_bp_plan* p, const void* stage, int n_rows, int a0, int a1, void* ws,
+                               void* stream) {
+    if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null bp plan");
     if (!(0 <= a0 && a0 <= a1 && a1 <= p->g.n_proj) || n_rows < 0)
         return set_error(TF_ERR_INVALID_ARGUMENT, "invalid rows/angles");
     if (!stage || !ws) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
@@ -1527,14 +1580,10 @@ extern "C" int tf_bp_tc_prepare(const tf_bp_plan* p, const void* stage, int n_ro
     if (n_rows == 0 || a0 == a1) return TF_OK;
     const int nzb = (n_rows + kZB - 1) / kZB;
     const long long per_angle = (long long)nzb * p->g.n_chan * kZP;
-    const float* st = static_cast<const float*>(stage);
-    tc_absmax_kernel<<<148 * 8, 256, 0, s>>>(st + (size_t)a0 * per_angle, (long long)(a1 - a0) * per_angle, hdr);
-    TF_CUDA_TRY(cudaGetLastError());
-    const long long items = (long long)(a1 - a0) * nzb * 4 * p->g.n_chan;
-    __half* data = reinterpret_cast<__half*>(static_cast<uint8_t*>(ws) + kTcHeader);
-    tc_convert_kernel<<<148 * 16, 256, 0, s>>>(st, data, hdr, reinterpret_cast<int*>(hdr + 1), items, nzb, p->g.n_chan,
-                                               a0);
-    return check_launch("tc_convert_kernel");
+    tc_absmax_kernel<<<148 * 8, 256, 0, s>>>(static_cast<const float*>(stage) + (size_t)a0 * per_angle,
+                                             (long long)(a1 - a0) * nzb * p->g.n_chan * 8, nzb, p->g.n_chan, n_rows,
+                                             hdr);
+    return check_launch("tc_absmax_kernel");
 }
 
 extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* ws, int ws_a0, int ws_a1, int n_rows, float* vol,
@@ -1598,6 +1647,7 @@ extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* ws, int ws_a0,
     a.sc2 = p->sc2;
     a.angle_wf = p->angle_wf;
     a.dbg = tc_debug_buffer();
+    a.kcount = g_tc_count;
     const int nty = (g.ny + kTcTY - 1) / kTcTY;
     const int smem = kTcSB * 2 * N * kTcK * 2 + (2 * kTcSB + kTcSA + 5) * 8 + 8 + 4 * kTcSB;
     TF_CUDA_TRY(cudaFuncSetAttribute(bp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -227,7 +227,19 @@ class ZSlabReconstructor:
         self.filter(raw_chunk)
         self.exchange()
         self.stage()
-        return self.local.backproject()
+        self.prepare_bp()
+        return self.local.backproject(prepared=True)
+
+    def prepare_bp(self):
+        """Tensor-core K2: every rank scales its fp16 taps by the same 2^e, from
+        max |T| all-reduced over the group (one int32), so the z-slab volume is
+        bitwise the 1-GPU volume's rows."""
+        if self.local.tensor:
+            import torch.distributed as dist
+
+            m = self.local.tc_absmax()
+            dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
+            self.local.prepare_tc(use_max=True)
 
     def updates(self) -> int:
         return self.local.updates()

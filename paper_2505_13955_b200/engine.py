@@ -19,6 +19,7 @@ timed (and CUDA-graph captured) without allocator noise.
 from __future__ import annotations
 
 import ctypes
+import os
 
 from . import _lib
 from ._lib import check, lib
@@ -30,10 +31,15 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def tensor_default() -> bool:
+    """K2 on the tensor cores (tf_backproject_tc) unless TF_BP_TENSOR=0."""
+    return os.environ.get("TF_BP_TENSOR", "1") != "0"
+
+
 class SlabReconstructor:
     def __init__(self, params: AcquisitionParams, dims: VolumeDims, spec: FilterSpec | None = None,
                  i0: float = 1e5, feather_band: int = 32, rows: tuple[int, int] | None = None,
-                 device=None, in_place_filter: bool = False, stage=None):
+                 device=None, in_place_filter: bool = False, stage=None, tensor: bool | None = None):
         import torch
 
         self.torch = torch
@@ -58,6 +64,16 @@ class SlabReconstructor:
                 self.stage = torch.empty(need, dtype=torch.uint8, device=self.device)
             self.vol = torch.empty((self.k, dims.ny, dims.nx), dtype=torch.float32,
                                    device=self.device)
+            # K2 variant: tensor cores (fp16 hi/lo split GEMMs per angle, tf_backproject_tc)
+            # or the CUDA-core x-pair gather (tf_backproject)
+            sup = bool(lib().tf_bp_tc_supported(self.bplan.handle))
+            if tensor and not sup:
+                raise ValueError("tensor-core back-projection needs voxel_pitch / pixel_pitch <= 1.5")
+            self.tensor = sup and (tensor_default() if tensor is None else bool(tensor))
+            self.tc_ws = None
+            if self.tensor:
+                nb = lib().tf_bp_tc_workspace_bytes(self.bplan.handle, self.k, 0, params.n_proj)
+                self.tc_ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
 
     @property
     def filt(self):
@@ -83,19 +99,50 @@ class SlabReconstructor:
         """Fused K1: raw counts (n_proj, k, n_chan) -> Beer-Lambert -> ramp
         filter -> feather -> z-blocked staging buffer (no filtered copy)."""
         n_lines = raw.numel() // self.params.n_chan
+        i0 = self.i0 if i0 is None else float(i0)
         check(lib().tf_filter_stage(self.fplan.handle, self.bplan.handle, _ptr(raw), _ptr(self.stage), n_lines,
-                                    self.i0 if i0 is None else float(i0), self.k, 0, None, None,
-                                    self._s(stream)))
+                                    i0, self.k, 0, None, None, self._s(stream)))
 
     def stage_rows(self, filt, rows_per_angle=None, r0=0, stream=None):
         rpa = rows_per_angle if rows_per_angle is not None else self.k
         check(lib().tf_bp_stage(self.bplan.handle, _ptr(filt), rpa, r0, r0 + self.k, _ptr(self.stage),
                                 self._s(stream)))
 
-    def backproject(self, a0=0, a1=None, flags=_lib.TF_BP_FINALIZE, stream=None, vol=None):
+    def tc_absmax(self, a0=0, a1=None, stream=None):
+        """Tensor path: max |T| of the staged taps into the workspace header and
+        return it as a 1-element int32 device view (float bits; non-negative
+        floats order like ints, so an NCCL MAX all-reduce of it is the global
+        max).  The next prepare_tc(use_max=True) scales by it."""
+        a1 = self.params.n_proj if a1 is None else a1
+        check(lib().tf_bp_tc_absmax(self.bplan.handle, _ptr(self.stage), self.k, a0, a1, _ptr(self.tc_ws),
+                                    self._s(stream)))
+        return self.tc_ws[:4].view(self.torch.int32)
+
+    def prepare_tc(self, a0=0, a1=None, stream=None, n_rows=None, use_max=False):
+        """Tensor path only: staged taps of angles [a0, a1) -> fp16 hi/lo
+        workspace, scaled by 2^e from the data's max |T| (or, with use_max,
+        the max tc_absmax left in the workspace)."""
+        a1 = self.params.n_proj if a1 is None else a1
+        k = self.k if n_rows is None else n_rows
+        check(lib().tf_bp_tc_prepare(self.bplan.handle, _ptr(self.stage), k, a0, a1, -1.0 if use_max else 0.0,
+                                     _ptr(self.tc_ws), self._s(stream)))
+        self._prepared = (a0, a1, k)
+
+    def backproject(self, a0=0, a1=None, flags=_lib.TF_BP_FINALIZE, stream=None, vol=None, n_rows=None,
+                    prepared=False):
+        """K2 over angles [a0, a1) of the staged rows (n_rows, default the slab's).
+        On the tensor path it first converts the staged taps (prepare_tc)
+        unless `prepared` says that was just done for the same range."""
         a1 = self.params.n_proj if a1 is None else a1
         vol = self.vol if vol is None else vol
-        check(lib().tf_backproject(self.bplan.handle, _ptr(self.stage), self.k, _ptr(vol), a0, a1,
+        k = self.k if n_rows is None else n_rows
+        if self.tensor and not flags & _lib.TF_BP_KERNEL_V1:  # V1 forces the CUDA-core 2-tap kernel
+            if not prepared or getattr(self, "_prepared", None) != (a0, a1, k):
+                self.prepare_tc(a0, a1, stream, k)
+            check(lib().tf_backproject_tc(self.bplan.handle, _ptr(self.tc_ws), a0, a1, k, _ptr(vol), a0, a1,
+                                          0, self.dims.nx, 0, self.dims.ny, flags, self._s(stream)))
+            return vol
+        check(lib().tf_backproject(self.bplan.handle, _ptr(self.stage), k, _ptr(vol), a0, a1,
                                    0, self.dims.nx, 0, self.dims.ny, flags, self._s(stream)))
         return vol
 
@@ -160,7 +207,8 @@ class StreamedReconstructor:
     """
 
     def __init__(self, params: AcquisitionParams, dims: VolumeDims, spec: FilterSpec | None = None,
-                 i0: float = 1e5, feather_band: int = 32, slab_rows: int = 256, device=None):
+                 i0: float = 1e5, feather_band: int = 32, slab_rows: int = 256, device=None,
+                 tensor: bool | None = None):
         import torch
 
         self.torch = torch
@@ -170,7 +218,7 @@ class StreamedReconstructor:
         k = self.slab_rows
         with torch.cuda.device(self.device):
             self.eng = SlabReconstructor(params, dims, spec, i0, feather_band, rows=(0, k),
-                                         device=self.device)
+                                         device=self.device, tensor=tensor)
             shape = (params.n_proj, k, params.n_chan)
             self.raw = [torch.empty(shape, dtype=torch.float32, device=self.device) for _ in range(2)]
             self.vol = [self.eng.vol, torch.empty_like(self.eng.vol)]
@@ -262,9 +310,7 @@ class StreamedReconstructor:
             raw_free[b] = ev
             if vol_free[b] is not None:
                 self.s_comp.wait_event(vol_free[b])
-            check(lib().tf_backproject(self.eng.bplan.handle, _ptr(self.eng.stage), k, _ptr(self.vol[b]), 0,
-                                       p.n_proj, 0, d.nx, 0, d.ny, _lib.TF_BP_FINALIZE,
-                                       ctypes.c_void_p(self.s_comp.cuda_stream)))
+            self.eng.backproject(stream=self.s_comp, vol=self.vol[b], n_rows=k)
             src_vol = self.vol[b]
             if quantize is not None:  # fbp.quantize on the device (K3)
                 lo, hi = quantize

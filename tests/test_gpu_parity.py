@@ -313,7 +313,7 @@ def test_accumulate_chaining_is_bitwise(F):
     p = AcquisitionParams(n_proj=n_proj, n_rows=40, n_chan=n)
     d = VolumeDims(n, n, 40)
     raw = _phantom_rows(p, d, 0, 40)
-    eng = SlabReconstructor(p, d, i0=1e5)
+    eng = SlabReconstructor(p, d, i0=1e5, tensor=False)  # the CUDA-core kernel's property
     one = eng.run(raw).clone()
     vol2 = torch.zeros_like(one)
     cuts = [0, 7, 50, 51, 100]
@@ -332,14 +332,14 @@ def test_row_slabs_are_bitwise(F):
     p = AcquisitionParams(n_proj=90, n_rows=70, n_chan=n)
     d = VolumeDims(n, n, 70)
     raw = _phantom_rows(p, d, 0, 70)
-    full = SlabReconstructor(p, d, i0=1e5).run(raw).cpu()
+    full = SlabReconstructor(p, d, i0=1e5, tensor=False).run(raw).cpu()  # tensor path: its own test
     # K1 filters two lines per complex FFT, so bitwise identity needs slab
     # boundaries that keep the (even, odd) row pairing -- z-slabs are
     # multiples of 32 rows in practice; odd splits agree to fp32 roundoff
     for r0, r1 in [(0, 32), (32, 70), (6, 8)]:
-        part = SlabReconstructor(p, d, i0=1e5, rows=(r0, r1)).run(raw[:, r0:r1].contiguous()).cpu()
+        part = SlabReconstructor(p, d, i0=1e5, rows=(r0, r1), tensor=False).run(raw[:, r0:r1].contiguous()).cpu()
         assert (part == full[r0:r1]).all()
-    part = SlabReconstructor(p, d, i0=1e5, rows=(5, 6)).run(raw[:, 5:6].contiguous()).cpu()
+    part = SlabReconstructor(p, d, i0=1e5, rows=(5, 6), tensor=False).run(raw[:, 5:6].contiguous()).cpu()
     assert rel_l2(part.numpy(), full[5:6].numpy()) < 1e-6
 
 
@@ -366,7 +366,7 @@ def test_block_kernel_bitwise_equals_two_tap_kernel(F, case):
     else:
         p = AcquisitionParams(n_proj=90, n_rows=64, n_chan=128)
         d = VolumeDims(128, 128, 64)
-    eng = SlabReconstructor(p, d, i0=1e5)
+    eng = SlabReconstructor(p, d, i0=1e5, tensor=False)  # CUDA-core variants
     raw = _phantom_rows(p, d, 0, p.n_rows)
     filt = eng.filter(raw)
     eng.stage_rows(filt)
@@ -378,7 +378,8 @@ def test_block_kernel_bitwise_equals_two_tap_kernel(F, case):
 
 def test_streamed_host_path_equals_device_path(F):
     """Pinned host in/out with 3-stream z-sub-slab pipelining == the
-    device-resident reconstruction, bit for bit (incl. a ragged last slab)."""
+    device-resident reconstruction, bit for bit (incl. a ragged last slab), on
+    the CUDA-core kernel (the tensor-core path: test_tensor_core_row_slabs_and_streaming)."""
     import torch
 
     from paper_2505_13955_b200.engine import SlabReconstructor, StreamedReconstructor
@@ -388,11 +389,11 @@ def test_streamed_host_path_equals_device_path(F):
     p = AcquisitionParams(n_proj=120, n_rows=rows, n_chan=n, pixel_pitch=12.0)
     d = VolumeDims(n, n, rows, voxel_pitch=12.0)
     raw = _phantom_rows(p, d, 0, rows)
-    ref = SlabReconstructor(p, d, i0=1e5).run(raw).cpu()
+    ref = SlabReconstructor(p, d, i0=1e5, tensor=False).run(raw).cpu()
     h_raw = torch.empty(raw.shape, dtype=torch.float32, pin_memory=True)
     h_raw.copy_(raw)
     h_vol = torch.zeros((rows, n, n), dtype=torch.float32, pin_memory=True)
-    st = StreamedReconstructor(p, d, i0=1e5, slab_rows=32)
+    st = StreamedReconstructor(p, d, i0=1e5, slab_rows=32, tensor=False)
     st.run(h_raw, h_vol)
     torch.cuda.synchronize()
     assert torch.equal(h_vol, ref)
@@ -530,7 +531,7 @@ def test_backproject_reduce_matches_single_pass(F, n_slabs, scale):
     n, n_proj, rows = 96, 150, 45
     p = AcquisitionParams(n_proj=n_proj, n_rows=rows, n_chan=n, pixel_pitch=12.0)
     d = VolumeDims(n, n, rows, voxel_pitch=12.0 * scale)
-    eng = SlabReconstructor(p, d, i0=1e5)
+    eng = SlabReconstructor(p, d, i0=1e5, tensor=False)  # the reduce epilogue is the CUDA-core kernel's
     raw = torch.empty((n_proj, rows, n), device="cuda")
     phantom_raw(p, d, raw)
     eng.filter_stage(raw)
@@ -764,3 +765,122 @@ def test_large_detector_parity_c4_c5(F, n, n_proj):
     err = rel_l2(got, ref)
     print(f"{n}^2 x {n_proj}, row {row}: rel_l2 {err:.2e} max_abs {np.abs(got - ref).max():.2e}")
     assert err <= REL_L2
+
+
+# ---- tensor-core K2 (tf_backproject_tc) ------------------------------------
+TC_CASES = {
+    "normal": (dict(n_proj=90, n_rows=64, n_chan=128), dict(nx=128, ny=128, nz=64)),
+    "offset": (dict(n_proj=64, n_rows=33, n_chan=80, angle_span=2 * math.pi, offset_chan=13), dict(nx=100, ny=96, nz=33)),
+    "pitch": (dict(n_proj=50, n_rows=32, n_chan=64, pixel_pitch=1.0), dict(nx=70, ny=70, nz=32, voxel_pitch=1.3)),
+    "ragged": (dict(n_proj=37, n_rows=45, n_chan=61), dict(nx=61, ny=53, nz=45)),
+    "rows300": (dict(n_proj=40, n_rows=300, n_chan=64), dict(nx=64, ny=64, nz=300)),
+}
+
+
+def _tc_case(case):
+    from paper_2505_13955_b200.geometry import AcquisitionParams, ScanMode, VolumeDims
+
+    pa, da = TC_CASES[case]
+    pa = dict(pa)
+    if "offset_chan" in pa:
+        pa["scan_mode"] = ScanMode.OFFSET
+    da = dict(da)
+    return AcquisitionParams(**pa), VolumeDims(da.pop("nx"), da.pop("ny"), da.pop("nz"), **da)
+
+
+@pytest.mark.parametrize("case", sorted(TC_CASES))
+def test_tensor_core_bp_matches_oracle(F, case):
+    """The tensor-core K2 (per-angle fp16 hi/lo split GEMMs, fp32 TMEM
+    accumulation flushed in RN fp32 every 16 angles) against the C oracle's
+    float64 reconstruction of the same raw rows: relative L2 <= 1e-5; and
+    against the CUDA-core kernel to fp32 roundoff (~1e-6)."""
+    import numpy as np
+
+    from oracle import c_oracle as C
+    from oracle import fbp_oracle as O
+    from paper_2505_13955_b200.engine import SlabReconstructor
+
+    p, d = _tc_case(case)
+    raw = _phantom_rows(p, d, 0, p.n_rows)
+    tc = SlabReconstructor(p, d, i0=1e5, tensor=True)
+    assert tc.tensor
+    got = tc.run(raw).cpu().numpy()
+    ref_cc = SlabReconstructor(p, d, i0=1e5, tensor=False).run(raw).cpu().numpy()
+    assert np.isfinite(got).all()
+    assert rel_l2(got, ref_cc) < 5e-6
+    yy, xx = np.meshgrid(np.arange(d.ny), np.arange(d.nx), indexing="ij")  # fbp.py:247-250 mask
+    half = (p.n_chan - 1) / 2.0
+    R = half + abs(p.offset_chan) if p.offset_chan else half
+    out = ((xx - (d.nx - 1) / 2.0) ** 2 + (yy - (d.ny - 1) / 2.0) ** 2) * (d.voxel_pitch / p.pixel_pitch) ** 2 > R * R
+    assert (got[:, out] == 0).all() and (ref_cc[:, out] == 0).all()
+    rows = sorted({0, p.n_rows // 2, p.n_rows - 1})
+    geom = O.make_geom(p.n_proj, len(rows), p.n_chan, nx=d.nx, ny=d.ny, span=p.angle_span,
+                       pixel_pitch=p.pixel_pitch, voxel_pitch=d.voxel_pitch, offset_chan=p.offset_chan)
+    oref = C.fbp_rows(raw[:, rows].cpu().numpy(), geom)
+    # pitch 1 um with the 3.5e-4 /um phantom gives depths ~1e-3, where K1's fp32 log alone is
+    # ~1e-5 off for BOTH kernels: the tensor path may add at most fp32 roundoff to that
+    err_tc, err_cc = rel_l2(got[rows], oref), rel_l2(ref_cc[rows], oref)
+    assert err_tc <= max(REL_L2, err_cc + 2e-6), (err_tc, err_cc)
+
+
+def test_tensor_core_row_slabs_and_streaming(F):
+    """Tensor-core path over z-slabs and host-streamed sub-slabs: with the
+    same fp16 scale (the full volume's max |T| handed in, as the multi-GPU
+    z-slab split does with an all-reduce) a row's result does not depend on
+    the slab or the 128-row MMA block it sits in -- bit for bit; with each
+    sub-slab's own scale (streaming) it agrees to fp32 roundoff."""
+    import torch
+
+    from paper_2505_13955_b200.engine import SlabReconstructor, StreamedReconstructor
+    from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
+
+    n = 64
+    p = AcquisitionParams(n_proj=90, n_rows=200, n_chan=n)
+    d = VolumeDims(n, n, 200)
+    raw = _phantom_rows(p, d, 0, 200)
+    fe = SlabReconstructor(p, d, i0=1e5, tensor=True)
+    full = fe.run(raw).cpu()
+    gmax = fe.tc_absmax().clone()
+    for r0, r1 in [(0, 32), (32, 200), (64, 192)]:
+        pe = SlabReconstructor(p, d, i0=1e5, rows=(r0, r1), tensor=True)
+        pe.filter_stage(raw[:, r0:r1].contiguous())
+        pe.tc_absmax()
+        pe.tc_ws[:4].view(torch.int32).copy_(gmax)  # the all-reduced max of a z-slab split
+        pe.prepare_tc(use_max=True)
+        part = pe.backproject(prepared=True).cpu()
+        assert torch.equal(part, full[r0:r1]), (r0, r1)
+    h_raw = raw.cpu().pin_memory()
+    h_vol = torch.empty((200, n, n), dtype=torch.float32).pin_memory()
+    st = StreamedReconstructor(p, d, i0=1e5, slab_rows=64)
+    assert st.eng.tensor
+    st.run(h_raw, h_vol)
+    torch.cuda.synchronize()
+    assert rel_l2(h_vol.numpy(), full.numpy()) < 1e-6
+
+
+def test_tensor_core_angle_chunks_and_depth_input(F):
+    """Angle-chunked TF_BP_ACCUMULATE passes on the tensor path agree with one
+    pass to fp32 roundoff (the RN flush blocks restart per launch), and depth
+    input (i0 <= 0) matches the CUDA-core kernel on the same depth."""
+    import torch
+
+    from paper_2505_13955_b200 import _lib
+    from paper_2505_13955_b200.engine import SlabReconstructor
+    from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
+
+    n, n_proj = 96, 100
+    p = AcquisitionParams(n_proj=n_proj, n_rows=40, n_chan=n)
+    d = VolumeDims(n, n, 40)
+    raw = _phantom_rows(p, d, 0, 40)
+    eng = SlabReconstructor(p, d, i0=1e5, tensor=True)
+    one = eng.run(raw).clone()
+    vol2 = torch.zeros_like(one)
+    cuts = [0, 7, 50, 51, 100]
+    for i, (a, b) in enumerate(zip(cuts[:-1], cuts[1:])):
+        flags = (_lib.TF_BP_ACCUMULATE if i else 0) | (_lib.TF_BP_FINALIZE if b == n_proj else 0)
+        eng.backproject(a, b, flags=flags, vol=vol2)
+    assert rel_l2(vol2.cpu().numpy(), one.cpu().numpy()) < 1e-6
+    depth = -torch.log(torch.clamp(raw, min=1.0) / 1e5)
+    got = SlabReconstructor(p, d, i0=0.0, tensor=True).run(depth).cpu().numpy()
+    ref = SlabReconstructor(p, d, i0=0.0, tensor=False).run(depth).cpu().numpy()
+    assert rel_l2(got, ref) < 2e-6

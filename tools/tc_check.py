@@ -30,10 +30,11 @@ def main():
     ap.add_argument("--oracle-rows", type=int, default=2)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--dbg", action="store_true", help="print the kernel's per-role wait-cycle counters")
+    ap.add_argument("--pitch", type=float, default=12.0)
     a = ap.parse_args()
     n, k = a.n, a.rows
-    p = AcquisitionParams(n_proj=a.n_proj, n_rows=n, n_chan=n, pixel_pitch=12.0)
-    d = VolumeDims(n, n, n, voxel_pitch=12.0)
+    p = AcquisitionParams(n_proj=a.n_proj, n_rows=n, n_chan=n, pixel_pitch=a.pitch)
+    d = VolumeDims(n, n, n, voxel_pitch=a.pitch)
     r0 = n // 2 - k // 2
     eng = SlabReconstructor(p, d, i0=1e5, rows=(0, k))
     raw = torch.empty((a.n_proj, k, n), dtype=torch.float32, device="cuda")
@@ -48,7 +49,7 @@ def main():
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
     def prep():
-        check(L.tf_bp_tc_prepare(h, ctypes.c_void_p(eng.stage.data_ptr()), k, 0, a.n_proj,
+        check(L.tf_bp_tc_prepare(h, ctypes.c_void_p(eng.stage.data_ptr()), k, 0, a.n_proj, 0.0,
                                  ctypes.c_void_p(ws.data_ptr()), st))
 
     def bp():
@@ -68,10 +69,14 @@ def main():
         names = ["mma_total", "", "", "w_total"]
         print(json.dumps({"dbg_ctas": len(d8), **{nm: round(float(d8[:, i].mean()) / a.n_proj, 1)
                                                  for i, nm in enumerate(names) if nm}, "unit": "clk per angle"}))
+    first = vol.clone()
+    bp()
+    torch.cuda.synchronize()
+    deterministic = bool(torch.equal(first, vol))
     e = int(torch.tensor(ws[4:8].cpu().numpy().view(np.int32))[0])
     diff = (vol - ref).double()
     rel = float(diff.norm() / ref.double().norm())
-    out = {"n": n, "n_proj": a.n_proj, "rows": k, "exp": e, "nan": int(torch.isnan(vol).sum()),
+    out = {"n": n, "n_proj": a.n_proj, "rows": k, "exp": e, "deterministic": deterministic, "nan": int(torch.isnan(vol).sum()),
            "rel_l2_vs_default": rel, "max_abs_vs_default": float(diff.abs().max()),
            "ref_max": float(ref.abs().max())}
 
@@ -97,7 +102,7 @@ def main():
         from oracle import fbp_oracle as O
 
         rows = [k // 2, k - 1][: a.oracle_rows]
-        geom = O.make_geom(a.n_proj, len(rows), n, pixel_pitch=12.0, voxel_pitch=12.0)
+        geom = O.make_geom(a.n_proj, len(rows), n, pixel_pitch=a.pitch, voxel_pitch=a.pitch)
         oref = C.fbp_rows(raw[:, rows].cpu().numpy(), geom)
         got = vol[rows].cpu().numpy().astype(np.float64)
         dft = ref[rows].cpu().numpy().astype(np.float64)
