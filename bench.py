@@ -714,9 +714,9 @@ def main():
         },
         "clocks": clk,
         # our kernels per step: K1 + K2, + tf_bp_stage (allgather, p2p) or + tf_bp_finalize (angle split)
-        # (+1 with the tensor-core K2: tc_convert_kernel; its scale comes from tap_bound, no absmax pass)
+        # (+2 with the tensor-core K2: tc_absmax_kernel for the fp16 tap scale, tc_convert_kernel)
         "gpu_launches": ((3 if (world > 1 and (args.exchange in ("allgather", "p2p") or angle_split)) else 2)
-                         + (1 if tensor else 0)) * args.steps,
+                         + (2 if tensor else 0)) * args.steps,
     }
     if e2e is not None:
         line["e2e"] = e2e
