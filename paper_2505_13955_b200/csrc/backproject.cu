@@ -650,8 +650,8 @@ bool tile_order_enabled() {
 
 // tile shapes (TX, TY) with a launch order each; variant -> shape
 constexpr int kNumShapes = 5;
-// shape 4 (16 x 8 = 128 voxels, the MMA M) is the tensor-core kernel's tile (backproject_tc below)
-constexpr int kTileShape[kNumShapes][2] = {{16, 16}, {32, 16}, {24, 16}, {24, 8}, {16, 8}};
+// shape 4 (11 x 11 = 121 voxels in the MMA's M = 128 rows) is the tensor-core kernel's tile (backproject_tc below)
+constexpr int kTileShape[kNumShapes][2] = {{16, 16}, {32, 16}, {24, 16}, {24, 8}, {11, 11}};
 int variant_shape(int v) { return v == 10 ? 1 : (v >= 13 ? 3 : (v >= 11 ? 2 : 0)); }
 
 // smem bytes gathered per update: 16 B per LDS.128 of 4 rows, taps / voxels
@@ -1016,7 +1016,7 @@ extern "C" int tf_backproject_reduce(const tf_bp_plan* p, const void* stage, int
 // ============================================================================
 // K2-TC: back-projection on the 5th-generation tensor cores (tcgen05).
 //
-// For one angle, a tile of M = 128 voxel columns (16 x 8) and N detector rows,
+// For one angle, a tile of 121 voxel columns (11 x 11, padded to the MMA's M = 128) and N detector rows,
 // back-projection is a small GEMM: D[m][z] += sum_k W[m][k] * T[k][z], with
 // T the filtered taps of the tile's channel window [c_lo, c_lo + 32) and W the
 // interpolation matrix -- row m holds voxel m's exact two-tap weights
@@ -1047,7 +1047,12 @@ extern "C" int tf_backproject_reduce(const tf_bp_plan* p, const void* stage, int
 // ============================================================================
 namespace tf {
 namespace {
-constexpr int kTcTX = 16, kTcTY = 8, kTcM = kTcTX * kTcTY;  // voxels per CTA = MMA M
+// An 11 x 11 voxel tile (121 of the MMA's M = 128 rows; rows 121-127 carry zero weights).  The
+// tile's channel window is 10 (|cos| + |sin|) + 1 <= 15.2 channels wide, so 97% of the angles need
+// one K-step of 16 channels; a 16 x 8 tile (15 |cos| + 7 |sin|, up to 16.6) needs two for 61%
+// of them: 1.61 -> 1.03 K-steps per angle, 0.68x the MMA work per voxel.
+constexpr int kTcTX = 11, kTcTY = 11, kTcMV = kTcTX * kTcTY;  // voxels per CTA
+constexpr int kTcM = 128;                                       // MMA M (TMEM lanes)
 constexpr int kTcK = 32;                                     // channel window (2 MMA K-steps of 16)
 constexpr int kTcSB = 10;  // tap (TMA) ring depth (smem)
 constexpr int kTcSA = 4;   // weight ring depth (TMEM columns [384, 512): 32 per stage)
@@ -1185,6 +1190,11 @@ __device__ __forceinline__ TcWin tc_bcast(const TcWin& w, int src) {
         "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])            \
         : "memory")
 
+#define TC_ST8(ta, v)                                                                                             \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "r"(v[0]),   \
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])                      \
+                 : "memory")
+
 // TMEM columns: two MMA accumulators (ping-pong per block of kTcP angles) and
 // the round-to-nearest master sum, N = 128 columns each.
 constexpr int kTcN = 128;  // rows per CTA (MMA N)
@@ -1215,8 +1225,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
         if (all_out) {
             if (a.flags & TF_BP_FINALIZE) {
                 const int nz = min(kTcN, a.n_rows - zr0);
-                for (int i = threadIdx.x; i < kTcM * nz; i += blockDim.x) {
-                    int z = i / kTcM, r = i % kTcM;
+                for (int i = threadIdx.x; i < kTcMV * nz; i += blockDim.x) {
+                    int z = i / kTcMV, r = i % kTcMV;
                     int x = X0 + (r % kTcTX), y = Y0 + (r / kTcTX);
                     if (x >= ux0 && x < ux1 && y >= uy0 && y < uy1) a.vol[(size_t)(zr0 + z) * plane + (size_t)y * a.nx + x] = 0.f;
                 }
@@ -1339,6 +1349,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
         const int grp = (warp - 2) >> 2;  // kTcSA is even: group 0 owns the even weight slots
         const int q = warp & 3;
         const int m = q * 32 + lane;
+        const bool real = m < kTcMV;  // rows kTcMV..127 of the MMA: zero weights, no output
         const int vx = m % kTcTX, vy = m / kTcTX;
         const float fdx = (float)vx, fdy = (float)vy;
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);  // this warp's TMEM lanes
@@ -1384,7 +1395,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 const __half l0 = __float2half_rn(g0w - __half2float(h0)), l1 = __float2half_rn(f - __half2float(h1));
                 const __half z = __ushort_as_half(0);
                 const bool odd = o & 1;
-                const int jo = o >> 1;
+                const int jo = real ? o >> 1 : -8;  // -8: no column holds a weight
                 const uint32_t Xh = odd ? pack_h2(z, h0) : pack_h2(h0, h1), Yh = odd ? pack_h2(h1, z) : 0u;
                 const uint32_t Xl = odd ? pack_h2(z, l0) : pack_h2(l0, l1), Yl = odd ? pack_h2(l1, z) : 0u;
                 uint32_t vh[16], vl[16];
@@ -1394,8 +1405,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                     vl[j] = j == jo ? Xl : (j == jo + 1 ? Yl : 0u);
                 }
                 const uint32_t ta = tl + (uint32_t)(kTcAcol + s * 32);  // this voxel's row of the TMEM A tile
-                TC_ST16(ta, vh);
-                TC_ST16(ta + 16, vl);
+                // a one-K-step angle (the producer's test, on the same window) reads channels 0-15 only
+                const float span = w.F0 + fmaxf(0.f, w.B * (kTcTX - 1)) + fmaxf(0.f, w.C * (kTcTY - 1));
+                if (span < 14.9f) {
+                    TC_ST8(ta, vh);
+                    TC_ST8(ta + 16, vl);
+                } else {
+                    TC_ST16(ta, vh);
+                    TC_ST16(ta + 16, vl);
+                }
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 tc_fence_before();
                 __syncwarp();
@@ -1413,7 +1431,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
         while (flushed < n_blk - 1) flush(flushed++);  // short last block
         // ---- epilogue: master + last block -> volume
         const int x = X0 + vx, y = Y0 + vy;
-        const bool inside = x >= ux0 && x < ux1 && y >= uy0 && y < uy1;
+        const bool inside = real && x >= ux0 && x < ux1 && y >= uy0 && y < uy1;
         const bool fin = (a.flags & TF_BP_FINALIZE) != 0, accum = (a.flags & TF_BP_ACCUMULATE) != 0;
         const bool zero = fin && tc_outside_fov(x, y, a);
         const float sc = n_ang > 0 ? ldexpf(1.f, -*a.d_exp) : 0.f;
