@@ -1056,7 +1056,14 @@ constexpr int kTcM = 128;                                       // MMA M (TMEM l
 constexpr int kTcK = 32;                                     // channel window (2 MMA K-steps of 16)
 constexpr int kTcSB = 10;  // tap (TMA) ring depth (smem)
 constexpr int kTcSA = 4;   // weight ring depth (TMEM columns [384, 512): 32 per stage)
-constexpr int kTcThreads = 320;  // w0 TMA, w1 MMA, w2-5 / w6-9 weight groups (even / odd angles)
+#ifndef TF_TC_GROUPS
+#define TF_TC_GROUPS 4
+#endif
+constexpr int kTcG = TF_TC_GROUPS;  // weight-producer groups of 4 warps, angle g -> group g % kTcG: each
+                                    // group's per-angle chain (window, weights, tcgen05.st, arrive) is
+                                    // latency-bound, so more groups keep more angles in flight
+static_assert(kTcSA % kTcG == 0, "each group owns kTcSA / kTcG weight slots");
+constexpr int kTcThreads = 64 + 128 * kTcG;  // w0 TMA, w1 MMA, then the weight groups
 constexpr int kTcShape = 4;                                  // kTileShape[4] = {16, 8}
 constexpr int kTcHeader = 256;                               // workspace header: absmax bits, exponent
 
@@ -1152,7 +1159,7 @@ __device__ __forceinline__ TcWin tc_window_lane(int g0, int n_ang, double dX, do
 // windows of angles g0, g0 + 2, ..., g0 + 62 (one weight group's alternate angles), one per lane
 __device__ __forceinline__ TcWin tc_window_lane2(int g0, int n_ang, double dX, double dY, const TCArgs& a) {
     const int lane = threadIdx.x & 31;
-    const int g = min(g0 + 2 * lane, n_ang - 1);
+    const int g = min(g0 + kTcG * lane, n_ang - 1);
     return tc_window(dX, dY, a.trig[a.a0 + g], a);
 }
 __device__ __forceinline__ TcWin tc_bcast(const TcWin& w, int src) {
@@ -1346,7 +1353,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
     } else {
         // ---- weight producers: two groups of 4 warps take alternate angles (one voxel per
         // thread; TMEM lane quadrant = warp % 4); group 0 also does the RN flush and the epilogue
-        const int grp = (warp - 2) >> 2;  // kTcSA is even: group 0 owns the even weight slots
+        const int grp = (warp - 2) >> 2;  // group grp owns the weight slots s with s % kTcG == grp
         const int q = warp & 3;
         const int m = q * 32 + lane;
         const bool real = m < kTcMV;  // rows kTcMV..127 of the MMA: zero weights, no output
@@ -1376,10 +1383,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
         };
         int flushed = 0;
         const long long t_w0 = a.dbg ? clock64() : 0;
-        for (int g0 = grp; g0 < n_ang; g0 += 64) {
+        for (int g0 = grp; g0 < n_ang; g0 += 32 * kTcG) {
             const TcWin wl = tc_window_lane2(g0, n_ang, dX, dY, a);
             for (int i = 0; i < 32; ++i) {
-                const int g = g0 + 2 * i;
+                const int g = g0 + kTcG * i;
                 if (g >= n_ang) break;
                 const TcWin w = tc_bcast(wl, i);
                 const int s = g % kTcSA;
