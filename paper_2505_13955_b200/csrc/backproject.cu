@@ -39,14 +39,16 @@
 #include "common.cuh"
 #include "internal.hpp"
 
+constexpr int kNumTileShapes = 6;  // tile shapes with a launch order (kTileShape below)
+
 struct tf_bp_plan {
     tf_geometry g;
     int feather_band;
     double2* d_trig;  // (cos, sin) of k * (span / n_proj), fp64 libm, per angle
     float* d_w;       // feather weights (fp32, as numpy casts them)
     double ext;       // max channel extent of a tile's rays over all angles
-    int* d_order[5];  // launch order of the tiles (Morton, FoV-active first) per tile shape
-    int n_active[5];
+    int* d_order[kNumTileShapes];  // launch order of the tiles (Morton, FoV-active first) per tile shape
+    int n_active[kNumTileShapes];
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
 };
@@ -649,9 +651,9 @@ bool tile_order_enabled() {
 }
 
 // tile shapes (TX, TY) with a launch order each; variant -> shape
-constexpr int kNumShapes = 5;
+constexpr int kNumShapes = kNumTileShapes;
 // shape 4 (11 x 11 = 121 voxels in the MMA's M = 128 rows) is the tensor-core kernel's tile (backproject_tc below)
-constexpr int kTileShape[kNumShapes][2] = {{16, 16}, {32, 16}, {24, 16}, {24, 8}, {11, 11}};
+constexpr int kTileShape[kNumShapes][2] = {{16, 16}, {32, 16}, {24, 16}, {24, 8}, {11, 11}, {11, 10}};
 int variant_shape(int v) { return v == 10 ? 1 : (v >= 13 ? 3 : (v >= 11 ? 2 : 0)); }
 
 // smem bytes gathered per update: 16 B per LDS.128 of 4 rows, taps / voxels
@@ -1051,20 +1053,33 @@ namespace {
 // tile's channel window is 10 (|cos| + |sin|) + 1 <= 15.2 channels wide, so 97% of the angles need
 // one K-step of 16 channels; a 16 x 8 tile (15 |cos| + 7 |sin|, up to 16.6) needs two for 61%
 // of them: 1.61 -> 1.03 K-steps per angle, 0.68x the MMA work per voxel.
-constexpr int kTcTX = 11, kTcTY = 11, kTcMV = kTcTX * kTcTY;  // voxels per CTA
-constexpr int kTcM = 128;                                       // MMA M (TMEM lanes)
+// Optional "narrow" kernel (TF_TC_NARROW=1), when the geometry guarantees one K-step for every angle
+// (pitch ratio < 1.026): an 11 x 10 tile (10|cos| + 9|sin| + 1 <= 14.5 channels) and 16-column
+// weight slots, so the 128 TMEM weight columns hold 8 slots instead of 4.  It tested whether the
+// weight ring's depth bounds the MMA issue rate (ncu of the 11 x 11 kernel: the weight warps wait on
+// the slot's MMA completion for 48% of the stall samples, tensor pipe 46% busy).  It does not:
+// 8 slots ran 475 clk per angle per SM against 427 for 4 slots (profiles/r01_tc_check_v7_narrow.jsonl),
+// so it is off by default.
+template <bool NW>
+struct TcT {
+    static constexpr int TX = 11, TY = NW ? 10 : 11, MV = TX * TY;  // tile, voxels per CTA
+    static constexpr int SA = NW ? 8 : 4;                           // weight slots (ring depth)
+    static constexpr int SW = NW ? 16 : 32;                         // TMEM columns per slot (hi | lo)
+};
+constexpr int kTcSAmax = 8;
+constexpr int kTcM = 128;  // MMA M (TMEM lanes)
 constexpr int kTcK = 32;                                     // channel window (2 MMA K-steps of 16)
 constexpr int kTcSB = 10;  // tap (TMA) ring depth (smem)
-constexpr int kTcSA = 4;   // weight ring depth (TMEM columns [384, 512): 32 per stage)
+constexpr int kTcSA = 4;   // weight ring depth of the wide kernel (TMEM columns [384, 512): 32 per stage)
 #ifndef TF_TC_GROUPS
 #define TF_TC_GROUPS 4
 #endif
 constexpr int kTcG = TF_TC_GROUPS;  // weight-producer groups of 4 warps, angle g -> group g % kTcG: each
                                     // group's per-angle chain (window, weights, tcgen05.st, arrive) is
                                     // latency-bound, so more groups keep more angles in flight
-static_assert(kTcSA % kTcG == 0, "each group owns kTcSA / kTcG weight slots");
+static_assert(kTcSA % kTcG == 0 && kTcSAmax % kTcG == 0, "each group owns SA / kTcG weight slots");
 constexpr int kTcThreads = 64 + 128 * kTcG;  // w0 TMA, w1 MMA, then the weight groups
-constexpr int kTcShape = 4;                                  // kTileShape[4] = {16, 8}
+constexpr int kTcShape = 4;  // kTileShape[4] = {11, 11}, [5] = {11, 10} (narrow)
 constexpr int kTcHeader = 256;                               // workspace header: absmax bits, exponent
 
 struct TCArgs {
@@ -1131,11 +1146,12 @@ struct TcWin {
     int c_lo;
     float F0, B, C;
 };
+template <bool NW>
 __device__ __forceinline__ TcWin tc_window(double dX, double dY, double2 cs, const TCArgs& a) {
     double t0 = __dadd_rn(__dmul_rn(dX, cs.x), __dmul_rn(dY, cs.y));
     t0 = __dadd_rn(__dmul_rn(t0, a.scale), a.axis);
     const double B = cs.x * a.scale, C = cs.y * a.scale;
-    const double tmin = t0 + fmin(0.0, B * (kTcTX - 1)) + fmin(0.0, C * (kTcTY - 1));
+    const double tmin = t0 + fmin(0.0, B * (TcT<NW>::TX - 1)) + fmin(0.0, C * (TcT<NW>::TY - 1));
     TcWin w;
     w.c_lo = (int)floor(tmin);
     w.F0 = (float)(t0 - (double)w.c_lo);
@@ -1151,16 +1167,18 @@ __device__ __forceinline__ bool tc_outside_fov(int x, int y, const TCArgs& a) {
 }
 
 // 32 consecutive angles' windows, one per lane (g0 + lane); read back with tc_bcast
+template <bool NW>
 __device__ __forceinline__ TcWin tc_window_lane(int g0, int n_ang, double dX, double dY, const TCArgs& a) {
     const int lane = threadIdx.x & 31;
     const int g = min(g0 + lane, n_ang - 1);
-    return tc_window(dX, dY, a.trig[a.a0 + g], a);
+    return tc_window<NW>(dX, dY, a.trig[a.a0 + g], a);
 }
 // windows of angles g0, g0 + 2, ..., g0 + 62 (one weight group's alternate angles), one per lane
+template <bool NW>
 __device__ __forceinline__ TcWin tc_window_lane2(int g0, int n_ang, double dX, double dY, const TCArgs& a) {
     const int lane = threadIdx.x & 31;
     const int g = min(g0 + kTcG * lane, n_ang - 1);
-    return tc_window(dX, dY, a.trig[a.a0 + g], a);
+    return tc_window<NW>(dX, dY, a.trig[a.a0 + g], a);
 }
 __device__ __forceinline__ TcWin tc_bcast(const TcWin& w, int src) {
     TcWin r;
@@ -1209,7 +1227,10 @@ constexpr int kTcAcol = 3 * kTcN;  // first TMEM column of the weight (A) ring
 constexpr int kTcP = 16;   // angles per accumulator block (the tensor core's fp32 accumulation truncates:
                            // its bias grows with the count, so blocks are re-added in RN fp32 by threads)
 
+template <bool NW>
 __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_constant__ CUtensorMap map, const TCArgs a) {
+    using T = TcT<NW>;
+    constexpr int kTcTX = T::TX, kTcTY = T::TY, kTcMV = T::MV, kTcSA = T::SA;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % a.ntx, ty = tile / a.ntx;
@@ -1285,12 +1306,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
         // ---- TMA producer: windows for 32 angles per batch, one per lane
         if (lane == 0) tma_prefetch_desc(&map);
         for (int g0 = 0; g0 < n_ang; g0 += 32) {
-            const TcWin wl = tc_window_lane(g0, n_ang, dX, dY, a);
+            const TcWin wl = tc_window_lane<NW>(g0, n_ang, dX, dY, a);
             // one K-step suffices when every tap of the tile lies in the first 16 channels
             // (t - c_lo < 15 with a margin for the fp32 t of the weights; the skipped
             // weights are exact zeros)
             const float span = wl.F0 + fmaxf(0.f, wl.B * (kTcTX - 1)) + fmaxf(0.f, wl.C * (kTcTY - 1));
-            const int ksl = span < 14.9f ? 1 : 2;
+            const int ksl = (NW || span < 14.9f) ? 1 : 2;
             const int gn = min(32, n_ang - g0);
             for (int i = 0; i < gn; ++i) {
                 const int c_lo = __shfl_sync(0xffffffffu, wl.c_lo, i);
@@ -1332,7 +1353,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 ksum += nks;
                 if (elect_one()) {
                     const uint64_t dbh = db0 + (uint64_t)((sb * 2 * bbytes) >> 4), dbl = dbh + (bbytes >> 4);
-                    const uint32_t ah = tmem + (uint32_t)(kTcAcol + sa * 32), al = ah + 16;  // TMEM weight tiles
+                    const uint32_t ah = tmem + (uint32_t)(kTcAcol + sa * T::SW), al = ah + T::SW / 2;  // TMEM weights
                     const uint32_t td = tmem + (uint32_t)(b * kTcN);
                     umma_f16_ts(td, ah, dbh, idesc, first ? 0u : 1u);
                     umma_f16_ts(td, al, dbh, idesc, 1u);
@@ -1384,7 +1405,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
         int flushed = 0;
         const long long t_w0 = a.dbg ? clock64() : 0;
         for (int g0 = grp; g0 < n_ang; g0 += 32 * kTcG) {
-            const TcWin wl = tc_window_lane2(g0, n_ang, dX, dY, a);
+            const TcWin wl = tc_window_lane2<NW>(g0, n_ang, dX, dY, a);
             for (int i = 0; i < 32; ++i) {
                 const int g = g0 + kTcG * i;
                 if (g >= n_ang) break;
@@ -1411,10 +1432,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                     vh[j] = j == jo ? Xh : (j == jo + 1 ? Yh : 0u);
                     vl[j] = j == jo ? Xl : (j == jo + 1 ? Yl : 0u);
                 }
-                const uint32_t ta = tl + (uint32_t)(kTcAcol + s * 32);  // this voxel's row of the TMEM A tile
+                const uint32_t ta = tl + (uint32_t)(kTcAcol + s * T::SW);  // this voxel's row of the TMEM A tile
                 // a one-K-step angle (the producer's test, on the same window) reads channels 0-15 only
                 const float span = w.F0 + fmaxf(0.f, w.B * (kTcTX - 1)) + fmaxf(0.f, w.C * (kTcTY - 1));
-                if (span < 14.9f) {
+                if (NW) {
+                    TC_ST8(ta, vh);
+                    TC_ST8(ta + 8, vl);
+                } else if (span < 14.9f) {
                     TC_ST8(ta, vh);
                     TC_ST8(ta + 16, vl);
                 } else {
@@ -1645,9 +1669,17 @@ extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* ws, int ws_a0,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
 
+    // narrow kernel when every angle's window fits one K-step: frac(t_min) + scale (10|cos| + 9|sin|)
+    // < 1 + scale sqrt(181) must stay below the producer's 14.9-channel test (fp32 margin)
+    static const bool narrow_on = [] {
+        const char* e = getenv("TF_TC_NARROW");  // experiment knob: 1 = narrow kernel when it applies
+        return e ? atoi(e) != 0 : false;
+    }();
+    const bool nw = narrow_on && p->scale * std::sqrt(181.0) + 1.0 < 14.8;
+    const int TXs = nw ? TcT<true>::TX : TcT<false>::TX, TYs = nw ? TcT<true>::TY : TcT<false>::TY;
     TCArgs a{};
     a.trig = p->d_trig;
-    a.order = tile_order_enabled() ? p->d_order[kTcShape] : nullptr;
+    a.order = tile_order_enabled() ? p->d_order[kTcShape + (nw ? 1 : 0)] : nullptr;
     a.d_exp = reinterpret_cast<const int*>(static_cast<const uint8_t*>(ws) + 4);
     a.vol = vol;
     a.a0 = a0;
@@ -1661,7 +1693,7 @@ extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* ws, int ws_a0,
     a.x1 = x1;
     a.y0 = y0;
     a.y1 = y1;
-    a.ntx = (g.nx + kTcTX - 1) / kTcTX;
+    a.ntx = (g.nx + TXs - 1) / TXs;
     a.N = N;
     a.flags = flags;
     a.cx = p->cx;
@@ -1673,10 +1705,15 @@ extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* ws, int ws_a0,
     a.angle_wf = p->angle_wf;
     a.dbg = tc_debug_buffer();
     a.kcount = g_tc_count;
-    const int nty = (g.ny + kTcTY - 1) / kTcTY;
-    const int smem = kTcSB * 2 * N * kTcK * 2 + (2 * kTcSB + kTcSA + 5) * 8 + 8 + 4 * kTcSB;
-    TF_CUDA_TRY(cudaFuncSetAttribute(bp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int nty = (g.ny + TYs - 1) / TYs;
+    const int smem = kTcSB * 2 * N * kTcK * 2 + (2 * kTcSB + kTcSAmax + 5) * 8 + 8 + 4 * kTcSB;
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)((nzb * kZB + N - 1) / N));
-    bp_tc_kernel<<<grid, kTcThreads, smem, as_stream(stream)>>>(map, a);
+    if (nw) {
+        TF_CUDA_TRY(cudaFuncSetAttribute(bp_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        bp_tc_kernel<true><<<grid, kTcThreads, smem, as_stream(stream)>>>(map, a);
+    } else {
+        TF_CUDA_TRY(cudaFuncSetAttribute(bp_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        bp_tc_kernel<false><<<grid, kTcThreads, smem, as_stream(stream)>>>(map, a);
+    }
     return check_launch("bp_tc_kernel");
 }
