@@ -48,6 +48,15 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t da, uint64_t db, u
         "l"(da), "l"(db), "r"(IDESC), "r"(acc));
 }
 
+// -DATMEM: A from TMEM (columns [N, N + K/2), fp16 pairs, written with tcgen05.st), as the
+// tensor-core back-projection does with its weight rows
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t ta, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "r"(ta), "l"(db), "r"(IDESC), "r"(acc));
+}
+
 __global__ void __launch_bounds__(128, 1) k_probe(const __half* A, const __half* B, float* D, long long* clk, int reps) {
 #ifndef NBUF
 #define NBUF 1
@@ -77,20 +86,42 @@ __global__ void __launch_bounds__(128, 1) k_probe(const __half* A, const __half*
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)),
-                     "n"(256));
+                     "n"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t td = tbase;
+#ifdef ATMEM
+    {
+        uint32_t v[K / 2];
+        for (int j = 0; j < K / 2; ++j) {
+            __half2 h = __halves2half2(A[tid * K + 2 * j], A[tid * K + 2 * j + 1]);
+            v[j] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        const uint32_t ta = td + ((uint32_t)(warp * 32) << 16) + N;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                     ::"r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                     "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]) : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+#endif
     if (tid == 0) {
         long long t0 = clock64();
         for (int r = 0; r < reps; ++r) {
 #pragma unroll
             for (int s = 0; s < KS; ++s)
+#ifdef ATMEM
+                mma_ts(td, td + N + s * 8, sdesc(smem_u32(sb) + (r % NBUF) * N * K * 2 + s * 256, B_LBO, B_SBO),
+                       (r | s) ? 1u : 0u);
+#else
                 mma(td, sdesc(smem_u32(sa) + (r % NBUF) * M * K * 2 + s * 2 * A_LBO, A_LBO, A_SBO),
                     sdesc(smem_u32(sb) + (r % NBUF) * N * K * 2 + s * 256, B_LBO, B_SBO), (r | s) ? 1u : 0u);
+#endif
 #ifdef PCOMMIT  // a commit per KS-step group (as the back-projection kernel does per angle)
             for (int c = 0; c < PCOMMIT; ++c)
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -128,7 +159,7 @@ __global__ void __launch_bounds__(128, 1) k_probe(const __half* A, const __half*
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(td), "n"(256));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(td), "n"(512));
 }
 
 int main() {
