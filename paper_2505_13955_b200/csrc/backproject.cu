@@ -1228,7 +1228,8 @@ constexpr int kTcP = 16;   // angles per accumulator block (the tensor core's fp
                            // its bias grows with the count, so blocks are re-added in RN fp32 by threads)
 
 template <bool NW>
-__global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_constant__ CUtensorMap map, const TCArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_constant__ CUtensorMap map,
+                                                              const __grid_constant__ CUtensorMap map16, const TCArgs a) {
     using T = TcT<NW>;
     constexpr int kTcTX = T::TX, kTcTY = T::TY, kTcMV = T::MV, kTcSA = T::SA;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -1304,7 +1305,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
 
     if (warp == 0) {
         // ---- TMA producer: windows for 32 angles per batch, one per lane
-        if (lane == 0) tma_prefetch_desc(&map);
+        if (lane == 0) {
+            tma_prefetch_desc(&map);
+            tma_prefetch_desc(&map16);
+        }
         for (int g0 = 0; g0 < n_ang; g0 += 32) {
             const TcWin wl = tc_window_lane<NW>(g0, n_ang, dX, dY, a);
             // one K-step suffices when every tap of the tile lies in the first 16 channels
@@ -1322,10 +1326,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                     if (g >= kTcSB) mbar_wait(&empty[s], (uint32_t)((g / kTcSB) - 1) & 1u);
                     uint8_t* st = bring + s * 2 * bbytes;
                     kring[s] = nks;
-                    mbar_arrive_expect_tx(&full[s], 2 * bbytes);
+                    // a one-K-step angle loads the 16-channel box only (half the L2 -> smem bytes)
+                    const CUtensorMap* mp = nks > 1 ? &map : &map16;
+                    mbar_arrive_expect_tx(&full[s], nks > 1 ? 2 * bbytes : bbytes);
                     const int ka = 2 * (a.a0 + g - a.ws_a0);
-                    tma_load_3d(st, &map, &full[s], 8 * c_lo, zr0 / 8, ka);
-                    tma_load_3d(st + bbytes, &map, &full[s], 8 * c_lo, zr0 / 8, ka + 1);
+                    tma_load_3d(st, mp, &full[s], 8 * c_lo, zr0 / 8, ka);
+                    tma_load_3d(st + bbytes, mp, &full[s], 8 * c_lo, zr0 / 8, ka + 1);
                 }
                 __syncwarp();
             }
@@ -1339,6 +1345,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
             // B: LBO = 128 B between 8-channel chunks, SBO = 32 ch x 16 B between 8-row groups; the
             // start-address field (bits 0-13, addr >> 4) is advanced by adding offsets >> 4
             const uint64_t db0 = umma_sdesc(smem_u32(smem), 128, kTcK * 16);
+            const uint64_t db16 = umma_sdesc(smem_u32(smem), 128, 16 * 16);  // 16-channel boxes: SBO 256 B
             long long t_start = a.dbg ? clock64() : 0;
             int ksum = 0;
             for (int g = 0; g < n_ang; ++g) {
@@ -1352,7 +1359,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 const int nks = kring[sb];
                 ksum += nks;
                 if (elect_one()) {
-                    const uint64_t dbh = db0 + (uint64_t)((sb * 2 * bbytes) >> 4), dbl = dbh + (bbytes >> 4);
+                    const uint64_t dbh = (nks > 1 ? db0 : db16) + (uint64_t)((sb * 2 * bbytes) >> 4),
+                                   dbl = dbh + (bbytes >> 4);
                     const uint32_t ah = tmem + (uint32_t)(kTcAcol + sa * T::SW), al = ah + T::SW / 2;  // TMEM weights
                     const uint32_t td = tmem + (uint32_t)(b * kTcN);
                     umma_f16_ts(td, ah, dbh, idesc, first ? 0u : 1u);
@@ -1668,6 +1676,11 @@ extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* ws, int ws_a0,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+    CUtensorMap map16;  // the same taps, 16-channel boxes (one-K-step angles)
+    cuuint32_t box16[3] = {(cuuint32_t)(8 * 16), (cuuint32_t)(N / 8), 1u};
+    cr = enc(&map16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, data, dims, strides, box16, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
 
     // narrow kernel when every angle's window fits one K-step: frac(t_min) + scale (10|cos| + 9|sin|)
     // < 1 + scale sqrt(181) must stay below the producer's 14.9-channel test (fp32 margin)
@@ -1710,10 +1723,10 @@ extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* ws, int ws_a0,
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)((nzb * kZB + N - 1) / N));
     if (nw) {
         TF_CUDA_TRY(cudaFuncSetAttribute(bp_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        bp_tc_kernel<true><<<grid, kTcThreads, smem, as_stream(stream)>>>(map, a);
+        bp_tc_kernel<true><<<grid, kTcThreads, smem, as_stream(stream)>>>(map, map16, a);
     } else {
         TF_CUDA_TRY(cudaFuncSetAttribute(bp_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        bp_tc_kernel<false><<<grid, kTcThreads, smem, as_stream(stream)>>>(map, a);
+        bp_tc_kernel<false><<<grid, kTcThreads, smem, as_stream(stream)>>>(map, map16, a);
     }
     return check_launch("bp_tc_kernel");
 }
