@@ -633,7 +633,7 @@ def main():
         return
     tc_roof = None
     if tensor:
-        # tensor-core K2: per angle and CTA (128 voxels x 128 rows) 3 fp16 MMAs of 128 x 128 x 16
+        # tensor-core K2: per angle and CTA (121 voxels padded to M = 128, x 128 rows) 3 fp16 MMAs of 128 x 128 x 16
         # per K-step (T_hi W_hi + T_hi W_lo + T_lo W_hi), 1 or 2 K-steps by the tile's window
         flops = ksteps_per_launch * 3 * 2 * 128 * 128 * 16
         tflops = flops / (bp_avg_ms / 1e3) / 1e12
@@ -655,9 +655,10 @@ def main():
             "mma_ksteps_per_launch": ksteps_per_launch,
             "bp_ms_per_launch": round(bp_avg_ms, 3),
             "bp_gups_full_count": round(slab_updates / (bp_avg_ms / 1e3) / 1e9, 1),
-            # per angle and CTA: TMA writes 2 x 128 rows x 32 ch x 2 B = 16 KB, the MMAs read B 3x per
-            # K-step (2 x 12 KB); weights come from TMEM: (16 + 24) KB / 16384 updates
-            "smem_bytes_per_update": 2.5,
+            # per angle and CTA (11 x 11 voxels x 128 rows = 15488 updates), one K-step (97% of angles):
+            # TMA writes 2 x 128 rows x 16 ch x 2 B = 8 KB and the MMAs read B 3 x 4 KB; weights come
+            # from TMEM: 20 KB / 15488 updates
+            "smem_bytes_per_update": 1.32,
             "hbm_gbs_algorithmic": round(hbm_alg / (bp_avg_ms / 1e3) / 1e9, 1),
             "hbm_peak_measured": peaks.get("hbm_gbs"),
         }
