@@ -205,8 +205,8 @@ TF_API int tf_bp_kernel_info(const tf_bp_plan* plan, int flags, int n_rows, int 
 /* ---- tensor-core back-projection (K2-TC, same contract as tf_backproject) --
  * The same sum as tf_backproject (fbp.py:186-252) computed as per-angle GEMMs
  * D[voxel][row] += W[voxel][chan] * T[chan][row] on tcgen05 (fp16 hi/lo split
- * operands, fp32 TMEM accumulation): 16 x 8 voxel tiles, exact two-tap
- * weights.  Not bitwise equal to the CUDA-core kernels (different summation
+ * operands, fp32 TMEM accumulation): 11 x 11 voxel tiles (121 of the MMA's
+ * 128 rows), exact two-tap weights.  Not bitwise equal to the CUDA-core kernels (different summation
  * order); within the fp32 tolerance of the reference float64 output.
  * 1. tf_bp_tc_prepare converts angles [a0, a1) of a z-blocked staging buffer
  *    (tf_filter_stage / tf_bp_stage output for n_rows rows) into `ws`

@@ -1347,14 +1347,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
             const uint64_t db0 = umma_sdesc(smem_u32(smem), 128, kTcK * 16);
             const uint64_t db16 = umma_sdesc(smem_u32(smem), 128, 16 * 16);  // 16-channel boxes: SBO 256 B
             long long t_start = a.dbg ? clock64() : 0;
+            long long c_acc = 0, c_full = 0, c_afull = 0;  // wait cycles per barrier (a.dbg only)
             int ksum = 0;
             for (int g = 0; g < n_ang; ++g) {
                 const int sb = g % kTcSB, sa = g % kTcSA;
                 const int blk = g / kTcP, b = blk & 1;
                 const bool first = (g % kTcP) == 0;
+                const long long w0 = a.dbg ? clock64() : 0;
                 if (first && blk >= 2) mbar_wait(&accfree[b], (uint32_t)((blk / 2) - 1) & 1u);
+                const long long w1 = a.dbg ? clock64() : 0;
                 mbar_wait(&full[sb], (uint32_t)(g / kTcSB) & 1u);
+                const long long w2 = a.dbg ? clock64() : 0;
                 mbar_wait(&afull[sa], (uint32_t)(g / kTcSA) & 1u);
+                if (a.dbg) {
+                    const long long w3 = clock64();
+                    c_acc += w1 - w0;
+                    c_full += w2 - w1;
+                    c_afull += w3 - w2;
+                }
                 tc_fence_after();
                 const int nks = kring[sb];
                 ksum += nks;
@@ -1376,7 +1386,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 }
                 __syncwarp();
             }
-            if (a.dbg && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) a.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
+            if (a.dbg && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) {
+                a.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
+                a.dbg[blockIdx.x * 8 + 4] = c_acc;
+                a.dbg[blockIdx.x * 8 + 5] = c_full;
+                a.dbg[blockIdx.x * 8 + 6] = c_afull;
+            }
             if (a.kcount && lane == 0) atomicAdd(a.kcount, (unsigned long long)ksum);
         }
     } else {
@@ -1412,6 +1427,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
         };
         int flushed = 0;
         const long long t_w0 = a.dbg ? clock64() : 0;
+        long long c_wempty = 0;  // this warp's wait cycles on weight-slot reuse (a.dbg only)
         for (int g0 = grp; g0 < n_ang; g0 += 32 * kTcG) {
             const TcWin wl = tc_window_lane2<NW>(g0, n_ang, dX, dY, a);
             for (int i = 0; i < 32; ++i) {
@@ -1421,7 +1437,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
                 const int s = g % kTcSA;
                 // weight slot s was last used by angle g - kTcSA: wait for its MMAs (the tap
                 // ring's empty barrier of that angle; the MMA thread commits one per angle)
+                const long long we0 = a.dbg ? clock64() : 0;
                 if (g >= kTcSA) mbar_wait(&empty[(g - kTcSA) % kTcSB], (uint32_t)((g - kTcSA) / kTcSB) & 1u);
+                if (a.dbg) c_wempty += clock64() - we0;
                 const float t = fmaxf(fmaf(fdy, w.C, fmaf(fdx, w.B, w.F0)), 0.f);
                 const float fl = floorf(t);
                 const float f = t - fl;
@@ -1465,6 +1483,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_const
         }
         if (a.dbg && warp == 2 && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) {
             a.dbg[blockIdx.x * 8 + 3] = clock64() - t_w0;
+            a.dbg[blockIdx.x * 8 + 7] = c_wempty;
         }
         if (grp == 0) {
         while (flushed < n_blk - 1) flush(flushed++);  // short last block

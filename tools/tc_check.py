@@ -66,7 +66,8 @@ def main():
     if a.dbg:
         d8 = dbg.view(1024, 8).cpu().numpy().astype(np.float64)
         d8 = d8[d8[:, 0] > 0]
-        names = ["mma_total", "", "", "w_total"]
+        names = ["mma_total", "", "", "w_total", "mma_wait_accfree", "mma_wait_full", "mma_wait_afull",
+                 "w_wait_empty"]
         print(json.dumps({"dbg_ctas": len(d8), **{nm: round(float(d8[:, i].mean()) / a.n_proj, 1)
                                                  for i, nm in enumerate(names) if nm}, "unit": "clk per angle"}))
     first = vol.clone()
