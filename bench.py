@@ -443,10 +443,9 @@ def main():
         def step_parts():
             eng.filter(raw)
             eng.exchange()
-            eng.stage()
-            eng.prepare_bp()  # tensor-core K2: fp16 hi/lo taps, scale from the all-reduced max |T|
+            eng.stage()  # owner: natural rows -> tap planes (tensor K2) or z-blocked staging
             bp_ev[0].record()
-            eng.local.backproject(prepared=True)
+            eng.local.backproject()
             bp_ev[1].record()
     else:
         eng = slab = SlabReconstructor(p, d, i0=I0, device=dev)
@@ -455,11 +454,9 @@ def main():
         k_rows = n
 
         def step_parts():
-            eng.filter_stage(raw)  # K1 fused: Beer-Lambert + ramp + feather -> z-blocked staging
-            if eng.tensor:
-                eng.prepare_tc()  # fp16 hi/lo taps for the tensor-core K2
+            eng.filter_stage(raw)  # K1 fused: Beer-Lambert + ramp + feather -> tap planes (or staging)
             bp_ev[0].record()
-            eng.backproject(prepared=True)
+            eng.backproject()
             bp_ev[1].record()
 
     torch.cuda.synchronize()
@@ -481,20 +478,14 @@ def main():
     if world > 1:
         dist.barrier()
     tensor = bool(getattr(slab, "tensor", False)) and not angle_split
-    if tensor:  # count the MMA K-steps K2 issues in the timed steps (its FLOPs)
-        from paper_2505_13955_b200._lib import lib as _tl
-
-        kcount = torch.zeros(1, dtype=torch.int64, device=dev)
-        _tl().tf_bp_tc_count(ctypes.c_void_p(kcount.data_ptr()))
     for e in evs:
         bp_ev = [e[1], e[2]]
         e[0].record()
         step_parts()
         e[3].record()
     torch.cuda.synchronize()
-    if tensor:
-        _tl().tf_bp_tc_count(None)
-        ksteps_per_launch = kcount.item() / args.steps
+    if tensor:  # the MMA items K2 issues per launch (same window test as the kernel, tf_bp_tc_work)
+        ksteps_per_launch = slab.bp_work(bp_a0, bp_a1)["mma_items"]
     if world > 1:
         dist.barrier()
     clk = clocks.stop()

@@ -135,6 +135,20 @@ TF_API int tf_filter_stage_peers(const tf_filter_plan* plan, const tf_bp_plan* b
 TF_API int tf_filter_peers(const tf_filter_plan* plan, const float* in, int64_t n_lines, float i0, int rows_per_angle,
                            int n_slabs, const int32_t* slab_row0, void* const* slab_dst, void* stream);
 
+/* K1 straight into K2-TC's tap planes (tf_bp_tc_taps_bytes): Beer-Lambert,
+ * ramp filter, feather, x 2^e[r], fp16 hi/lo split in the epilogue -- no fp32
+ * staging, no conversion pass.  Lines are (angle, row) of an angle-major
+ * block of rows_per_angle rows; the workspace's angle 0 is the block's first.
+ * i0 > 0 (raw counts): one exponent for every row from the analytic bound
+ * |T| <= max|depth| * sum|h| / pitch with |depth| <= max(ln i0, ln FLT_MAX -
+ * ln i0) (tf_filter_tap_bound), so the scale never depends on the data and
+ * sub-slabs, chunks and GPUs see the same taps.  i0 <= 0 (optical depth):
+ * per-row exponents from each row's max |depth| (one extra read pass). */
+TF_API int tf_filter_taps(const tf_filter_plan* plan, const tf_bp_plan* bp, const float* in, void* taps,
+                          int64_t taps_bytes, int64_t n_lines, float i0, int rows_per_angle, void* stream);
+/* The bound on |T| that tf_filter_taps uses for raw counts with this i0. */
+TF_API int tf_filter_tap_bound(const tf_filter_plan* plan, double i0, double* bound);
+
 /* Beer-Lambert only (fbp.py:75-83): fp32 or fp64 counts -> fp64 depth
  * (the reference's output dtype), computed in fp64. */
 TF_API int tf_preprocess(const void* raw, int raw_dtype, double* out, int64_t n, double i0, void* stream);
@@ -202,36 +216,47 @@ TF_API int tf_bp_smem_bytes_per_update(const tf_bp_plan* plan, int flags, double
 TF_API int tf_bp_kernel_info(const tf_bp_plan* plan, int flags, int n_rows, int a0, int a1, double* bytes,
                              int64_t* executed_updates);
 
-/* ---- tensor-core back-projection (K2-TC, same contract as tf_backproject) --
+/* ---- tensor-core back-projection (K2-TC, the default; same contract as
+ * tf_backproject) ------------------------------------------------------------
  * The same sum as tf_backproject (fbp.py:186-252) computed as per-angle GEMMs
- * D[voxel][row] += W[voxel][chan] * T[chan][row] on tcgen05 (fp16 hi/lo split
- * operands, fp32 TMEM accumulation): 11 x 11 voxel tiles (121 of the MMA's
- * 128 rows), exact two-tap weights.  Not bitwise equal to the CUDA-core kernels (different summation
- * order); within the fp32 tolerance of the reference float64 output.
- * 1. tf_bp_tc_prepare converts angles [a0, a1) of a z-blocked staging buffer
- *    (tf_filter_stage / tf_bp_stage output for n_rows rows) into `ws`
- *    (tf_bp_tc_workspace_bytes): fp16 hi/lo taps scaled by 2^e with
- *    max|T| 2^e < 2^15.  t_bound == 0 takes max|T| from the data on the
- *    device (no host sync); t_bound > 0 is a caller bound on |T|; t_bound < 0
- *    uses the max already in ws (tf_bp_tc_absmax, possibly all-reduced over
- *    the ranks of a z-slab split so every rank uses the same scale).
- * 2. tf_backproject_tc back-projects angles [a0, a1) within the prepared
- *    [ws_a0, ws_a1), flags as tf_backproject (TF_BP_ACCUMULATE/FINALIZE).
- * Requires voxel_pitch / pixel_pitch <= 1.5 (tf_bp_tc_supported). */
+ * D[voxel][row] += W[voxel][chan] * T[chan][row] on tcgen05: 11 x 11 voxel
+ * tiles (121 of the MMA's M = 128 rows) x 256 (or 128) detector rows, exact
+ * two-tap weights, fp16 hi/lo split operands, fp32 accumulation in TMEM over
+ * blocks of 16 angles (blocks of the absolute angle index k / 16) re-added in
+ * round-to-nearest fp32.  Not bitwise equal to the CUDA-core kernels
+ * (different summation order); within the fp32 tolerance of the reference's
+ * float64 output.  Angle chunks chained with TF_BP_ACCUMULATE at multiples of
+ * 16 angles give the single-pass result bit for bit.
+ *
+ * Input: "tap planes", a workspace of tf_bp_tc_taps_bytes(plan, n_rows,
+ * n_angles) bytes: a header of per-row exponents e[r], then per angle fp16
+ * planes [hi, lo][row / 8][chan][row % 8] of the feathered filtered taps
+ * scaled by 2^e[r].  Producers: tf_filter_taps (K1 straight from raw counts
+ * or depth) and tf_bp_tc_stage (from filtered natural-layout rows).
+ * Requires voxel_pitch / pixel_pitch <= 2.12 (tf_bp_tc_supported). */
 TF_API int tf_bp_tc_supported(const tf_bp_plan* plan);
-/* Adds the MMA K-steps of every later tf_backproject_tc launch to the device
- * uint64 `counter` (each K-step = 3 MMAs of 128 x 128 x 16); NULL: off. */
-TF_API int tf_bp_tc_count(void* dev_counter);
-/* development: per-CTA wait-cycle counters of the first 1024 tiles (8 int64
- * each) into a device buffer; NULL turns the instrumentation off. */
-TF_API int tf_bp_tc_debug(void* dev_buf);
-TF_API int64_t tf_bp_tc_workspace_bytes(const tf_bp_plan* plan, int n_rows, int a0, int a1);
-TF_API int tf_bp_tc_prepare(const tf_bp_plan* plan, const void* stage, int n_rows, int a0, int a1, double t_bound,
-                            void* ws, void* stream);
-TF_API int tf_bp_tc_absmax(const tf_bp_plan* plan, const void* stage, int n_rows, int a0, int a1, void* ws,
-                           void* stream);
-TF_API int tf_backproject_tc(const tf_bp_plan* plan, const void* ws, int ws_a0, int ws_a1, int n_rows, float* vol,
-                             int a0, int a1, int x0, int x1, int y0, int y1, int flags, void* stream);
+TF_API int64_t tf_bp_tc_taps_bytes(const tf_bp_plan* plan, int n_rows, int n_angles);
+/* Filtered rows [r0, r1) of angles [a0, a1) of an angle-major fp32 sinogram
+ * (row pitch n_chan, angle pitch rows_per_angle * n_chan) -> tap planes (the
+ * workspace's angle 0 = a0).  t_bound > 0: a bound on |T| fixes one exponent
+ * for every row (results independent of the data's range; an undersized
+ * bound saturates the fp16 taps); t_bound <= 0: per-row exponents from the
+ * rows' own max |T w| over [a0, a1). */
+TF_API int tf_bp_tc_stage(const tf_bp_plan* plan, const float* sino, int rows_per_angle, int r0, int r1, int a0,
+                          int a1, double t_bound, void* taps, int64_t taps_bytes, void* stream);
+/* Sets every row's exponent of a tap workspace from the bound t_bound > 0. */
+TF_API int tf_bp_tc_set_exponent(const tf_bp_plan* plan, void* taps, int n_rows, double t_bound, void* stream);
+/* Back-projects angles [a0, a1) of tap planes holding [taps_a0, taps_a1) for
+ * n_rows rows into vol (n_rows, ny, nx), tile and flags as tf_backproject. */
+TF_API int tf_backproject_tc(const tf_bp_plan* plan, const void* taps, int64_t taps_bytes, int taps_a0, int taps_a1,
+                             int n_rows, float* vol, int a0, int a1, int x0, int x1, int y0, int y1, int flags,
+                             void* stream);
+/* Work of one tf_backproject_tc call over n_rows rows and angles [a0, a1)
+ * (host query, synchronous): MMA items (K-steps of 3 fp16 MMAs), voxel x
+ * angle x row updates of the FoV-active tiles (the roofline's executed
+ * updates), and tensor-pipe clocks of the MMAs (items x 3 x N/2). */
+TF_API int tf_bp_tc_work(const tf_bp_plan* plan, int n_rows, int a0, int a1, int64_t* items,
+                         int64_t* executed_updates, int64_t* mma_clocks);
 
 /* ---- quantize (fbp.py:255-259) ------------------------------------------ */
 /* vol is fp32 or fp64 (vol_dtype); arithmetic is fp64, round-half-even,

@@ -56,12 +56,13 @@ SIGNATURES = {
     "tf_bp_finalize": (_i, [_vp, _vp, _i, _vp]),
     "tf_bp_kernel_info": (_i, [_vp, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]),
     "tf_bp_tc_supported": (_i, [_vp]),
-    "tf_bp_tc_debug": (_i, [_vp]),
-    "tf_bp_tc_workspace_bytes": (_i64, [_vp, _i, _i, _i]),
-    "tf_bp_tc_prepare": (_i, [_vp, _vp, _i, _i, _i, _d, _vp, _vp]),
-    "tf_bp_tc_count": (_i, [_vp]),
-    "tf_bp_tc_absmax": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
-    "tf_backproject_tc": (_i, [_vp, _vp, _i, _i, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp]),
+    "tf_bp_tc_taps_bytes": (_i64, [_vp, _i, _i]),
+    "tf_bp_tc_stage": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _d, _vp, _i64, _vp]),
+    "tf_bp_tc_set_exponent": (_i, [_vp, _vp, _i, _d, _vp]),
+    "tf_backproject_tc": (_i, [_vp, _vp, _i64, _i, _i, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp]),
+    "tf_bp_tc_work": (_i, [_vp, _i, _i, _i, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "tf_filter_taps": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _f, _i, _vp]),
+    "tf_filter_tap_bound": (_i, [_vp, _d, ctypes.POINTER(_d)]),
     "tf_quantize": (_i, [_vp, _i, _vp, _i64, _d, _d, _vp]),
     "tf_phantom_sinogram": (_i, [_pg, _i, _i, _i, _i, _d, _d, _vp, _vp]),
     "tf_forward_project": (_i, [_pg, _vp, _vp, _vp]),

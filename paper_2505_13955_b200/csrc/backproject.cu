@@ -36,54 +36,25 @@
 
 #include <cuda_fp16.h>
 
+#include "bp_plan.hpp"
 #include "common.cuh"
-#include "internal.hpp"
-
-constexpr int kNumTileShapes = 6;  // tile shapes with a launch order (kTileShape below)
-
-struct tf_bp_plan {
-    tf_geometry g;
-    int feather_band;
-    double2* d_trig;  // (cos, sin) of k * (span / n_proj), fp64 libm, per angle
-    float* d_w;       // feather weights (fp32, as numpy casts them)
-    double ext;       // max channel extent of a tile's rays over all angles
-    int* d_order[kNumTileShapes];  // launch order of the tiles (Morton, FoV-active first) per tile shape
-    int n_active[kNumTileShapes];
-    double cx, cy, scale, axis, R2, sc2;
-    float angle_wf;
-};
 
 namespace tf {
 namespace {
 
 
 // Consumer layouts.  A thread owns a VX x VY block of voxel columns and ZT of
-// the tile's 32 rows.  NT detector taps per block serve all its voxels:
-//   V1 (1x1, NT=2, ZT=32): the classic two-tap gather, 8 B of smem per update.
-//   V4 (2x2, NT=4, ZT=16): the 2x2 block's rays span < sqrt(2)*scale + 1
-//       channels, so 4 consecutive taps cover all four voxels; each tap row
-//       is read once per block, 4 B of smem per update (half of V1).  The
-//       per-voxel weights are tents sat(1 - |u - j|): exactly {1-f, f} on the
-//       two live taps and 0 elsewhere, so the FMA sequence -- and the result
-//       -- is bit-identical to V1.
-template <int VX, int VY, int NT, int ZT, int STAGES_ = 3, int APS_ = 4, bool PIPE_ = false, int MINB_ = 2,
-          int PW_ = 4, bool ROLE_ = false, int TX_ = 16, int TY_ = 16, bool XR_ = false>
+// the tile's 32 rows; NT detector taps per block serve all its voxels:
+//   V1 (1x1, NT=2, ZT=32): the classic two-tap gather, 8 B of smem per update;
+//   pair (2x1, NT=3, ZT=32, the default): the pair's rays differ by
+//       |cos|*scale <= 1 channel, so 3 taps serve both voxels, 6 B per update,
+//       with each voxel's exact {1-f, f} weights (bit-identical to V1).
+// Other blockings (2x2 / 4 taps, x-runs of 3, a 2x2 "role" kernel) were
+// measured in round 1 (profiles/r01_bp_variants_*.jsonl) and
+// lost to the pair kernel; they are no longer compiled into the library.
+template <int VX, int VY, int NT, int ZT, int STAGES_, int APS_, bool PIPE_, int MINB_, int PW_>
 struct Layout {
-    static constexpr int TX = TX_, TY = TY_;  // voxel columns per CTA tile
-    // ROLE (2x2, 4 taps): per angle the block voxel with the smallest t is
-    // the "base" (its taps are exactly 0,1); its x-, y- and diagonal
-    // neighbours need taps 0..2, 0..2 and 0..3.  Accumulating each voxel only
-    // over its possible taps costs 12 FMA per 4 updates instead of 16, with
-    // exact {1-f, f} weights (bit-identical to the 2-tap kernel).  The voxel
-    // -> role map depends on the signs of cos/sin (warp-uniform per angle).
-    static constexpr bool ROLE = ROLE_;
-    // XR (VX x 1, VX + 1 taps): a run of VX voxels along x; the run's rays
-    // span <= (VX-1)*|cos|*scale <= VX-1 channels, so VX + 1 taps cover it.
-    // The end voxel with the smaller t (by the sign of cos, warp-uniform) is
-    // the base (taps 0,1); the voxel r steps away needs taps 0..r+1.  With
-    // VX = 3: 4 taps / 3 voxels = 5.33 B of smem and 3 FMA per update, exact
-    // {1-f, f} weights (bit-identical to the 2-tap kernel).
-    static constexpr bool XR = XR_;
+    static constexpr int TX = kTileShape[kShapeCuda][0], TY = kTileShape[kShapeCuda][1];  // voxel columns per CTA
     static constexpr int PW = PW_, PH = 8 / PW_;  // one 8-lane LDS.128 phase = PW x PH blocks
     static constexpr int STAGES = STAGES_, APS = APS_, RING = STAGES_ * APS_;  // smem ring of angle slots
     static constexpr bool PIPE = PIPE_;  // software-pipeline the next angle's setup under this angle's FMAs
@@ -97,6 +68,7 @@ struct Layout {
     static constexpr int NTHREADS = NCT + 32;          // + TMA producer warp
     static constexpr int WX = BX / 8;                  // warps across a z-group (8x4 blocks each)
     static_assert(COLS % 32 == 0 && BX % 8 == 0 && BY % 4 == 0, "warp tiling");
+    static_assert(NT == VX * VY + 1 || NT == 2, "V1 or the x-pair kernel");
 };
 
 struct BPArgs {
@@ -132,57 +104,6 @@ __device__ __forceinline__ void fma4(float2& a01, float2& a23, const float4& t, 
     a01 = __ffma2_rn(make_float2(t.x, t.y), make_float2(w, w), a01);
     a23 = __ffma2_rn(make_float2(t.z, t.w), make_float2(w, w), a23);
 }
-
-// Role-kernel inner loop for one angle: voxel (C ^ r) plays role r and only
-// touches taps 0..ntap(r)-1 (see Layout::ROLE).
-__host__ __device__ constexpr int role_taps(int r) { return r == 0 ? 2 : (r == 3 ? 4 : 3); }
-
-template <int C, int ZT>
-__device__ __forceinline__ void accumulate_roles(float (&acc)[4][ZT], const float* p0, const float (&w)[4][4]) {
-#pragma unroll
-    for (int c = 0; c < ZT / 4; ++c) {
-        float4 T[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) T[j] = *reinterpret_cast<const float4*>(p0 + j * kZP + 4 * c);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int v = C ^ r;
-            float2 a01 = make_float2(acc[v][4 * c + 0], acc[v][4 * c + 1]);
-            float2 a23 = make_float2(acc[v][4 * c + 2], acc[v][4 * c + 3]);
-#pragma unroll
-            for (int j = 0; j < role_taps(r); ++j) fma4(a01, a23, T[j], w[r][j]);
-            acc[v][4 * c + 0] = a01.x;
-            acc[v][4 * c + 1] = a01.y;
-            acc[v][4 * c + 2] = a23.x;
-            acc[v][4 * c + 3] = a23.y;
-        }
-    }
-}
-
-template <int C, int VXn, int ZT>
-__device__ __forceinline__ void accumulate_xrun(float (&acc)[VXn][ZT], const float* p0, const float (&w)[VXn][VXn + 1]) {
-#pragma unroll
-    for (int c = 0; c < ZT / 4; ++c) {
-        float4 T[VXn + 1];
-#pragma unroll
-        for (int j = 0; j <= VXn; ++j) T[j] = *reinterpret_cast<const float4*>(p0 + j * kZP + 4 * c);
-#pragma unroll
-        for (int v = 0; v < VXn; ++v) {
-            const int r = C ? VXn - 1 - v : v;  // steps from the base voxel
-            float2 a01 = make_float2(acc[v][4 * c + 0], acc[v][4 * c + 1]);
-            float2 a23 = make_float2(acc[v][4 * c + 2], acc[v][4 * c + 3]);
-#pragma unroll
-            for (int j = 0; j < r + 2; ++j) fma4(a01, a23, T[j], w[v][j]);
-            acc[v][4 * c + 0] = a01.x;
-            acc[v][4 * c + 1] = a01.y;
-            acc[v][4 * c + 2] = a23.x;
-            acc[v][4 * c + 3] = a23.y;
-        }
-    }
-}
-
-template <class L>
-struct Setup;
 
 template <class L, bool RED = false>  // RED: TF_BP_REDUCE epilogue (own instantiation: no register cost elsewhere)
 __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
@@ -315,52 +236,11 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
 
     // per-angle setup: detector coordinates -> tap row + interpolation weights
     const uint8_t* ring_z = ring + zg * ZT * 4;
-    auto setup = [&](int g, const float*& p0, float (&w)[VX * VY][NT], int& cls) {
+    auto setup = [&](int g, const float*& p0, float (&w)[VX * VY][NT]) {
         const int slot = g % L::RING;  // RING need not be a power of 2
         const float4 p = prm[slot];
         const uint8_t* base = ring_z + slot * args.slot_bytes;
-        cls = 0;
-        if constexpr (L::ROLE) {
-            static_assert(VX == 2 && VY == 2 && NT == 4, "role kernel is 2x2 x 4 taps");
-            cls = (p.y < 0.f ? 1 : 0) | (p.z < 0.f ? 2 : 0);  // base voxel index = cls, role r voxel = cls ^ r
-            float t[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int v = cls ^ r;
-                t[r] = fmaxf(fmaf((float)(dy0 + (v >> 1)), p.z, fmaf((float)(dx0 + (v & 1)), p.y, p.x)), 0.f);
-            }
-            const float fb = floorf(t[0]);  // the base voxel has the smallest t (monotone rounding)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const float fl = floorf(t[r]);
-                const float f = t[r] - fl;
-                const float g0 = 1.f - f;
-                const float o = fl - fb;  // 0 (base), 0..1 (x / y neighbour), 0..2 (diagonal)
-                w[r][0] = o == 0.f ? g0 : 0.f;
-                w[r][1] = o == 0.f ? f : (o == 1.f ? g0 : 0.f);
-                w[r][2] = o == 1.f ? f : (o == 2.f ? g0 : 0.f);
-                w[r][3] = o == 2.f ? f : 0.f;
-            }
-            p0 = reinterpret_cast<const float*>(base + (int)fb * kRowBytes);
-        } else if constexpr (L::XR) {
-            static_assert(VY == 1 && NT == VX + 1, "x-run kernel is VX x 1 with VX + 1 taps");
-            cls = p.y < 0.f ? 1 : 0;  // t falls along the run: the last voxel is the base
-            float t[VX];
-#pragma unroll
-            for (int v = 0; v < VX; ++v)
-                t[v] = fmaxf(fmaf((float)dy0, p.z, fmaf((float)(dx0 + v), p.y, p.x)), 0.f);
-            const float fb = floorf(cls ? t[VX - 1] : t[0]);  // smallest t (monotone rounding)
-#pragma unroll
-            for (int v = 0; v < VX; ++v) {
-                const float fl = floorf(t[v]);
-                const float f = t[v] - fl;
-                const float g0 = 1.f - f;
-                const float o = fl - fb;
-#pragma unroll
-                for (int j = 0; j < NT; ++j) w[v][j] = o == (float)j ? g0 : (o == (float)(j - 1) ? f : 0.f);
-            }
-            p0 = reinterpret_cast<const float*>(base + (int)fb * kRowBytes);
-        } else if constexpr (NT == 2) {
+        if constexpr (NT == 2) {
             float t = fmaf((float)dy0, p.z, fmaf((float)dx0, p.y, p.x));
             t = fmaxf(t, 0.f);
             const float fl = floorf(t);
@@ -391,39 +271,9 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
                 w[v][2] = hi ? f : 0.f;
             }
             p0 = reinterpret_cast<const float*>(base + (int)fb * kRowBytes);
-        } else {
-            float t[VX * VY];
-            float tmin = 3.0e38f;
-#pragma unroll
-            for (int v = 0; v < VX * VY; ++v) {
-                t[v] = fmaxf(fmaf((float)(dy0 + v / VX), p.z, fmaf((float)(dx0 + v % VX), p.y, p.x)), 0.f);
-                tmin = fminf(tmin, t[v]);
-            }
-            const float fb = floorf(tmin);
-#pragma unroll
-            for (int v = 0; v < VX * VY; ++v) {
-                const float u = t[v] - fb;  // exact
-#pragma unroll
-                for (int j = 0; j < NT; ++j) w[v][j] = __saturatef(1.f - fabsf(u - (float)j));
-            }
-            p0 = reinterpret_cast<const float*>(base + (int)fb * kRowBytes);
         }
     };
-    auto accumulate = [&](const float* p0, const float (&w)[VX * VY][NT], int cls) {
-        if constexpr (L::XR) {
-            if (cls) accumulate_xrun<1, VX, ZT>(acc, p0, w);  // warp-uniform: sign of cos
-            else accumulate_xrun<0, VX, ZT>(acc, p0, w);
-            return;
-        }
-        if constexpr (L::ROLE) {
-            switch (cls) {  // warp-uniform: depends on the angle only
-                case 0: accumulate_roles<0, ZT>(acc, p0, w); break;
-                case 1: accumulate_roles<1, ZT>(acc, p0, w); break;
-                case 2: accumulate_roles<2, ZT>(acc, p0, w); break;
-                default: accumulate_roles<3, ZT>(acc, p0, w); break;
-            }
-            return;
-        }
+    auto accumulate = [&](const float* p0, const float (&w)[VX * VY][NT]) {
 #pragma unroll
         for (int c = 0; c < ZT / 4; ++c) {
             float4 T[NT];
@@ -456,28 +306,24 @@ __global__ void __launch_bounds__(L::NTHREADS, L::MINB)
             if (g % APS == 0) wait_full(g);
             const float* p0;
             float w[VX * VY][NT];
-            int cls;
-            setup(g, p0, w, cls);
-            accumulate(p0, w, cls);
+            setup(g, p0, w);
+            accumulate(p0, w);
             if (g % APS == APS - 1 || g == n_ang - 1) release(g);
         }
     } else if (n_ang > 0) {
         wait_full(0);
         const float* p0;
         float w[VX * VY][NT];
-        int cls;
-        setup(0, p0, w, cls);
+        setup(0, p0, w);
         for (int g = 0; g < n_ang; ++g) {
             const int gn = g + 1;
             if (gn < n_ang && gn % APS == 0) wait_full(gn);
             const float* q0;
             float wn[VX * VY][NT];
-            int clsn;
-            setup(min(gn, n_ang - 1), q0, wn, clsn);  // independent of this angle's FMAs
-            accumulate(p0, w, cls);
+            setup(min(gn, n_ang - 1), q0, wn);  // independent of this angle's FMAs
+            accumulate(p0, w);
             if (gn % APS == 0 || gn == n_ang) release(g);
             p0 = q0;
-            cls = clsn;
 #pragma unroll
             for (int v = 0; v < VX * VY; ++v)
 #pragma unroll
@@ -586,61 +432,31 @@ __global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ si
     }
 }
 
-typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
-                                      CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
-                                      CUtensorMapFloatOOBfill);
-
-PFN_encodeTiled_t encode_fn() {
-    static PFN_encodeTiled_t fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_encodeTiled_t>(p);
-    }
-    return fn;
-}
-
 template <class L>
 int bp_smem_bytes(int slot_bytes) {
     return L::RING * slot_bytes + L::RING * (int)sizeof(float4) + 2 * L::STAGES * (int)sizeof(uint64_t);
 }
 
 }  // namespace
+
+PFN_encodeTiled_t encode_fn() {
+    static PFN_encodeTiled_t fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<PFN_encodeTiled_t>(p);
+        return (PFN_encodeTiled_t) nullptr;
+    }();
+    return fn;
+}
 }  // namespace tf
 
 namespace tf {
 namespace {
-// kernel configurations (VX, VY, taps, rows/thread, stages, angles/stage, pipelined setup, min CTAs/SM)
-using V1Cfg = Layout<1, 1, 2, 32, 4, 4, false, 2>;
-using V4Cfg1 = Layout<2, 2, 4, 16, 4, 4, false, 3>;
-using V4Cfg2 = Layout<2, 2, 4, 16, 8, 2, false, 3>;
-using V4Cfg3 = Layout<2, 2, 4, 16, 8, 2, true, 3>;
-using V4Cfg4 = Layout<2, 2, 4, 16, 8, 2, true, 2>;
-using P3Cfg5 = Layout<2, 1, 3, 32, 4, 4, false, 3, 2>;
-using P3Cfg6 = Layout<2, 1, 3, 32, 8, 2, true, 3, 2>;
-using P3Cfg7 = Layout<2, 1, 3, 32, 8, 2, false, 3, 2>;
-using Q4Cfg8 = Layout<2, 2, 4, 16, 8, 2, true, 3, 2, true>;
-using Q4Cfg9 = Layout<2, 2, 4, 16, 8, 2, false, 3, 2, true>;
-// 2x2 role kernel with a full 32-row column per thread (128 accumulators) on
-// a 32x16 tile: setup amortised over 128 updates, 4 B smem + 3 FMA per update
-using Q4Cfg10 = Layout<2, 2, 4, 32, 8, 2, true, 2, 2, true, 32, 16>;
-// x-run of 3 voxels, 4 taps, 16 rows per thread, 24x16 tiles (5.33 B/update)
-using X3Cfg11 = Layout<3, 1, 4, 16, 8, 2, false, 2, 2, false, 24, 16, true>;
-using X3Cfg12 = Layout<3, 1, 4, 16, 8, 2, true, 2, 2, false, 24, 16, true>;
-using X3Cfg13 = Layout<3, 1, 4, 16, 8, 2, false, 3, 2, false, 24, 8, true>;
-using X3Cfg14 = Layout<3, 1, 4, 16, 8, 2, true, 3, 2, false, 24, 8, true>;
-
-int default_variant() {
-    static int v = [] {
-        const char* e = getenv("TF_BP_VARIANT");  // benchmarking knob: 1..4
-        int x = e ? atoi(e) : 0;
-        return (x >= 1 && x <= 14) ? x : 6;
-    }();
-    return v;
-}
+// kernel configurations (VX, VY, taps, rows/thread, stages, angles/stage, pipelined setup, min CTAs/SM, phase width)
+using V1Cfg = Layout<1, 1, 2, 32, 4, 4, false, 2, 4>;
+using PairCfg = Layout<2, 1, 3, 32, 8, 2, true, 3, 2>;
 
 bool tile_order_enabled() {
     static int v = [] {
@@ -650,27 +466,11 @@ bool tile_order_enabled() {
     return v != 0;
 }
 
-// tile shapes (TX, TY) with a launch order each; variant -> shape
-constexpr int kNumShapes = kNumTileShapes;
-// shape 4 (11 x 11 = 121 voxels in the MMA's M = 128 rows) is the tensor-core kernel's tile (backproject_tc below)
-constexpr int kTileShape[kNumShapes][2] = {{16, 16}, {32, 16}, {24, 16}, {24, 8}, {11, 11}, {11, 10}};
-int variant_shape(int v) { return v == 10 ? 1 : (v >= 13 ? 3 : (v >= 11 ? 2 : 0)); }
+// the x-pair kernel needs |cos| * scale <= 1 (3 taps per pair); V1 otherwise or on request
+bool use_v1(const tf_bp_plan* p, int flags) { return (flags & TF_BP_KERNEL_V1) || p->scale > 1.0; }
 
-// smem bytes gathered per update: 16 B per LDS.128 of 4 rows, taps / voxels
-double bytes_per_update(int v) {
-    if (v == 0) return 8.0;
-    if (v >= 5 && v <= 7) return 6.0;
-    if (v >= 11) return 16.0 / 3.0;
-    return 4.0;
-}
-
-int select_variant(const tf_bp_plan* p, int flags) {
-    int variant = (flags & TF_BP_KERNEL_V1) ? 0 : ((flags & TF_BP_REDUCE) ? 6 : default_variant());
-    if (((variant >= 5 && variant <= 7) || variant >= 11) && p->scale > 1.0)
-        variant = 0;  // x-runs need |cos|*scale <= 1 (VX + 1 taps)
-    if (variant >= 1 && p->scale > 1.4) variant = 0;  // 2x2 blocks need sqrt(2)*scale < 2 (4 taps)
-    return variant;
-}
+// smem bytes gathered per update: 16 B per LDS.128 of 4 rows x taps / voxels
+double bytes_per_update(bool v1) { return v1 ? 8.0 : 6.0; }
 
 template <class L, bool RED = false>
 int launch_bp(const CUtensorMap& map, const BPArgs& a, dim3 grid, void* stream) {
@@ -731,8 +531,8 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     p->feather_band = feather_band;
     p->scale = g->voxel_pitch / g->pixel_pitch;
     // window: max over angles of a 16x16 tile's channel extent + taps + floor slack
-    p->ext = std::sqrt(15.0 * 15.0 * 2) * p->scale;
-    if (bp_smem_bytes<V1Cfg>((kRowBytes * (int)std::ceil(p->ext + 3.0) + 127) / 128 * 128) > 227 * 1024) {
+    const double ext = std::sqrt(15.0 * 15.0 * 2) * p->scale;
+    if (bp_smem_bytes<V1Cfg>((kRowBytes * (int)std::ceil(ext + 3.0) + 127) / 128 * 128) > 227 * 1024) {
         delete p;
         return set_error(TF_ERR_UNSUPPORTED, "voxel/pixel pitch ratio %.3g too large for the tile window",
                          p->scale);
@@ -748,8 +548,8 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     p->angle_wf = (float)step;
     // tile launch order per tile shape: FoV-active tiles (same fp64 test as
     // the kernel's early-out) in Morton order, then the inactive ones
-    std::vector<int> orders[kNumShapes];
-    for (int shape = 0; shape < kNumShapes; ++shape) {
+    std::vector<int> orders[kNumTileShapes];
+    for (int shape = 0; shape < kNumTileShapes; ++shape) {
         const int TXs = kTileShape[shape][0], TYs = kTileShape[shape][1];
         const int ntx = (g->nx + TXs - 1) / TXs, nty = (g->ny + TYs - 1) / TYs;
         std::vector<int> act, inact;
@@ -788,7 +588,7 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     std::vector<float> wf(g->n_chan);
     for (int i = 0; i < g->n_chan; ++i) wf[i] = (float)w[i];
     cudaError_t e = cudaMalloc(&p->d_trig, sizeof(double2) * g->n_proj);
-    for (int s = 0; s < kNumShapes && e == cudaSuccess; ++s) {
+    for (int s = 0; s < kNumTileShapes && e == cudaSuccess; ++s) {
         e = cudaMalloc(&p->d_order[s], sizeof(int) * orders[s].size());
         if (e == cudaSuccess)
             e = cudaMemcpy(p->d_order[s], orders[s].data(), sizeof(int) * orders[s].size(), cudaMemcpyHostToDevice);
@@ -809,7 +609,7 @@ extern "C" int tf_bp_plan_destroy(tf_bp_plan* p) {
     if (!p) return TF_OK;
     cudaFree(p->d_trig);
     cudaFree(p->d_w);
-    for (int s = 0; s < kNumShapes; ++s) cudaFree(p->d_order[s]);
+    for (int s = 0; s < kNumTileShapes; ++s) cudaFree(p->d_order[s]);
     delete p;
     return TF_OK;
 }
@@ -858,13 +658,13 @@ int backproject_impl(const tf_bp_plan* p, const void* stage, int n_rows, float* 
     const int nzb = (n_rows + kZB - 1) / kZB;
     if (a0 == a1 && !(flags & TF_BP_FINALIZE)) return TF_OK;
 
-    // kernel variant: the 2x2-block 4-tap gather needs the block's rays to span
-    // < 2 channels (sqrt(2) * voxel/pixel pitch ratio); else the 2-tap kernel
-    const int variant = select_variant(p, flags);
-    const int shape = variant_shape(variant);
+    // kernel: the x-pair gather needs the pair's rays within one channel
+    // (|cos| * voxel/pixel pitch ratio <= 1); else the 2-tap V1
+    const bool v1 = use_v1(p, flags);
+    const int shape = kShapeCuda;
     const int TXv = kTileShape[shape][0], TYv = kTileShape[shape][1];
     const double ext = std::sqrt((double)(TXv - 1) * (TXv - 1) + (double)(TYv - 1) * (TYv - 1)) * p->scale;
-    const int W = (int)std::ceil(ext + (variant == 0 ? 3.0 : 4.0));
+    const int W = (int)std::ceil(ext + (v1 ? 3.0 : 4.0));
 
     PFN_encodeTiled_t enc = encode_fn();
     if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
@@ -913,28 +713,10 @@ int backproject_impl(const tf_bp_plan* p, const void* stage, int n_rows, float* 
     const int nty = (g.ny + TYv - 1) / TYv;
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)nzb);
     int st;
-    if (flags & TF_BP_REDUCE) {  // reduce epilogue: the default pair kernel, or V1 (select_variant maps others)
-        st = variant == 0 ? launch_bp<V1Cfg, true>(map, a, grid, stream) : launch_bp<P3Cfg6, true>(map, a, grid, stream);
-        if (st) return st;
-        return check_launch("bp_kernel");
-    }
-    switch (variant) {
-        case 0: st = launch_bp<V1Cfg>(map, a, grid, stream); break;
-        case 1: st = launch_bp<V4Cfg1>(map, a, grid, stream); break;
-        case 2: st = launch_bp<V4Cfg2>(map, a, grid, stream); break;
-        case 3: st = launch_bp<V4Cfg3>(map, a, grid, stream); break;
-        case 4: st = launch_bp<V4Cfg4>(map, a, grid, stream); break;
-        case 5: st = launch_bp<P3Cfg5>(map, a, grid, stream); break;
-        case 6: st = launch_bp<P3Cfg6>(map, a, grid, stream); break;
-        case 7: st = launch_bp<P3Cfg7>(map, a, grid, stream); break;
-        case 8: st = launch_bp<Q4Cfg8>(map, a, grid, stream); break;
-        case 9: st = launch_bp<Q4Cfg9>(map, a, grid, stream); break;
-        case 10: st = launch_bp<Q4Cfg10>(map, a, grid, stream); break;
-        case 11: st = launch_bp<X3Cfg11>(map, a, grid, stream); break;
-        case 12: st = launch_bp<X3Cfg12>(map, a, grid, stream); break;
-        case 13: st = launch_bp<X3Cfg13>(map, a, grid, stream); break;
-        default: st = launch_bp<X3Cfg14>(map, a, grid, stream); break;
-    }
+    if (flags & TF_BP_REDUCE)  // reduce epilogue (own instantiations)
+        st = v1 ? launch_bp<V1Cfg, true>(map, a, grid, stream) : launch_bp<PairCfg, true>(map, a, grid, stream);
+    else
+        st = v1 ? launch_bp<V1Cfg>(map, a, grid, stream) : launch_bp<PairCfg>(map, a, grid, stream);
     if (st) return st;
     return check_launch("bp_kernel");
 }
@@ -949,9 +731,8 @@ extern "C" int tf_backproject(const tf_bp_plan* p, const void* stage, int n_rows
 extern "C" int tf_bp_kernel_info(const tf_bp_plan* p, int flags, int n_rows, int a0, int a1, double* bytes,
                                  int64_t* executed_updates) {
     if (!p || !bytes || !executed_updates) return set_error(TF_ERR_INVALID_ARGUMENT, "null argument");
-    const int v = select_variant(p, flags);
-    *bytes = bytes_per_update(v);
-    const int shape = variant_shape(v);
+    *bytes = bytes_per_update(use_v1(p, flags));
+    const int shape = kShapeCuda;
     const int64_t tile_vox = kTileShape[shape][0] * kTileShape[shape][1];
     const int64_t rows = (int64_t)((n_rows + kZB - 1) / kZB) * kZB;
     *executed_updates = (int64_t)p->n_active[shape] * tile_vox * rows * (int64_t)(a1 - a0);
@@ -960,8 +741,7 @@ extern "C" int tf_bp_kernel_info(const tf_bp_plan* p, int flags, int n_rows, int
 
 extern "C" int tf_bp_smem_bytes_per_update(const tf_bp_plan* p, int flags, double* bytes) {
     if (!p || !bytes) return set_error(TF_ERR_INVALID_ARGUMENT, "null argument");
-    const int v = select_variant(p, flags);
-    *bytes = bytes_per_update(v);
+    *bytes = bytes_per_update(use_v1(p, flags));
     return TF_OK;
 }
 
@@ -1013,739 +793,4 @@ extern "C" int tf_backproject_reduce(const tf_bp_plan* p, const void* stage, int
     for (int s = 0; s < n_slabs; ++s) rm.dst[s] = static_cast<float*>(slab_dst[s]);
     return backproject_impl(p, stage, n_rows, nullptr, a0, a1, 0, p->g.nx, 0, p->g.ny,
                             (flags & TF_BP_KERNEL_V1) | TF_BP_REDUCE, stream, &rm, a0);
-}
-
-// ============================================================================
-// K2-TC: back-projection on the 5th-generation tensor cores (tcgen05).
-//
-// For one angle, a tile of 121 voxel columns (11 x 11, padded to the MMA's M = 128) and N detector rows,
-// back-projection is a small GEMM: D[m][z] += sum_k W[m][k] * T[k][z], with
-// T the filtered taps of the tile's channel window [c_lo, c_lo + 32) and W the
-// interpolation matrix -- row m holds voxel m's exact two-tap weights
-// {1 - f, f} at k = floor(t) - c_lo and k + 1, zeros elsewhere (fbp.py:237-245).
-// Summed over all angles, D is the unscaled back-projection.  The tensor core
-// runs at 8192 FLOP/clk/SM (128 x 256 x 16 fp16 MMA in 128 clk, measured,
-// tools/micro/umma_probe.cu), so even at 2 x 32 FLOP per update it outruns the
-// shared-memory gather of the CUDA-core kernel.
-//
-// Precision: fp32 operands are split into fp16 pairs (hi + lo, 22 significant
-// bits) and D accumulates W_hi T_hi + W_lo T_hi + W_hi T_lo in fp32 TMEM (the
-// dropped W_lo T_lo term is < 2^-22 relative).  The taps are scaled by a
-// power of two 2^e (from the data's max |T|, computed on the device) so they
-// sit in fp16's normal range; the epilogue multiplies by 2^-e exactly.
-//
-// Roles per CTA (192 threads, one CTA per SM):
-//   warp 0  TMA producer: per angle the fp64 window origin (same operations as
-//           bp_kernel) and two TMA loads (T_hi, T_lo boxes of N rows x 32
-//           channels, MN-major canonical layout) into a 10-stage ring; the OOB
-//           zero fill is the reference's zero guard for off-detector taps.
-//   warp 1  TMEM owner + MMA issuer (one thread): 6 tcgen05.mma per angle
-//           (2 K-steps x 3 split products) into one fp32 accumulator of N
-//           TMEM columns, tcgen05.commit frees the stage.
-//   warps 2-5  one voxel per thread: fp32 t relative to the fp64 window
-//           origin (as bp_kernel), the weights as fp16 hi/lo K-major rows of
-//           the W tile; after the last angle the epilogue: tcgen05.ld of the
-//           voxel's N rows, x 2^-e, FoV mask and angle weight (fbp.py:247-251).
-// ============================================================================
-namespace tf {
-namespace {
-// An 11 x 11 voxel tile (121 of the MMA's M = 128 rows; rows 121-127 carry zero weights).  The
-// tile's channel window is 10 (|cos| + |sin|) + 1 <= 15.2 channels wide, so 97% of the angles need
-// one K-step of 16 channels; a 16 x 8 tile (15 |cos| + 7 |sin|, up to 16.6) needs two for 61%
-// of them: 1.61 -> 1.03 K-steps per angle, 0.68x the MMA work per voxel.
-// Optional "narrow" kernel (TF_TC_NARROW=1), when the geometry guarantees one K-step for every angle
-// (pitch ratio < 1.026): an 11 x 10 tile (10|cos| + 9|sin| + 1 <= 14.5 channels) and 16-column
-// weight slots, so the 128 TMEM weight columns hold 8 slots instead of 4.  It tested whether the
-// weight ring's depth bounds the MMA issue rate (ncu of the 11 x 11 kernel: the weight warps wait on
-// the slot's MMA completion for 48% of the stall samples, tensor pipe 46% busy).  It does not:
-// 8 slots ran 475 clk per angle per SM against 427 for 4 slots (profiles/r01_tc_check_v7_narrow.jsonl),
-// so it is off by default.
-template <bool NW>
-struct TcT {
-    static constexpr int TX = 11, TY = NW ? 10 : 11, MV = TX * TY;  // tile, voxels per CTA
-    static constexpr int SA = NW ? 8 : 4;                           // weight slots (ring depth)
-    static constexpr int SW = NW ? 16 : 32;                         // TMEM columns per slot (hi | lo)
-};
-constexpr int kTcSAmax = 8;
-constexpr int kTcM = 128;  // MMA M (TMEM lanes)
-constexpr int kTcK = 32;                                     // channel window (2 MMA K-steps of 16)
-constexpr int kTcSB = 10;  // tap (TMA) ring depth (smem)
-constexpr int kTcSA = 4;   // weight ring depth of the wide kernel (TMEM columns [384, 512): 32 per stage)
-#ifndef TF_TC_GROUPS
-#define TF_TC_GROUPS 4
-#endif
-constexpr int kTcG = TF_TC_GROUPS;  // weight-producer groups of 4 warps, angle g -> group g % kTcG: each
-                                    // group's per-angle chain (window, weights, tcgen05.st, arrive) is
-                                    // latency-bound, so more groups keep more angles in flight
-static_assert(kTcSA % kTcG == 0 && kTcSAmax % kTcG == 0, "each group owns SA / kTcG weight slots");
-constexpr int kTcThreads = 64 + 128 * kTcG;  // w0 TMA, w1 MMA, then the weight groups
-constexpr int kTcShape = 4;  // kTileShape[4] = {11, 11}, [5] = {11, 10} (narrow)
-constexpr int kTcHeader = 256;                               // workspace header: absmax bits, exponent
-
-struct TCArgs {
-    const double2* trig;
-    const int* order;
-    const int* d_exp;  // power-of-2 exponent of the fp16 tap scale (workspace header)
-    float* vol;
-    int a0, a1, ws_a0, n_rows, nx, ny, n_chan;
-    int x0, x1, y0, y1;
-    int ntx, N, flags;
-    double cx, cy, scale, axis, R2, sc2;
-    float angle_wf;
-    long long* dbg;                // optional per-CTA cycle counters (tools/tc_check.py --dbg)
-    unsigned long long* kcount;    // optional: total MMA K-steps issued (the roofline's FLOP count)
-};
-
-__device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;  // descriptor version (sm_100); SWIZZLE_NONE, base offset 0
-    return d;
-}
-
-__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(idesc), "r"(acc)
-        : "memory");
-}
-
-// A (the weights) from TMEM: lane m = voxel m, column c = fp16 pair (k = 2c, 2c + 1)
-__device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc)
-        : "memory");
-}
-
-__device__ __forceinline__ bool elect_one() {
-    uint32_t pred;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
-        : "=r"(pred));
-    return pred != 0;
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ uint32_t pack_h2(__half lo, __half hi) {
-    return (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
-}
-
-// the tile's channel window for angle k: fp64, same operation order as bp_kernel's producer
-struct TcWin {
-    int c_lo;
-    float F0, B, C;
-};
-template <bool NW>
-__device__ __forceinline__ TcWin tc_window(double dX, double dY, double2 cs, const TCArgs& a) {
-    double t0 = __dadd_rn(__dmul_rn(dX, cs.x), __dmul_rn(dY, cs.y));
-    t0 = __dadd_rn(__dmul_rn(t0, a.scale), a.axis);
-    const double B = cs.x * a.scale, C = cs.y * a.scale;
-    const double tmin = t0 + fmin(0.0, B * (TcT<NW>::TX - 1)) + fmin(0.0, C * (TcT<NW>::TY - 1));
-    TcWin w;
-    w.c_lo = (int)floor(tmin);
-    w.F0 = (float)(t0 - (double)w.c_lo);
-    w.B = (float)B;
-    w.C = (float)C;
-    return w;
-}
-
-__device__ __forceinline__ bool tc_outside_fov(int x, int y, const TCArgs& a) {
-    double dx = __dsub_rn((double)x, a.cx), dy = __dsub_rn((double)y, a.cy);
-    double rr = __dmul_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), a.sc2);
-    return rr > a.R2;
-}
-
-// 32 consecutive angles' windows, one per lane (g0 + lane); read back with tc_bcast
-template <bool NW>
-__device__ __forceinline__ TcWin tc_window_lane(int g0, int n_ang, double dX, double dY, const TCArgs& a) {
-    const int lane = threadIdx.x & 31;
-    const int g = min(g0 + lane, n_ang - 1);
-    return tc_window<NW>(dX, dY, a.trig[a.a0 + g], a);
-}
-// windows of angles g0, g0 + 2, ..., g0 + 62 (one weight group's alternate angles), one per lane
-template <bool NW>
-__device__ __forceinline__ TcWin tc_window_lane2(int g0, int n_ang, double dX, double dY, const TCArgs& a) {
-    const int lane = threadIdx.x & 31;
-    const int g = min(g0 + kTcG * lane, n_ang - 1);
-    return tc_window<NW>(dX, dY, a.trig[a.a0 + g], a);
-}
-__device__ __forceinline__ TcWin tc_bcast(const TcWin& w, int src) {
-    TcWin r;
-    r.c_lo = __shfl_sync(0xffffffffu, w.c_lo, src);
-    r.F0 = __shfl_sync(0xffffffffu, w.F0, src);
-    r.B = __shfl_sync(0xffffffffu, w.B, src);
-    r.C = __shfl_sync(0xffffffffu, w.C, src);
-    return r;
-}
-
-#define TC_LD32(ta, v)                                                                                            \
-    asm volatile(                                                                                                 \
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"  \
-        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                         \
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),          \
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),    \
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),  \
-          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])   \
-        : "r"(ta))
-#define TC_ST32(ta, v)                                                                                            \
-    asm volatile(                                                                                                 \
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"  \
-        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta),                              \
-        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),         \
-        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), \
-        "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]),           \
-        "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])                                     \
-        : "memory")
-
-#define TC_ST16(ta, v)                                                                                            \
-    asm volatile(                                                                                                 \
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
-        ::"r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),      \
-        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])            \
-        : "memory")
-
-#define TC_ST8(ta, v)                                                                                             \
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "r"(v[0]),   \
-                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])                      \
-                 : "memory")
-
-// TMEM columns: two MMA accumulators (ping-pong per block of kTcP angles) and
-// the round-to-nearest master sum, N = 128 columns each.
-constexpr int kTcN = 128;  // rows per CTA (MMA N)
-constexpr int kTcAcol = 3 * kTcN;  // first TMEM column of the weight (A) ring
-constexpr int kTcP = 16;   // angles per accumulator block (the tensor core's fp32 accumulation truncates:
-                           // its bias grows with the count, so blocks are re-added in RN fp32 by threads)
-
-template <bool NW>
-__global__ void __launch_bounds__(kTcThreads, 1) bp_tc_kernel(const __grid_constant__ CUtensorMap map,
-                                                              const __grid_constant__ CUtensorMap map16, const TCArgs a) {
-    using T = TcT<NW>;
-    constexpr int kTcTX = T::TX, kTcTY = T::TY, kTcMV = T::MV, kTcSA = T::SA;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
-    const int tx = tile % a.ntx, ty = tile / a.ntx;
-    const int X0 = tx * kTcTX, Y0 = ty * kTcTY;
-    const int zr0 = blockIdx.y * kTcN;
-    const int xe = min(X0 + kTcTX, a.nx), ye = min(Y0 + kTcTY, a.ny);
-    const int ux0 = max(X0, a.x0), ux1 = min(xe, a.x1);
-    const int uy0 = max(Y0, a.y0), uy1 = min(ye, a.y1);
-    if (ux0 >= ux1 || uy0 >= uy1) return;
-    const size_t plane = (size_t)a.nx * a.ny;
-    {
-        int nxv = (int)fmin(fmax(rint(a.cx), (double)X0), (double)(xe - 1));
-        int nyv = (int)fmin(fmax(rint(a.cy), (double)Y0), (double)(ye - 1));
-        bool all_out = true;
-        for (int ddx = -1; ddx <= 1; ++ddx)
-            for (int ddy = -1; ddy <= 1; ++ddy) {
-                int xx = min(max(nxv + ddx, X0), xe - 1), yy = min(max(nyv + ddy, Y0), ye - 1);
-                all_out = all_out && tc_outside_fov(xx, yy, a);
-            }
-        if (all_out) {
-            if (a.flags & TF_BP_FINALIZE) {
-                const int nz = min(kTcN, a.n_rows - zr0);
-                for (int i = threadIdx.x; i < kTcMV * nz; i += blockDim.x) {
-                    int z = i / kTcMV, r = i % kTcMV;
-                    int x = X0 + (r % kTcTX), y = Y0 + (r / kTcTX);
-                    if (x >= ux0 && x < ux1 && y >= uy0 && y < uy1) a.vol[(size_t)(zr0 + z) * plane + (size_t)y * a.nx + x] = 0.f;
-                }
-            }
-            return;
-        }
-    }
-
-    constexpr uint32_t bbytes = kTcN * kTcK * 2;   // one split of the tap box
-    uint8_t* const bring = smem;                              // [kTcSB][hi, lo] tap boxes
-    uint64_t* full = reinterpret_cast<uint64_t*>(bring + kTcSB * 2 * bbytes);
-    uint64_t* empty = full + kTcSB;
-    uint64_t* afull = empty + kTcSB;
-    uint64_t* accfull = afull + kTcSA;  // [2]: MMA block done -> flush
-    uint64_t* accfree = accfull + 2;        // [2]: flushed -> MMA may overwrite
-    uint64_t* done = accfree + 2;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
-    int* kring = reinterpret_cast<int*>(tslot + 1);  // [kTcSB]: MMA K-steps of the angle in tap slot s
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kTcSB; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        for (int s = 0; s < kTcSA; ++s) {
-            mbar_init(&afull[s], 4);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&accfull[b], 1);
-            mbar_init(&accfree[b], 4);
-        }
-        mbar_init(done, 1);
-        fence_barrier_init();
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                     "n"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tslot;  // columns [0,128) acc0, [128,256) acc1, [256,384) master
-    const int n_ang = a.a1 - a.a0;
-    const int n_blk = (n_ang + kTcP - 1) / kTcP;
-    const double dX = (double)X0 - a.cx, dY = (double)Y0 - a.cy;
-
-    if (warp == 0) {
-        // ---- TMA producer: windows for 32 angles per batch, one per lane
-        if (lane == 0) {
-            tma_prefetch_desc(&map);
-            tma_prefetch_desc(&map16);
-        }
-        for (int g0 = 0; g0 < n_ang; g0 += 32) {
-            const TcWin wl = tc_window_lane<NW>(g0, n_ang, dX, dY, a);
-            // one K-step suffices when every tap of the tile lies in the first 16 channels
-            // (t - c_lo < 15 with a margin for the fp32 t of the weights; the skipped
-            // weights are exact zeros)
-            const float span = wl.F0 + fmaxf(0.f, wl.B * (kTcTX - 1)) + fmaxf(0.f, wl.C * (kTcTY - 1));
-            const int ksl = (NW || span < 14.9f) ? 1 : 2;
-            const int gn = min(32, n_ang - g0);
-            for (int i = 0; i < gn; ++i) {
-                const int c_lo = __shfl_sync(0xffffffffu, wl.c_lo, i);
-                const int nks = __shfl_sync(0xffffffffu, ksl, i);
-                const int g = g0 + i;
-                if (lane == 0) {
-                    const int s = g % kTcSB;
-                    if (g >= kTcSB) mbar_wait(&empty[s], (uint32_t)((g / kTcSB) - 1) & 1u);
-                    uint8_t* st = bring + s * 2 * bbytes;
-                    kring[s] = nks;
-                    // a one-K-step angle loads the 16-channel box only (half the L2 -> smem bytes)
-                    const CUtensorMap* mp = nks > 1 ? &map : &map16;
-                    mbar_arrive_expect_tx(&full[s], nks > 1 ? 2 * bbytes : bbytes);
-                    const int ka = 2 * (a.a0 + g - a.ws_a0);
-                    tma_load_3d(st, mp, &full[s], 8 * c_lo, zr0 / 8, ka);
-                    tma_load_3d(st + bbytes, mp, &full[s], 8 * c_lo, zr0 / 8, ka + 1);
-                }
-                __syncwarp();
-            }
-        }
-    } else if (warp == 1) {
-        // ---- MMA issue: the whole warp runs the loop (waits are warp-uniform) and one elected
-        // lane issues, so the tcgen05 ops are not wrapped in per-thread issue loops
-        if (n_ang > 0) {
-            // D f32, A/B f16, A K-major (TMEM), B MN-major, N = 128, M = 128
-            constexpr uint32_t idesc = (1u << 4) | (1u << 16) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
-            // B: LBO = 128 B between 8-channel chunks, SBO = 32 ch x 16 B between 8-row groups; the
-            // start-address field (bits 0-13, addr >> 4) is advanced by adding offsets >> 4
-            const uint64_t db0 = umma_sdesc(smem_u32(smem), 128, kTcK * 16);
-            const uint64_t db16 = umma_sdesc(smem_u32(smem), 128, 16 * 16);  // 16-channel boxes: SBO 256 B
-            long long t_start = a.dbg ? clock64() : 0;
-            long long c_acc = 0, c_full = 0, c_afull = 0;  // wait cycles per barrier (a.dbg only)
-            int ksum = 0;
-            for (int g = 0; g < n_ang; ++g) {
-                const int sb = g % kTcSB, sa = g % kTcSA;
-                const int blk = g / kTcP, b = blk & 1;
-                const bool first = (g % kTcP) == 0;
-                const long long w0 = a.dbg ? clock64() : 0;
-                if (first && blk >= 2) mbar_wait(&accfree[b], (uint32_t)((blk / 2) - 1) & 1u);
-                const long long w1 = a.dbg ? clock64() : 0;
-                mbar_wait(&full[sb], (uint32_t)(g / kTcSB) & 1u);
-                const long long w2 = a.dbg ? clock64() : 0;
-                mbar_wait(&afull[sa], (uint32_t)(g / kTcSA) & 1u);
-                if (a.dbg) {
-                    const long long w3 = clock64();
-                    c_acc += w1 - w0;
-                    c_full += w2 - w1;
-                    c_afull += w3 - w2;
-                }
-                tc_fence_after();
-                const int nks = kring[sb];
-                ksum += nks;
-                if (elect_one()) {
-                    const uint64_t dbh = (nks > 1 ? db0 : db16) + (uint64_t)((sb * 2 * bbytes) >> 4),
-                                   dbl = dbh + (bbytes >> 4);
-                    const uint32_t ah = tmem + (uint32_t)(kTcAcol + sa * T::SW), al = ah + T::SW / 2;  // TMEM weights
-                    const uint32_t td = tmem + (uint32_t)(b * kTcN);
-                    umma_f16_ts(td, ah, dbh, idesc, first ? 0u : 1u);
-                    umma_f16_ts(td, al, dbh, idesc, 1u);
-                    umma_f16_ts(td, ah, dbl, idesc, 1u);
-                    if (nks > 1) {  // channels 16..31: +16 ch x 16 B = 256 B
-                        umma_f16_ts(td, ah + 8, dbh + 16, idesc, 1u);
-                        umma_f16_ts(td, al + 8, dbh + 16, idesc, 1u);
-                        umma_f16_ts(td, ah + 8, dbl + 16, idesc, 1u);
-                    }
-                    umma_commit(&empty[sb]);  // frees tap slot sb and weight slot sa (one commit per angle)
-                    if (g % kTcP == kTcP - 1 || g == n_ang - 1) umma_commit(&accfull[b]);
-                }
-                __syncwarp();
-            }
-            if (a.dbg && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) {
-                a.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
-                a.dbg[blockIdx.x * 8 + 4] = c_acc;
-                a.dbg[blockIdx.x * 8 + 5] = c_full;
-                a.dbg[blockIdx.x * 8 + 6] = c_afull;
-            }
-            if (a.kcount && lane == 0) atomicAdd(a.kcount, (unsigned long long)ksum);
-        }
-    } else {
-        // ---- weight producers: two groups of 4 warps take alternate angles (one voxel per
-        // thread; TMEM lane quadrant = warp % 4); group 0 also does the RN flush and the epilogue
-        const int grp = (warp - 2) >> 2;  // group grp owns the weight slots s with s % kTcG == grp
-        const int q = warp & 3;
-        const int m = q * 32 + lane;
-        const bool real = m < kTcMV;  // rows kTcMV..127 of the MMA: zero weights, no output
-        const int vx = m % kTcTX, vy = m / kTcTX;
-        const float fdx = (float)vx, fdy = (float)vy;
-        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);  // this warp's TMEM lanes
-        auto flush = [&](int blk) {  // master (+)= acc[blk & 1], round to nearest
-            const int b = blk & 1;
-            mbar_wait(&accfull[b], (uint32_t)(blk / 2) & 1u);
-            tc_fence_after();
-#pragma unroll 1
-            for (int c = 0; c < kTcN; c += 32) {
-                uint32_t v[32], u[32];
-                TC_LD32(tl + (uint32_t)(b * kTcN + c), v);
-                if (blk > 0) TC_LD32(tl + (uint32_t)(2 * kTcN + c), u);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (blk > 0) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__fadd_rn(__uint_as_float(u[j]), __uint_as_float(v[j])));
-                }
-                TC_ST32(tl + (uint32_t)(2 * kTcN + c), v);
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&accfree[b]);
-        };
-        int flushed = 0;
-        const long long t_w0 = a.dbg ? clock64() : 0;
-        long long c_wempty = 0;  // this warp's wait cycles on weight-slot reuse (a.dbg only)
-        for (int g0 = grp; g0 < n_ang; g0 += 32 * kTcG) {
-            const TcWin wl = tc_window_lane2<NW>(g0, n_ang, dX, dY, a);
-            for (int i = 0; i < 32; ++i) {
-                const int g = g0 + kTcG * i;
-                if (g >= n_ang) break;
-                const TcWin w = tc_bcast(wl, i);
-                const int s = g % kTcSA;
-                // weight slot s was last used by angle g - kTcSA: wait for its MMAs (the tap
-                // ring's empty barrier of that angle; the MMA thread commits one per angle)
-                const long long we0 = a.dbg ? clock64() : 0;
-                if (g >= kTcSA) mbar_wait(&empty[(g - kTcSA) % kTcSB], (uint32_t)((g - kTcSA) / kTcSB) & 1u);
-                if (a.dbg) c_wempty += clock64() - we0;
-                const float t = fmaxf(fmaf(fdy, w.C, fmaf(fdx, w.B, w.F0)), 0.f);
-                const float fl = floorf(t);
-                const float f = t - fl;
-                const float g0w = 1.f - f;
-                const int o = (int)fl;
-                const __half h0 = __float2half_rn(g0w), h1 = __float2half_rn(f);
-                const __half l0 = __float2half_rn(g0w - __half2float(h0)), l1 = __float2half_rn(f - __half2float(h1));
-                const __half z = __ushort_as_half(0);
-                const bool odd = o & 1;
-                const int jo = real ? o >> 1 : -8;  // -8: no column holds a weight
-                const uint32_t Xh = odd ? pack_h2(z, h0) : pack_h2(h0, h1), Yh = odd ? pack_h2(h1, z) : 0u;
-                const uint32_t Xl = odd ? pack_h2(z, l0) : pack_h2(l0, l1), Yl = odd ? pack_h2(l1, z) : 0u;
-                uint32_t vh[16], vl[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    vh[j] = j == jo ? Xh : (j == jo + 1 ? Yh : 0u);
-                    vl[j] = j == jo ? Xl : (j == jo + 1 ? Yl : 0u);
-                }
-                const uint32_t ta = tl + (uint32_t)(kTcAcol + s * T::SW);  // this voxel's row of the TMEM A tile
-                // a one-K-step angle (the producer's test, on the same window) reads channels 0-15 only
-                const float span = w.F0 + fmaxf(0.f, w.B * (kTcTX - 1)) + fmaxf(0.f, w.C * (kTcTY - 1));
-                if (NW) {
-                    TC_ST8(ta, vh);
-                    TC_ST8(ta + 8, vl);
-                } else if (span < 14.9f) {
-                    TC_ST8(ta, vh);
-                    TC_ST8(ta + 16, vl);
-                } else {
-                    TC_ST16(ta, vh);
-                    TC_ST16(ta + 16, vl);
-                }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&afull[s]);
-                // flush block j once angle (j+1)P + kTcSA is being produced: its aempty-wait
-                // above proved the MMAs through angle (j+1)P retired, so the accfull wait is
-                // immediate (flushing at (j+1)P instead drained the whole MMA pipeline)
-                if (grp == 0 && g % kTcP == kTcSA && g >= kTcP) flush(flushed++);
-            }
-        }
-        if (a.dbg && warp == 2 && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) {
-            a.dbg[blockIdx.x * 8 + 3] = clock64() - t_w0;
-            a.dbg[blockIdx.x * 8 + 7] = c_wempty;
-        }
-        if (grp == 0) {
-        while (flushed < n_blk - 1) flush(flushed++);  // short last block
-        // ---- epilogue: master + last block -> volume
-        const int x = X0 + vx, y = Y0 + vy;
-        const bool inside = real && x >= ux0 && x < ux1 && y >= uy0 && y < uy1;
-        const bool fin = (a.flags & TF_BP_FINALIZE) != 0, accum = (a.flags & TF_BP_ACCUMULATE) != 0;
-        const bool zero = fin && tc_outside_fov(x, y, a);
-        const float sc = n_ang > 0 ? ldexpf(1.f, -*a.d_exp) : 0.f;
-        const int lb = n_blk - 1;
-        if (n_ang > 0) mbar_wait(&accfull[lb & 1], (uint32_t)(lb / 2) & 1u);
-        tc_fence_after();
-        float* out = a.vol + (size_t)y * a.nx + x;
-        for (int c = 0; c < kTcN; c += 32) {
-            uint32_t v[32], u[32];
-            TC_LD32(tl + (uint32_t)((lb & 1) * kTcN + c), v);
-            TC_LD32(tl + (uint32_t)(2 * kTcN + c), u);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (inside) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int zz = zr0 + c + j;
-                    if (zz < a.n_rows) {
-                        float sum = lb > 0 ? __fadd_rn(__uint_as_float(u[j]), __uint_as_float(v[j])) : __uint_as_float(v[j]);
-                        float val = n_ang > 0 ? sum * sc : 0.f;
-                        float* p = out + (size_t)zz * plane;
-                        if (accum) val += *p;
-                        if (fin) val = zero ? 0.f : val * a.angle_wf;
-                        *p = val;
-                    }
-                }
-            }
-        }
-        }  // grp == 0
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
-}
-
-// |T| max over the staged taps (non-negative floats order as their bit patterns).  Only the
-// n_rows real rows count: the 4 pad floats of each 36-float channel row and the rows past
-// n_rows of a ragged last z-block are never written by K1 (uninitialised memory).
-__global__ void tc_absmax_kernel(const float* __restrict__ st, long long n_items, int nzb, int n_chan, int n_rows,
-                                 unsigned* __restrict__ out) {
-    float mx = 0.f;
-    // item = (angle, z-block, channel, 4-row group): one float4
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_items;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int g = (int)(i & 7);
-        const long long row = i >> 3;  // (angle * nzb + zb) * n_chan + c
-        const int zb = (int)((row / n_chan) % nzb);
-        const int z0 = zb * kZB + 4 * g;
-        if (z0 >= n_rows) continue;
-        const float4 v = *reinterpret_cast<const float4*>(st + row * kZP + 4 * g);
-        const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float a = fabsf(e[j]);
-            if (z0 + j < n_rows && a <= 3.0e38f) mx = fmaxf(mx, a);  // skip inf/nan
-        }
-    }
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(out, __float_as_uint(mx));
-}
-
-// z-blocked fp32 staging [k][zb][c][36] -> fp16 pairs [k][hi,lo][zb*4+g][c][8] scaled by 2^e
-__global__ void tc_convert_kernel(const float* __restrict__ st, __half* __restrict__ ws, const unsigned* __restrict__ hdr,
-                                  int* __restrict__ exp_out, long long n_items, int nzb, int n_chan, int a0,
-                                  float bound) {
-    const float mx = bound > 0.f ? bound : __uint_as_float(hdr[0]);
-    const int e = mx > 0.f ? 14 - ilogbf(mx) : 0;  // max |T| * 2^e in [2^14, 2^15)
-    if (blockIdx.x == 0 && threadIdx.x == 0) *exp_out = e;
-    const float s = ldexpf(1.f, e);
-    const int R8 = nzb * 4;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_items; i += (long long)gridDim.x * blockDim.x) {
-        const int c = (int)(i % n_chan);
-        long long r = i / n_chan;
-        const int g8 = (int)(r % R8);  // 8-row group
-        const long long k = r / R8;    // angle relative to a0
-        const int zb = g8 >> 2, g = g8 & 3;
-        const float* src = st + (((size_t)(a0 + k) * nzb + zb) * n_chan + c) * kZP + 8 * g;
-        const float4 u = *reinterpret_cast<const float4*>(src), v = *reinterpret_cast<const float4*>(src + 4);
-        const float x[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
-        uint32_t hw[4], lw[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float p0 = x[2 * j] * s, p1 = x[2 * j + 1] * s;
-            const __half h0 = __float2half_rn(p0), h1 = __float2half_rn(p1);
-            const __half l0 = __float2half_rn(p0 - __half2float(h0)), l1 = __float2half_rn(p1 - __half2float(h1));
-            hw[j] = pack_h2(h0, h1);
-            lw[j] = pack_h2(l0, l1);
-        }
-        const size_t plane8 = (size_t)R8 * n_chan * 8;  // halves per split per angle
-        __half* dh = ws + (size_t)k * 2 * plane8 + ((size_t)g8 * n_chan + c) * 8;
-        *reinterpret_cast<uint4*>(dh) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(dh + plane8) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-    }
-}
-}  // namespace
-}  // namespace tf
-
-namespace tf {
-namespace {
-long long* g_tc_dbg = nullptr;  // development instrumentation (tf_bp_tc_debug), off by default
-long long* tc_debug_buffer() { return g_tc_dbg; }
-unsigned long long* g_tc_count = nullptr;  // MMA K-step counter (tf_bp_tc_count), off by default
-}  // namespace
-}  // namespace tf
-
-extern "C" int tf_bp_tc_debug(void* buf) {
-    g_tc_dbg = static_cast<long long*>(buf);
-    return TF_OK;
-}
-
-extern "C" int tf_bp_tc_count(void* counter) {
-    g_tc_count = static_cast<unsigned long long*>(counter);
-    return TF_OK;
-}
-
-extern "C" int tf_bp_tc_supported(const tf_bp_plan* p) {
-    // a 16 x 8 tile's rays span <= sqrt(15^2 + 7^2) * scale + 2 taps; the window holds 32
-    return p && p->scale <= 1.5 ? 1 : 0;
-}
-
-extern "C" int64_t tf_bp_tc_workspace_bytes(const tf_bp_plan* p, int n_rows, int a0, int a1) {
-    if (!p || n_rows < 0 || a0 < 0 || a1 < a0) return -1;
-    const int64_t nzb = (n_rows + kZB - 1) / kZB;
-    return kTcHeader + (int64_t)(a1 - a0) * 2 * (nzb * 4) * p->g.n_chan * 8 * 2;
-}
-
-extern "C" int tf_bp_tc_prepare(const tf_bp_plan* p, const void* stage, int n_rows, int a0, int a1, double t_bound,
-                                void* ws, void* stream) {
-    if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null bp plan");
-    if (!tf_bp_tc_supported(p))
-        return set_error(TF_ERR_UNSUPPORTED, "tensor-core back-projection needs voxel/pixel pitch <= 1.5");
-    if (!(0 <= a0 && a0 <= a1 && a1 <= p->g.n_proj) || n_rows < 0)
-        return set_error(TF_ERR_INVALID_ARGUMENT, "invalid rows/angles");
-    if (!stage || !ws) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
-    cudaStream_t s = as_stream(stream);
-    unsigned* hdr = static_cast<unsigned*>(ws);
-    // t_bound < 0: hdr[0] already holds the max |T| bits (tf_bp_tc_absmax, e.g. all-reduced over ranks)
-    if (t_bound >= 0) TF_CUDA_TRY(cudaMemsetAsync(hdr, 0, kTcHeader, s));
-    if (n_rows == 0 || a0 == a1) return TF_OK;
-    const int nzb = (n_rows + kZB - 1) / kZB;
-    const long long per_angle = (long long)nzb * p->g.n_chan * kZP;
-    const float* st = static_cast<const float*>(stage);
-    if (t_bound == 0) {  // t_bound > 0: the caller's bound on |T| fixes the scale
-        tc_absmax_kernel<<<148 * 8, 256, 0, s>>>(st + (size_t)a0 * per_angle,
-                                                 (long long)(a1 - a0) * nzb * p->g.n_chan * 8, nzb, p->g.n_chan,
-                                                 n_rows, hdr);
-        TF_CUDA_TRY(cudaGetLastError());
-    }
-    const long long items = (long long)(a1 - a0) * nzb * 4 * p->g.n_chan;
-    __half* data = reinterpret_cast<__half*>(static_cast<uint8_t*>(ws) + kTcHeader);
-    tc_convert_kernel<<<148 * 16, 256, 0, s>>>(st, data, hdr, reinterpret_cast<int*>(hdr + 1), items, nzb, p->g.n_chan,
-                                               a0, t_bound > 0 ? (float)t_bound : 0.f);
-    return check_launch("tc_convert_kernel");
-}
-
-extern "C" int tf_bp_tc_absmax(const tf_bp_plan* p, const void* stage, int n_rows, int a0, int a1, void* ws,
-                               void* stream) {
-    if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null bp plan");
-    if (!(0 <= a0 && a0 <= a1 && a1 <= p->g.n_proj) || n_rows < 0)
-        return set_error(TF_ERR_INVALID_ARGUMENT, "invalid rows/angles");
-    if (!stage || !ws) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
-    cudaStream_t s = as_stream(stream);
-    unsigned* hdr = static_cast<unsigned*>(ws);
-    TF_CUDA_TRY(cudaMemsetAsync(hdr, 0, kTcHeader, s));
-    if (n_rows == 0 || a0 == a1) return TF_OK;
-    const int nzb = (n_rows + kZB - 1) / kZB;
-    const long long per_angle = (long long)nzb * p->g.n_chan * kZP;
-    tc_absmax_kernel<<<148 * 8, 256, 0, s>>>(static_cast<const float*>(stage) + (size_t)a0 * per_angle,
-                                             (long long)(a1 - a0) * nzb * p->g.n_chan * 8, nzb, p->g.n_chan, n_rows,
-                                             hdr);
-    return check_launch("tc_absmax_kernel");
-}
-
-extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* ws, int ws_a0, int ws_a1, int n_rows, float* vol,
-                                 int a0, int a1, int x0, int x1, int y0, int y1, int flags, void* stream) {
-    if (!p) return set_error(TF_ERR_INVALID_ARGUMENT, "null bp plan");
-    const tf_geometry& g = p->g;
-    if (!tf_bp_tc_supported(p))
-        return set_error(TF_ERR_UNSUPPORTED, "tensor-core back-projection needs voxel/pixel pitch <= 1.5");
-    if (!(ws_a0 <= a0 && a0 <= a1 && a1 <= ws_a1 && 0 <= ws_a0 && ws_a1 <= g.n_proj))
-        return set_error(TF_ERR_INVALID_ARGUMENT, "angle range (%d, %d) outside the prepared (%d, %d)", a0, a1, ws_a0,
-                         ws_a1);
-    if (!(0 <= x0 && x0 <= x1 && x1 <= g.nx && 0 <= y0 && y0 <= y1 && y1 <= g.ny))
-        return set_error(TF_ERR_INVALID_ARGUMENT, "tile (%d, %d, %d, %d) out of bounds", x0, x1, y0, y1);
-    if (n_rows < 0) return set_error(TF_ERR_INVALID_ARGUMENT, "n_rows must be >= 0");
-    if (n_rows == 0 || x0 == x1 || y0 == y1) return TF_OK;
-    if (!ws || !vol) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
-    if (a0 == a1 && !(flags & TF_BP_FINALIZE)) return TF_OK;
-    const int nzb = (n_rows + kZB - 1) / kZB;
-    const int R8 = nzb * 4;
-    const int N = kTcN;  // rows per CTA
-
-    PFN_encodeTiled_t enc = encode_fn();
-    if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-    CUtensorMap map;
-    void* data = static_cast<uint8_t*>(const_cast<void*>(ws)) + kTcHeader;
-    // dim 0 = (channel, row-in-group) flattened: a box row is 32 channels x 8 rows = 512 contiguous
-    // bytes (one L2 request of 16 sectors, not 32 requests of 16 B); channel c_lo starts at element 8 c_lo
-    cuuint64_t dims[3] = {(cuuint64_t)8 * g.n_chan, (cuuint64_t)R8, (cuuint64_t)(2 * (ws_a1 - ws_a0))};
-    cuuint64_t strides[2] = {(cuuint64_t)g.n_chan * 16u, (cuuint64_t)R8 * g.n_chan * 16u};
-    cuuint32_t box[3] = {(cuuint32_t)(8 * kTcK), (cuuint32_t)(N / 8), 1u};
-    cuuint32_t estr[3] = {1u, 1u, 1u};
-    CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, data, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
-    CUtensorMap map16;  // the same taps, 16-channel boxes (one-K-step angles)
-    cuuint32_t box16[3] = {(cuuint32_t)(8 * 16), (cuuint32_t)(N / 8), 1u};
-    cr = enc(&map16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, data, dims, strides, box16, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
-
-    // narrow kernel when every angle's window fits one K-step: frac(t_min) + scale (10|cos| + 9|sin|)
-    // < 1 + scale sqrt(181) must stay below the producer's 14.9-channel test (fp32 margin)
-    static const bool narrow_on = [] {
-        const char* e = getenv("TF_TC_NARROW");  // experiment knob: 1 = narrow kernel when it applies
-        return e ? atoi(e) != 0 : false;
-    }();
-    const bool nw = narrow_on && p->scale * std::sqrt(181.0) + 1.0 < 14.8;
-    const int TXs = nw ? TcT<true>::TX : TcT<false>::TX, TYs = nw ? TcT<true>::TY : TcT<false>::TY;
-    TCArgs a{};
-    a.trig = p->d_trig;
-    a.order = tile_order_enabled() ? p->d_order[kTcShape + (nw ? 1 : 0)] : nullptr;
-    a.d_exp = reinterpret_cast<const int*>(static_cast<const uint8_t*>(ws) + 4);
-    a.vol = vol;
-    a.a0 = a0;
-    a.a1 = a1;
-    a.ws_a0 = ws_a0;
-    a.n_rows = n_rows;
-    a.nx = g.nx;
-    a.ny = g.ny;
-    a.n_chan = g.n_chan;
-    a.x0 = x0;
-    a.x1 = x1;
-    a.y0 = y0;
-    a.y1 = y1;
-    a.ntx = (g.nx + TXs - 1) / TXs;
-    a.N = N;
-    a.flags = flags;
-    a.cx = p->cx;
-    a.cy = p->cy;
-    a.scale = p->scale;
-    a.axis = p->axis;
-    a.R2 = p->R2;
-    a.sc2 = p->sc2;
-    a.angle_wf = p->angle_wf;
-    a.dbg = tc_debug_buffer();
-    a.kcount = g_tc_count;
-    const int nty = (g.ny + TYs - 1) / TYs;
-    const int smem = kTcSB * 2 * N * kTcK * 2 + (2 * kTcSB + kTcSAmax + 5) * 8 + 8 + 4 * kTcSB;
-    dim3 grid((unsigned)(a.ntx * nty), (unsigned)((nzb * kZB + N - 1) / N));
-    if (nw) {
-        TF_CUDA_TRY(cudaFuncSetAttribute(bp_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        bp_tc_kernel<true><<<grid, kTcThreads, smem, as_stream(stream)>>>(map, map16, a);
-    } else {
-        TF_CUDA_TRY(cudaFuncSetAttribute(bp_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        bp_tc_kernel<false><<<grid, kTcThreads, smem, as_stream(stream)>>>(map, map16, a);
-    }
-    return check_launch("bp_tc_kernel");
 }

@@ -20,6 +20,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "internal.hpp"
 
@@ -40,6 +42,7 @@ struct tf_filter_plan {
     bool fused;          // fused-I/O FFT path
     int mode;            // 0 generic, 1 fused radix-16, 2 fused radix-8
     int run;             // mode 2: consecutive line pairs per CTA turn (TF_FILTER_RUN)
+    double hsum;         // sum |h_P(d)| of the circular kernel K1 applies (incl. 1 / pitch): |T| <= max|x| hsum
 };
 
 namespace tf {
@@ -355,13 +358,52 @@ __device__ __forceinline__ void fft_fused(float2* buf, const float2* tw0, int P,
 // Where filtered line l = (angle a, row r) goes (tf_filter's slab map and
 // output layout, see include/tomofuse_b200.h).
 struct OutMap {
-    int zblocked;        // 0: [a][r][c] rows; 1: z-blocked staging [a][zb][c][36] (K2 input)
+    int zblocked;        // 0: [a][r][c] rows; 1: z-blocked staging [a][zb][c][36] (K2 input);
+                         // 2: K2-TC tap planes [a][hi, lo][r / 8][c][r % 8] fp16 x 2^e[r] (dst[0])
     int n_slabs;         // >= 1 (1 slab == whole row range)
     int rows_per_angle;
     int32_t row0[9];
     float* dst[8];       // start of each slab's block (may be a peer GPU's buffer over NVLink)
-    const float* w;      // per-channel feather (z-blocked output only), may be null
+    const float* w;      // per-channel feather (z-blocked / tap output only), may be null
+    const int* e;        // tap planes: per-row exponents
+    int R8;              // tap planes: 8-row groups per angle
 };
+
+// Tap-plane destination of line l = (angle a, row r): element offset of (hi plane, channel 0, r % 8)
+// and the row's exact scale 2^e[r]
+__device__ __forceinline__ __half* taps_ptr(long long l, int n, const OutMap& m, float* dst0, float& sc, int& zi) {
+    const long long a = l / m.rows_per_angle;
+    const int r = (int)(l - a * m.rows_per_angle);
+    zi = r & 7;
+    sc = __int_as_float((127 + m.e[r]) << 23);
+    return reinterpret_cast<__half*>(dst0) + (a * 2 * m.R8 + (r >> 3)) * (long long)n * 8 + zi;
+}
+
+__device__ __forceinline__ void split_half(float x, __half& hi, __half& lo) {
+    hi = __float2half_rn(x);
+    lo = __float2half_rn(x - __half2float(hi));
+}
+
+// Feathered (fbp.py:242, f32 product), scaled (exact) and split taps of channel m of a line pair:
+// both rows in one 4-B store per plane when they share an 8-row group (a even row and its successor)
+__device__ __forceinline__ void store_taps(__half* ta, __half* tb, bool has_b, bool pairwise, long long plane8,
+                                           int m, float2 y, float wm, float sa, float sb) {
+    __half ha, la, hb, lb;
+    split_half((y.x * wm) * sa, ha, la);
+    if (pairwise) {
+        split_half((-y.y * wm) * sb, hb, lb);
+        *reinterpret_cast<__half2*>(ta + (size_t)m * 8) = __halves2half2(ha, hb);
+        *reinterpret_cast<__half2*>(ta + plane8 + (size_t)m * 8) = __halves2half2(la, lb);
+        return;
+    }
+    ta[(size_t)m * 8] = ha;
+    ta[plane8 + (size_t)m * 8] = la;
+    if (has_b) {
+        split_half((-y.y * wm) * sb, hb, lb);
+        tb[(size_t)m * 8] = hb;
+        tb[plane8 + (size_t)m * 8] = lb;
+    }
+}
 
 // row0/base are read from a shared-memory copy (dynamic indexing of a
 // kernel-parameter array would spill the struct to local memory)
@@ -428,12 +470,22 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 256 ? 2 : 1)) ramp_filter_kerne
             }
             return make_float2(a, b);
         };
-        int za, zb = 0;
-        float* oa = out_ptr(la, n, map, s_row0, s_dst, za);
-        float* ob = has_b ? out_ptr(la + 1, n, map, s_row0, s_dst, zb) : nullptr;
-        // both rows in one 8-B store when they are z-neighbours of the same block
-        const bool pairwise = map.zblocked && has_b && (ob == oa + 1) && ((za & 1) == 0);
+        int za = 0, zb = 0;
+        float sa = 1.f, sb = 1.f;
+        const bool taps = map.zblocked == 2;
+        float* oa = taps ? nullptr : out_ptr(la, n, map, s_row0, s_dst, za);
+        float* ob = (has_b && !taps) ? out_ptr(la + 1, n, map, s_row0, s_dst, zb) : nullptr;
+        __half* ta = taps ? taps_ptr(la, n, map, s_dst[0], sa, za) : nullptr;
+        __half* tb = (taps && has_b) ? taps_ptr(la + 1, n, map, s_dst[0], sb, zb) : nullptr;
+        const long long plane8 = (long long)map.R8 * n * 8;
+        // both rows in one 8-B (4-B) store when they are z-neighbours of the same block (8-row group)
+        const bool pairwise = taps ? (has_b && tb == ta + 1 && (za & 1) == 0)
+                                   : (map.zblocked && has_b && (ob == oa + 1) && ((za & 1) == 0));
         auto store = [&](int m, float2 y) {
+            if (taps) {
+                store_taps(ta, tb, has_b, pairwise, plane8, m, y, map.w ? __ldg(&map.w[m]) : 1.f, sa, sb);
+                return;
+            }
             if (!map.zblocked) {
                 __stcs(oa + m, y.x);
                 if (has_b) __stcs(ob + m, -y.y);
@@ -714,14 +766,24 @@ __device__ __forceinline__ void r8_pairs(const float* __restrict__ in, long long
         }
         prefetch(pair_of(it + 1) < n_pairs ? pair_of(it + 1) : pair_of(it + kRun - it % kRun));
         // output pointers resolved after the forward half (fewer live registers)
-        int za, zb = 0;
-        float* oa = out_ptr(la, n, map, s_row0, s_dst, za);
-        float* ob = has_b ? out_ptr(la + 1, n, map, s_row0, s_dst, zb) : nullptr;
-        // both rows in one 8-B store when they are z-neighbours of the same block
-        const bool pairwise = map.zblocked && has_b && (ob == oa + 1) && ((za & 1) == 0);
+        int za = 0, zb = 0;
+        float sa = 1.f, sb = 1.f;
+        const bool taps = map.zblocked == 2;
+        float* oa = taps ? nullptr : out_ptr(la, n, map, s_row0, s_dst, za);
+        float* ob = (has_b && !taps) ? out_ptr(la + 1, n, map, s_row0, s_dst, zb) : nullptr;
+        __half* ta = taps ? taps_ptr(la, n, map, s_dst[0], sa, za) : nullptr;
+        __half* tb = (taps && has_b) ? taps_ptr(la + 1, n, map, s_dst[0], sb, zb) : nullptr;
+        const long long plane8 = (long long)map.R8 * n * 8;
+        // both rows in one 8-B (4-B) store when they are z-neighbours of the same block (8-row group)
+        const bool pairwise = taps ? (has_b && tb == ta + 1 && (za & 1) == 0)
+                                   : (map.zblocked && has_b && (ob == oa + 1) && ((za & 1) == 0));
         const float* w = map.w;
         const bool zbl = map.zblocked;
         auto store = [&](int m, float2 y) {
+            if (taps) {
+                store_taps(ta, tb, has_b, pairwise, plane8, m, y, w ? __ldg(&w[m]) : 1.f, sa, sb);
+                return;
+            }
             if (!zbl) {
                 __stcs(oa + m, y.x);
                 if (has_b) __stcs(ob + m, -y.y);
@@ -830,6 +892,16 @@ extern "C" int tf_filter_plan_create(int n_chan, int kind, int64_t padded, doubl
     multiplier_fp64(kind, P, pixel_pitch, mult.data());
     std::vector<float> multf(P / 2 + 1);
     for (int k = 0; k <= P / 2; ++k) multf[k] = (float)(mult[k] / (double)P);
+    {
+        // the spatial kernel K1 applies is h_P = IFFT(multiplier) (real, even): its l1 norm bounds
+        // |filtered| by max|input| (the blur is a normalised non-negative kernel)
+        std::vector<std::complex<double>> X((size_t)P);
+        for (int k = 0; k < P; ++k) X[(size_t)k] = mult[(size_t)(k <= P / 2 ? k : P - k)];
+        fft_pow2(X);
+        double hs = 0;
+        for (int k = 0; k < P; ++k) hs += std::fabs(X[(size_t)k].real()) / (double)P;
+        p->hsum = hs;
+    }
     int rad = 0;
     std::vector<float> bw;
     if (blur_sigma > 0) {  // scipy: radius = int(truncate * sigma + 0.5), truncate 4
@@ -1016,6 +1088,55 @@ extern "C" int tf_filter_peers(const tf_filter_plan* p, const float* in, int64_t
     if (st) return st;
     map.zblocked = 0;  // natural rows: each line one contiguous run (coalesced NVLink stores)
     map.w = nullptr;
+    return launch_filter(p, in, map.dst[0], n_lines, i0, map, stream);
+}
+
+namespace tf {
+namespace {
+// |depth| = |ln i0 - ln max(raw, 1)| <= max(|ln i0|, |ln i0 - ln FLT_MAX|) for finite counts
+double depth_bound(double i0) {
+    const double l = std::log(i0);
+    return std::max(std::fabs(l), std::fabs(l - std::log(3.4028234663852886e38)));
+}
+constexpr double kTapMargin = 1.01;  // fp32 FFT round-off above the exact l1 bound
+}  // namespace
+}  // namespace tf
+
+extern "C" int tf_filter_tap_bound(const tf_filter_plan* p, double i0, double* bound) {
+    if (!p || !bound) return set_error(TF_ERR_INVALID_ARGUMENT, "null argument");
+    if (!(i0 > 0)) return set_error(TF_ERR_INVALID_ARGUMENT, "i0 must be positive, got %g", i0);
+    *bound = depth_bound(i0) * p->hsum * kTapMargin;
+    return TF_OK;
+}
+
+extern "C" int tf_filter_taps(const tf_filter_plan* p, const tf_bp_plan* bp, const float* in, void* taps,
+                              int64_t taps_bytes, int64_t n_lines, float i0, int rows_per_angle, void* stream) {
+    if (!p || !bp) return set_error(TF_ERR_INVALID_ARGUMENT, "null plan");
+    if (n_lines < 0 || rows_per_angle < 1) return set_error(TF_ERR_INVALID_ARGUMENT, "invalid line counts");
+    if (n_lines % rows_per_angle != 0)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "n_lines must be a multiple of rows_per_angle");
+    if (bp_plan_n_chan(bp) != p->n) return set_error(TF_ERR_INVALID_ARGUMENT, "filter/bp plans disagree on n_chan");
+    if (!tf_bp_tc_supported(bp))
+        return set_error(TF_ERR_UNSUPPORTED, "tensor-core tap planes need voxel_pitch / pixel_pitch <= 2.12");
+    if (!in || !taps) return set_error(TF_ERR_INVALID_ARGUMENT, "null buffer");
+    const int n_ang = (int)(n_lines / rows_per_angle);
+    const int64_t need = tf_bp_tc_taps_bytes(bp, rows_per_angle, n_ang);
+    if (taps_bytes < need)
+        return set_error(TF_ERR_INVALID_ARGUMENT, "tap workspace too small: %lld < %lld bytes", (long long)taps_bytes,
+                         (long long)need);
+    cudaStream_t s = as_stream(stream);
+    int st = i0 > 0.f ? tc_uniform_exponents(taps, rows_per_angle, depth_bound(i0) * p->hsum * kTapMargin, s)
+                      : tc_row_exponents(taps, in, rows_per_angle, n_ang, p->n, nullptr, p->hsum * kTapMargin, s);
+    if (st) return st;
+    if (n_lines == 0) return TF_OK;
+    OutMap map{};
+    st = build_map(map, reinterpret_cast<float*>(static_cast<uint8_t*>(taps) + bp_tc_header_bytes(rows_per_angle)),
+                   n_lines, rows_per_angle, 0, nullptr, nullptr);
+    if (st) return st;
+    map.zblocked = 2;
+    map.w = bp_plan_weights(bp);
+    map.e = static_cast<const int*>(taps);
+    map.R8 = (rows_per_angle + 7) / 8;
     return launch_filter(p, in, map.dst[0], n_lines, i0, map, stream);
 }
 

@@ -16,6 +16,11 @@ int set_error(int status, const char* fmt, ...);
 const float* bp_plan_weights(const tf_bp_plan* p);  // device feather weights, nullptr if all ones
 int bp_plan_n_chan(const tf_bp_plan* p);
 int check_launch(const char* what);
+// K2-TC tap-plane workspace (bp_tc.cu), for K1 writing it directly (filter.cu)
+int64_t bp_tc_header_bytes(int n_rows);
+int tc_uniform_exponents(void* taps, int n_rows, double bound, cudaStream_t s);
+int tc_row_exponents(void* taps, const float* lines, int rows_per_angle, int n_ang, int n_chan, const float* w,
+                     double factor, cudaStream_t s);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

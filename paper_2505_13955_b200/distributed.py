@@ -153,9 +153,13 @@ class ZSlabReconstructor:
             else:
                 k = self.r1 - self.r0
                 self.recv = buf[: n_proj * k * n_chan].view(n_proj, k, n_chan)
-        # local slab engine; its staging buffer is the exchange landing zone
+        # local slab engine; for "alltoall" / "p2p-zblocked" its fp32 staging buffer is the exchange
+        # landing zone (CUDA-core K2); "p2p" / "allgather" land natural rows that the owner stages
+        # into tap planes for the tensor-core K2 with the raw-count bound (bitwise K1's own taps)
+        zblocked_landing = exchange_mode in ("alltoall", "p2p-zblocked")
         self.local = SlabReconstructor(params, dims, spec, i0, feather_band, rows=(self.r0, self.r1),
-                                       device=self.device, stage=stage)
+                                       device=self.device, stage=stage,
+                                       tensor=False if zblocked_landing else None)
         if exchange_mode.startswith("p2p"):
             self.send = None
         else:
@@ -227,19 +231,7 @@ class ZSlabReconstructor:
         self.filter(raw_chunk)
         self.exchange()
         self.stage()
-        self.prepare_bp()
-        return self.local.backproject(prepared=True)
-
-    def prepare_bp(self):
-        """Tensor-core K2: every rank scales its fp16 taps by the same 2^e, from
-        max |T| all-reduced over the group (one int32), so the z-slab volume is
-        bitwise the 1-GPU volume's rows."""
-        if self.local.tensor:
-            import torch.distributed as dist
-
-            m = self.local.tc_absmax()
-            dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
-            self.local.prepare_tc(use_max=True)
+        return self.local.backproject()
 
     def updates(self) -> int:
         return self.local.updates()

@@ -37,9 +37,15 @@ def tensor_default() -> bool:
 
 
 class SlabReconstructor:
+    """HBM buffers and kernels of one row slab.  K2 runs on the tensor cores
+    (tap planes written by K1 directly, tf_filter_taps -> tf_backproject_tc)
+    unless `tensor=False` / TF_BP_TENSOR=0 selects the CUDA-core kernel
+    (fp32 z-blocked staging, tf_filter_stage -> tf_backproject)."""
+
     def __init__(self, params: AcquisitionParams, dims: VolumeDims, spec: FilterSpec | None = None,
                  i0: float = 1e5, feather_band: int = 32, rows: tuple[int, int] | None = None,
-                 device=None, in_place_filter: bool = False, stage=None, tensor: bool | None = None):
+                 device=None, in_place_filter: bool = False, stage=None, tensor: bool | None = None,
+                 n_angles: int | None = None):
         import torch
 
         self.torch = torch
@@ -48,32 +54,37 @@ class SlabReconstructor:
         self.i0 = float(i0)
         self.r0, self.r1 = rows if rows is not None else (0, params.n_rows)
         self.k = self.r1 - self.r0
+        self.n_angles = params.n_proj if n_angles is None else int(n_angles)  # angles the taps buffer holds
         self.device = torch.device(device if device is not None else "cuda")
         with torch.cuda.device(self.device):
             self.fplan = filter_plan(params.n_chan, self.spec, params.pixel_pitch)
             self.bplan = bp_plan(params, dims, feather_band)
             self.in_place = in_place_filter
             self._filt = None  # natural-layout filtered rows, only for the unfused path
-            need = self.bplan.stage_bytes(self.k)
-            if stage is not None:  # caller-provided (e.g. NVLink-mapped symmetric memory)
-                stage = stage.view(torch.uint8).view(-1)
-                if stage.numel() < need:
-                    raise ValueError(f"staging buffer too small: {stage.numel()} < {need} bytes")
-                self.stage = stage[:need]
-            else:
-                self.stage = torch.empty(need, dtype=torch.uint8, device=self.device)
-            self.vol = torch.empty((self.k, dims.ny, dims.nx), dtype=torch.float32,
-                                   device=self.device)
-            # K2 variant: tensor cores (fp16 hi/lo split GEMMs per angle, tf_backproject_tc)
-            # or the CUDA-core x-pair gather (tf_backproject)
             sup = bool(lib().tf_bp_tc_supported(self.bplan.handle))
             if tensor and not sup:
-                raise ValueError("tensor-core back-projection needs voxel_pitch / pixel_pitch <= 1.5")
+                raise ValueError("tensor-core back-projection needs voxel_pitch / pixel_pitch <= 2.12")
             self.tensor = sup and (tensor_default() if tensor is None else bool(tensor))
-            self.tc_ws = None
+            self.stage = self.taps = None
             if self.tensor:
-                nb = lib().tf_bp_tc_workspace_bytes(self.bplan.handle, self.k, 0, params.n_proj)
-                self.tc_ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
+                nb = int(lib().tf_bp_tc_taps_bytes(self.bplan.handle, self.k, self.n_angles))
+                if stage is not None:
+                    stage = stage.view(torch.uint8).view(-1)
+                    if stage.numel() < nb:
+                        raise ValueError(f"tap buffer too small: {stage.numel()} < {nb} bytes")
+                    self.taps = stage[:nb]
+                else:
+                    self.taps = torch.empty(nb, dtype=torch.uint8, device=self.device)
+            else:
+                need = self.bplan.stage_bytes(self.k)
+                if stage is not None:  # caller-provided (e.g. NVLink-mapped symmetric memory)
+                    stage = stage.view(torch.uint8).view(-1)
+                    if stage.numel() < need:
+                        raise ValueError(f"staging buffer too small: {stage.numel()} < {need} bytes")
+                    self.stage = stage[:need]
+                else:
+                    self.stage = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self.vol = torch.empty((self.k, dims.ny, dims.nx), dtype=torch.float32, device=self.device)
 
     @property
     def filt(self):
@@ -82,66 +93,70 @@ class SlabReconstructor:
                                           dtype=self.torch.float32, device=self.device)
         return self._filt
 
+    def tap_bound(self, i0=None) -> float:
+        """The |T| bound K1 uses for raw counts (tf_filter_tap_bound): every
+        producer of tap planes from raw counts scales by the same 2^e."""
+        b = ctypes.c_double()
+        check(lib().tf_filter_tap_bound(self.fplan.handle, self.i0 if i0 is None else float(i0), ctypes.byref(b)))
+        return b.value
+
     # -- individual kernels (stream = torch current stream unless given)
     def _s(self, stream):
         st = stream if stream is not None else self.torch.cuda.current_stream(self.device)
         return ctypes.c_void_p(st.cuda_stream)
 
     def filter(self, raw, out=None, stream=None, i0=None):
-        """K1 on raw counts (or depth when i0 <= 0)."""
+        """K1 on raw counts (or depth when i0 <= 0) -> natural-layout fp32 rows."""
         out = out if out is not None else (raw if self.in_place else self.filt)
         n_lines = raw.numel() // self.params.n_chan
         check(lib().tf_filter(self.fplan.handle, _ptr(raw), _ptr(out), n_lines,
                               self.i0 if i0 is None else float(i0), 0, 0, None, None, self._s(stream)))
         return out
 
-    def filter_stage(self, raw, stream=None, i0=None):
-        """Fused K1: raw counts (n_proj, k, n_chan) -> Beer-Lambert -> ramp
-        filter -> feather -> z-blocked staging buffer (no filtered copy)."""
+    def filter_stage(self, raw, stream=None, i0=None, n_rows=None):
+        """Fused K1: raw counts (A, k, n_chan) -> Beer-Lambert -> ramp filter
+        -> feather -> K2's input (tap planes, or z-blocked staging for the
+        CUDA-core kernel), no filtered copy."""
+        k = self.k if n_rows is None else n_rows
         n_lines = raw.numel() // self.params.n_chan
         i0 = self.i0 if i0 is None else float(i0)
-        check(lib().tf_filter_stage(self.fplan.handle, self.bplan.handle, _ptr(raw), _ptr(self.stage), n_lines,
-                                    i0, self.k, 0, None, None, self._s(stream)))
+        if self.tensor:
+            check(lib().tf_filter_taps(self.fplan.handle, self.bplan.handle, _ptr(raw), _ptr(self.taps),
+                                       self.taps.numel(), n_lines, i0, k, self._s(stream)))
+        else:
+            check(lib().tf_filter_stage(self.fplan.handle, self.bplan.handle, _ptr(raw), _ptr(self.stage), n_lines,
+                                        i0, k, 0, None, None, self._s(stream)))
 
-    def stage_rows(self, filt, rows_per_angle=None, r0=0, stream=None):
+    def stage_rows(self, filt, rows_per_angle=None, r0=0, stream=None, a0=0, a1=None, t_bound=None):
+        """Filtered natural rows [r0, r0 + k) of angles [a0, a1) -> K2's input.
+        Tensor path: tap planes scaled from `t_bound` (default: the raw-count
+        bound of this slab's i0, so rows staged after an exchange match K1's
+        own tap planes bit for bit); t_bound <= 0 takes per-row data maxima."""
         rpa = rows_per_angle if rows_per_angle is not None else self.k
+        if self.tensor:
+            a1 = self.params.n_proj if a1 is None else a1
+            tb = self.tap_bound() if t_bound is None else float(t_bound)
+            check(lib().tf_bp_tc_stage(self.bplan.handle, _ptr(filt), rpa, r0, r0 + self.k, a0, a1, tb,
+                                       _ptr(self.taps), self.taps.numel(), self._s(stream)))
+            return
         check(lib().tf_bp_stage(self.bplan.handle, _ptr(filt), rpa, r0, r0 + self.k, _ptr(self.stage),
                                 self._s(stream)))
 
-    def tc_absmax(self, a0=0, a1=None, stream=None):
-        """Tensor path: max |T| of the staged taps into the workspace header and
-        return it as a 1-element int32 device view (float bits; non-negative
-        floats order like ints, so an NCCL MAX all-reduce of it is the global
-        max).  The next prepare_tc(use_max=True) scales by it."""
-        a1 = self.params.n_proj if a1 is None else a1
-        check(lib().tf_bp_tc_absmax(self.bplan.handle, _ptr(self.stage), self.k, a0, a1, _ptr(self.tc_ws),
-                                    self._s(stream)))
-        return self.tc_ws[:4].view(self.torch.int32)
-
-    def prepare_tc(self, a0=0, a1=None, stream=None, n_rows=None, use_max=False):
-        """Tensor path only: staged taps of angles [a0, a1) -> fp16 hi/lo
-        workspace, scaled by 2^e from the data's max |T| (or, with use_max,
-        the max tc_absmax left in the workspace)."""
-        a1 = self.params.n_proj if a1 is None else a1
-        k = self.k if n_rows is None else n_rows
-        check(lib().tf_bp_tc_prepare(self.bplan.handle, _ptr(self.stage), k, a0, a1, -1.0 if use_max else 0.0,
-                                     _ptr(self.tc_ws), self._s(stream)))
-        self._prepared = (a0, a1, k)
-
     def backproject(self, a0=0, a1=None, flags=_lib.TF_BP_FINALIZE, stream=None, vol=None, n_rows=None,
-                    prepared=False):
-        """K2 over angles [a0, a1) of the staged rows (n_rows, default the slab's).
-        On the tensor path it first converts the staged taps (prepare_tc)
-        unless `prepared` says that was just done for the same range."""
+                    taps_a0=0, taps_a1=None):
+        """K2 over angles [a0, a1) of the staged rows (n_rows, default the
+        slab's); the tap planes hold angles [taps_a0, taps_a1)."""
         a1 = self.params.n_proj if a1 is None else a1
         vol = self.vol if vol is None else vol
         k = self.k if n_rows is None else n_rows
-        if self.tensor and not flags & _lib.TF_BP_KERNEL_V1:  # V1 forces the CUDA-core 2-tap kernel
-            if not prepared or getattr(self, "_prepared", None) != (a0, a1, k):
-                self.prepare_tc(a0, a1, stream, k)
-            check(lib().tf_backproject_tc(self.bplan.handle, _ptr(self.tc_ws), a0, a1, k, _ptr(vol), a0, a1,
-                                          0, self.dims.nx, 0, self.dims.ny, flags, self._s(stream)))
+        if self.tensor and not flags & _lib.TF_BP_KERNEL_V1:
+            ta1 = self.n_angles + taps_a0 if taps_a1 is None else taps_a1
+            check(lib().tf_backproject_tc(self.bplan.handle, _ptr(self.taps), self.taps.numel(), taps_a0, ta1, k,
+                                          _ptr(vol), a0, a1, 0, self.dims.nx, 0, self.dims.ny, flags,
+                                          self._s(stream)))
             return vol
+        if self.stage is None:
+            raise ValueError("the CUDA-core kernel needs the fp32 staging buffer (tensor=False)")
         check(lib().tf_backproject(self.bplan.handle, _ptr(self.stage), k, _ptr(vol), a0, a1,
                                    0, self.dims.nx, 0, self.dims.ny, flags, self._s(stream)))
         return vol
@@ -157,10 +172,10 @@ class SlabReconstructor:
         return self.backproject(stream=stream)
 
     def capture(self, raw):
-        """Record run(raw) -- K1 into staging, K2 into self.vol -- as a CUDA
-        graph and return it; `graph.replay()` re-runs the step on whatever
-        `raw` holds then, with one launch from the host.  The library call
-        path allocates nothing, so it is capture-safe."""
+        """Record run(raw) -- K1 into K2's input, K2 into self.vol -- as a
+        CUDA graph and return it; `graph.replay()` re-runs the step on
+        whatever `raw` holds then, with one launch from the host.  The
+        library call path allocates nothing, so it is capture-safe."""
         torch = self.torch
         side = torch.cuda.Stream(self.device)
         side.wait_stream(torch.cuda.current_stream(self.device))
@@ -171,6 +186,22 @@ class SlabReconstructor:
         with torch.cuda.graph(graph):
             self.run(raw)
         return graph
+
+    def bp_work(self, a0=0, a1=None, n_rows=None) -> dict:
+        """What K2 executes for angles [a0, a1): voxel x angle x row updates of
+        the FoV-active tiles, and on the tensor path the MMA items and the
+        tensor-pipe clocks (tf_bp_tc_work / tf_bp_kernel_info)."""
+        a1 = self.params.n_proj if a1 is None else a1
+        k = self.k if n_rows is None else n_rows
+        if self.tensor:
+            it, up, clk = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+            check(lib().tf_bp_tc_work(self.bplan.handle, k, a0, a1, ctypes.byref(it), ctypes.byref(up),
+                                      ctypes.byref(clk)))
+            return {"executed_updates": up.value, "mma_items": it.value, "mma_clocks": clk.value}
+        bpu, exe = ctypes.c_double(), ctypes.c_int64()
+        check(lib().tf_bp_kernel_info(self.bplan.handle, _lib.TF_BP_FINALIZE, k, a0, a1, ctypes.byref(bpu),
+                                      ctypes.byref(exe)))
+        return {"executed_updates": exe.value, "smem_bytes_per_update": bpu.value}
 
     def updates(self) -> int:
         """Voxel x projection updates of one run (pipeline.py:225-227 convention)."""
@@ -302,9 +333,7 @@ class StreamedReconstructor:
             h2d_done.record(self.s_h2d)
             # compute
             self.s_comp.wait_event(h2d_done)
-            check(lib().tf_filter_stage(self.eng.fplan.handle, self.eng.bplan.handle, _ptr(self.raw[b]),
-                                        _ptr(self.eng.stage), p.n_proj * k, self.eng.i0, k, 0, None, None,
-                                        ctypes.c_void_p(self.s_comp.cuda_stream)))
+            self.eng.filter_stage(self.raw[b].view(-1)[: p.n_proj * k * n], stream=self.s_comp, n_rows=k)
             ev = torch.cuda.Event()
             ev.record(self.s_comp)
             raw_free[b] = ev

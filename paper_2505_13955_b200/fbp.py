@@ -249,17 +249,36 @@ def offset_weights(params: AcquisitionParams, band: int = 32) -> np.ndarray:
     return out
 
 
+def _tensor_path(plan) -> bool:
+    """K2 on the tensor cores when the geometry allows it (the default);
+    TF_BP_TENSOR=0 selects the CUDA-core kernel."""
+    import os
+
+    return os.environ.get("TF_BP_TENSOR", "1") != "0" and bool(lib().tf_bp_tc_supported(plan.handle))
+
+
 def _bp_device(src_rows, params, dims, angles, tile, feather_band):
-    """Stage + back-project device rows (n_proj, k, n_chan) -> (k, ny, nx) fp32."""
+    """Stage + back-project device rows (n_proj, k, n_chan) -> (k, ny, nx) fp32.
+    Tensor path: tap planes of angles [a0, a1) with per-row exponents from
+    the rows' own data (row independence, test_fbp.py:180-191)."""
     torch = _torch()
     plan = bp_plan(params, dims, feather_band)
     k = src_rows.shape[1]
-    stage = torch.empty(plan.stage_bytes(k), dtype=torch.uint8, device="cuda")
-    vol = torch.zeros((k, dims.ny, dims.nx), dtype=torch.float32, device="cuda")
+    vol = torch.empty((k, dims.ny, dims.nx), dtype=torch.float32, device="cuda")
+    if (tile[1] - tile[0]) * (tile[3] - tile[2]) < dims.nx * dims.ny:
+        vol.zero_()  # voxels outside the tile are zero (fbp.py:236)
     s = _stream()
-    check(lib().tf_bp_stage(plan.handle, _ptr(src_rows), k, 0, k, _ptr(stage), s))
     a0, a1 = angles
     x0, x1, y0, y1 = tile
+    if _tensor_path(plan):
+        nb = int(lib().tf_bp_tc_taps_bytes(plan.handle, k, a1 - a0))
+        taps = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        check(lib().tf_bp_tc_stage(plan.handle, _ptr(src_rows), k, 0, k, a0, a1, 0.0, _ptr(taps), nb, s))
+        check(lib().tf_backproject_tc(plan.handle, _ptr(taps), nb, a0, a1, k, _ptr(vol), a0, a1, x0, x1, y0, y1,
+                                      _lib.TF_BP_FINALIZE, s))
+        return vol
+    stage = torch.empty(plan.stage_bytes(k), dtype=torch.uint8, device="cuda")
+    check(lib().tf_bp_stage(plan.handle, _ptr(src_rows), k, 0, k, _ptr(stage), s))
     check(lib().tf_backproject(plan.handle, _ptr(stage), k, _ptr(vol), a0, a1, x0, x1, y0, y1,
                                _lib.TF_BP_FINALIZE, s))
     return vol
@@ -328,8 +347,20 @@ def reconstruct(depth_sino, dims: VolumeDims, params: AcquisitionParams, spec: F
             f"({params.n_proj}, {params.n_rows}, {params.n_chan})")
     plan = filter_plan(params.n_chan, spec, params.pixel_pitch)
     src = _device_array(depth_sino, "float32")
+    bplan = bp_plan(params, dims, feather_band)
+    n_lines = src.numel() // params.n_chan
+    if _tensor_path(bplan):
+        # K1 straight into the tap planes (per-row exponents from the depth data), then K2-TC
+        nb = int(lib().tf_bp_tc_taps_bytes(bplan.handle, params.n_rows, params.n_proj))
+        taps = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        vol = torch.empty((params.n_rows, dims.ny, dims.nx), dtype=torch.float32, device="cuda")
+        s = _stream()
+        check(lib().tf_filter_taps(plan.handle, bplan.handle, _ptr(src), _ptr(taps), nb, n_lines, 0.0,
+                                   params.n_rows, s))
+        check(lib().tf_backproject_tc(bplan.handle, _ptr(taps), nb, 0, params.n_proj, params.n_rows, _ptr(vol), 0,
+                                      params.n_proj, 0, dims.nx, 0, dims.ny, _lib.TF_BP_FINALIZE, s))
+        return _finish(vol, tensor_in, dtype)
     filt = torch.empty_like(src)
-    check(lib().tf_filter(plan.handle, _ptr(src), _ptr(filt), src.numel() // params.n_chan, 0.0,
-                          0, 0, None, None, _stream()))
+    check(lib().tf_filter(plan.handle, _ptr(src), _ptr(filt), n_lines, 0.0, 0, 0, None, None, _stream()))
     vol = _bp_device(filt, params, dims, (0, params.n_proj), (0, dims.nx, 0, dims.ny), feather_band)
     return _finish(vol, tensor_in, dtype)
