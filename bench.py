@@ -4,21 +4,22 @@
     python bench.py [--gpus N --steps K --warmup W]            # our sm_100a path
     python bench.py --impl reference ...                        # CPU reference arm
     torchrun --nproc-per-node N bench.py --gpus N ...           # z-slab multi-GPU
+    python bench.py --config c4|c5 [--rows R]                   # slab-streamed (> HBM) configs
 
 A step = one complete reconstruction of the volume: raw counts (resident in
-HBM) -> K1 Beer-Lambert + ramp filter -> [N>1: row-slab exchange, by
-default K1's own stores into the owner GPU over NVLink] -> z-block staging
--> K2 back-projection -> fp32 volume.  `value` is whole-job
-GUPS (voxel x projection updates / s, N_p*N^3 convention of
-pipeline.py:225-227) over the max-over-ranks device time; `e2e` is the same
-through host pinned buffers (H2D of the raw counts + D2H of the volume inside
-every timed step).  Prints ONE JSON line on rank 0.
+HBM) -> K1 Beer-Lambert + ramp filter + feather, written straight into K2's
+fp16 tap planes -> [N>1: row-slab exchange, K1's own stores into the owner
+GPU over NVLink, owner stages its rows] -> K2 back-projection on the tensor
+cores -> fp32 volume.  `value` is whole-job GUPS (voxel x projection updates
+/ s, the N_p*N^3 convention of pipeline.py:225-227) over the max-over-ranks
+device time; `e2e` is the same through the public streaming API with host
+pinned buffers (H2D of the raw counts + D2H of the volume inside every timed
+step).  Prints ONE JSON line on rank 0.
 """
 
 from __future__ import annotations
 
 import argparse
-import ctypes
 import json
 import math
 import os
@@ -30,6 +31,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF = os.path.join(ROOT, "baseline", "_ref")  # the unmodified reference (tools/install_reference.sh)
 
 METRIC = "FDK backprojection GUPS & s/volume at 2048³ (1/2/4/8 B200) vs CPU ref"
 CONFIGS = {
@@ -45,19 +47,20 @@ SM_COUNT = 148
 # per SM per clock, measured: conflict-free LDS.128 over all 148 SMs, each SM timed on its own
 # clock64 (tools/micro/smem_rate.cu -> profiles/r01_smem_rate.jsonl; nominal 128)
 SMEM_BYTES_PER_CLK = 127.69
-TX = TY = 16   # BP tile (csrc/backproject.cu)
-ZB = 32
-
+FP32_FMA_PER_CLK = 128       # per SM
+TC_F16_FLOP_PER_CLK = 8192   # dense fp16 MMA per SM per clock (tools/micro/umma_probe.cu: 128x256x16 in 128 clk)
 
 EXCHANGE_STEP = {
-    "": "K1 Beer-Lambert+ramp+feather -> z-blocked staging -> K2 back-projection",
+    "": "K1 Beer-Lambert+ramp+feather -> fp16 hi/lo tap planes -> K2 tensor-core back-projection",
     "alltoall": "K1 Beer-Lambert+ramp+feather -> z-blocked staging per owner slab -> NCCL row-slab all-to-all "
-                "landing in the owner's staging buffer -> K2 back-projection",
+                "landing in the owner's staging buffer -> K2 (CUDA-core kernel)",
     "p2p": "K1 Beer-Lambert+ramp -> natural rows stored straight into the owner GPU's buffer over NVLink "
-           "(symmetric memory; the all-to-all is K1's store stream) -> owner stages (feather) -> K2",
+           "(symmetric memory; the all-to-all is K1's store stream) -> owner stages its rows into tap planes "
+           "(feather, raw-count bound) -> K2 tensor-core back-projection",
     "p2p-zblocked": "K1 Beer-Lambert+ramp+feather -> z-blocked rows stored straight into the owner's staging "
-                    "buffer over NVLink -> K2",
-    "allgather": "K1 Beer-Lambert+ramp -> NCCL all-gather of natural rows -> owner stages its rows -> K2",
+                    "buffer over NVLink -> K2 (CUDA-core kernel)",
+    "allgather": "K1 Beer-Lambert+ramp -> NCCL all-gather of natural rows -> owner stages its rows into tap "
+                 "planes -> K2 tensor-core back-projection",
 }
 
 
@@ -70,17 +73,18 @@ def parse():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--exchange", default="p2p",
                     choices=["alltoall", "allgather", "p2p", "p2p-zblocked", "angles-p2p", "angles-nccl"])
-    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=None, help="default: --steps")
     ap.add_argument("--slab-rows", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--parity-rows", type=int, default=8, help="full slices checked against the f64 oracle")
     ap.add_argument("--stream", action="store_true",
                     help="z-sub-slab streaming mode (automatic when the per-GPU slab exceeds HBM)")
     ap.add_argument("--rows", type=int, default=None,
-                    help="streaming mode: reconstruct only this many rows per GPU (bounded sample)")
-    ap.add_argument("--cpu-angles", type=int, default=None,
-                    help="angles per CPU-baseline sample (default sized for ~10 s)")
+                    help="streaming mode: reconstruct only this many rows per specimen and GPU (bounded sample)")
+    ap.add_argument("--specimens", type=int, default=2, help="streaming mode: synthetic specimens per batch")
+    ap.add_argument("--cpu-seconds", type=float, default=6.0, help="target CPU seconds per reference sample")
     return ap.parse_args()
 
 
@@ -97,6 +101,13 @@ def workload_desc(cfg):
     n, n_proj = cfg["n"], cfg["n_proj"]
     return (f"{n}^3 volume from {n_proj} parallel-beam projections of {n}x{n}, span pi, "
             f"Ram-Lak, pitch {PITCH:g} um, i0 {I0:g}")
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
 
 
 # ---------------------------------------------------------------- clocks
@@ -149,175 +160,306 @@ class Clocks:
                 "samples": len(sm), "power_w_max": max(power)}
 
 
-# ---------------------------------------------------------------- CPU reference arm
-def _cpu_worker(args):
-    """One process: the reference chain (numpy port, fp32 pipeline path of
-    pipeline.py:176-222) on one detector row and the first `na` angles."""
-    raw_row, n_proj_full, n, na = args
+# ---------------------------------------------------------------- CPU reference (baseline/_ref)
+_SHARED: dict = {}  # set in the parent before the fork: the sample's raw rows and geometry
+
+
+def _ref_import():
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import tomofuse.fbp as RF  # the UNMODIFIED reference package
+    import tomofuse.geometry as RG
+
+    return RF, RG
+
+
+def _ref_worker(job):
+    """One process: the reference chain on its contiguous row slab
+    [r0, r1) of the sample, through the reference's own `rows=` argument:
+    fbp.preprocess -> fbp.ramp_filter (timed) -> fbp.back_project(float32,
+    the pipeline.py:106 dtype) and optionally float64 (the oracle), timed."""
+    r0, r1, do64 = job
     import numpy as np
 
-    from oracle import fbp_oracle as O
-
-    span = math.pi * na / n_proj_full  # same angular positions as the full scan
-    geom = O.make_geom(na, 1, n, pixel_pitch=PITCH, voxel_pitch=PITCH, span=span)
+    RF, _ = _ref_import()
+    raw, params, dims = _SHARED["raw"], _SHARED["params"], _SHARED["dims"]
     t0 = time.perf_counter()
-    depth = O.preprocess(raw_row, I0)
-    filt = O.ramp_filter(depth, pixel_pitch=PITCH).astype(np.float32)
-    O.back_project(filt, geom, dtype=np.float32)
-    return time.perf_counter() - t0
+    depth = RF.preprocess(raw[:, r0:r1], I0)
+    filt = RF.ramp_filter(depth, RF.FilterSpec(), params.pixel_pitch)
+    t1 = time.perf_counter()
+    sino = np.zeros((params.n_proj, params.n_rows, params.n_chan), dtype=np.float32)
+    sino[:, r0:r1] = filt.astype(np.float32)  # pipeline.py:178 astype(float32)
+    t2 = time.perf_counter()
+    RF.back_project(sino, dims, params, rows=(r0, r1), dtype=np.float32)
+    t3 = time.perf_counter()
+    t64 = None
+    if do64:
+        s64 = np.zeros(sino.shape, dtype=np.float64)
+        s64[:, r0:r1] = filt
+        t4 = time.perf_counter()
+        RF.back_project(s64, dims, params, rows=(r0, r1), dtype=np.float64)
+        t64 = time.perf_counter() - t4
+    return t1 - t0, t3 - t2, t64
 
 
-def cpu_reference(cfg, steps, warmup, na=None, raw_rows=None):
-    """Times the reference algorithm (oracle numpy port) on all host cores:
-    one process per core, each a full slice x `na` angles.  Returns
-    (GUPS per step list, info)."""
-    import multiprocessing as mp
-
+def ref_sample(cfg, seconds, rows_per_proc=8):
+    """(cores, angles, rows) of the CPU sample: one contiguous slab of
+    `rows_per_proc` rows per core, spread over the volume, and enough of the
+    scan's first angles for ~`seconds` of float32 back_project per process
+    at ~0.03 GUPS per core."""
     import numpy as np
-
-    from oracle import phantom_cpu
 
     n, n_proj = cfg["n"], cfg["n_proj"]
     cores = os.cpu_count() or 1
-    if na is None:  # ~8-10 s per step at ~0.03 GUPS per core
-        na = max(4, min(n_proj, int(2.5e8 / (n * n))))
-    rows = np.linspace(0, n - 1, cores).astype(int)
-    if raw_rows is None:
-        raw = phantom_cpu.raw_counts(n_proj, n, n, n, n, np.arange(na), rows, pixel_pitch=PITCH,
-                                     voxel_pitch=PITCH, i0=I0)
-    else:
-        raw = raw_rows[:na]
-    jobs = [(raw[:, i:i + 1, :].copy(), n_proj, n, na) for i in range(len(rows))]
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    ctx = mp.get_context("fork")
-    gups = []
-    with ctx.Pool(cores) as pool:
-        pool.map(_cpu_worker, [(j[0][:1], n_proj, n, 1) for j in jobs])  # fork + import warm-up
-        for it in range(warmup + steps):
-            t0 = time.perf_counter()
-            pool.map(_cpu_worker, jobs, chunksize=1)
-            dt = time.perf_counter() - t0
-            if it >= warmup:
-                gups.append(len(jobs) * na * n * n / dt / 1e9)
-    cpu_model = ""
-    try:
-        for line in open("/proc/cpuinfo"):
-            if line.startswith("model name"):
-                cpu_model = line.split(":", 1)[1].strip()
-                break
-    except OSError:
-        pass
-    info = {"cores": cores, "kind": "port",
-            "sample": (f"{len(jobs)} processes x 1 detector row x first {na} of {n_proj} angles x full "
-                       f"{n}x{n} slice (preprocess + ramp_filter + back_project float32, numpy port of "
-                       f"fbp.py in oracle/fbp_oracle.py); rows {rows.tolist()}; CPU {cpu_model}"),
-            "updates_per_step": len(jobs) * na * n * n}
-    return gups, info
+    na = max(1, min(n_proj, int(round(seconds * 0.03e9 / (rows_per_proc * n * n)))))
+    starts = np.linspace(0, n - rows_per_proc, cores).astype(int)
+    rows = np.concatenate([np.arange(s, s + rows_per_proc) for s in starts])
+    return cores, na, rows
+
+
+class CpuReference:
+    """The reference's own CPU path (baseline/_ref tomofuse.fbp) on all host
+    cores: one forked process per core, each a contiguous
+    slab of `rows_per_proc` (>= 8) detector rows through back_project's
+    `rows=` argument, the first `na` angles of the scan (same angular
+    positions), full n x n slices; extrapolated linearly to the volume."""
+
+    def __init__(self, cfg, raw_rows, cores, na, rows_per_proc=8):
+        import multiprocessing as mp
+
+        _, RG = _ref_import()
+        n, n_proj = cfg["n"], cfg["n_proj"]
+        self.cores, self.k, self.na, self.n, self.n_proj = cores, rows_per_proc, na, n, n_proj
+        R = cores * rows_per_proc
+        span = math.pi * na / n_proj  # k * span / na = k * pi / n_proj: the scan's first na angles
+        params = RG.AcquisitionParams(n_proj=na, n_rows=R, n_chan=n, angle_span=span, pixel_pitch=PITCH)
+        dims = RG.VolumeDims(nx=n, ny=n, nz=R, voxel_pitch=PITCH)
+        _SHARED.update(raw=raw_rows, params=params, dims=dims)
+        os.environ.setdefault("OMP_NUM_THREADS", "1")
+        self.pool = mp.get_context("fork").Pool(cores)
+        self.pool.map(_ref_worker, [(0, 1, False)] * cores)  # fork + import warm-up
+        self.cpu_model = ""
+        try:
+            for line in open("/proc/cpuinfo"):
+                if line.startswith("model name"):
+                    self.cpu_model = line.split(":", 1)[1].strip()
+                    break
+        except OSError:
+            pass
+
+    def step(self, do64=False):
+        """One parallel pass over the sample: rates over the pool's wall time."""
+        jobs = [(i * self.k, (i + 1) * self.k, do64) for i in range(self.cores)]
+        t0 = time.perf_counter()
+        res = self.pool.map(_ref_worker, jobs, chunksize=1)
+        wall = time.perf_counter() - t0
+        upd = self.cores * self.k * self.na * self.n * self.n
+        lines = self.cores * self.k * self.na
+        out = {"chain_f32_gups": upd / wall / 1e9, "bp_f32_gups": upd / max(r[1] for r in res) / 1e9,
+               "ramp_filter_msamples_per_s": lines * self.n / max(r[0] for r in res) / 1e6, "wall_s": wall}
+        if do64:
+            out["chain_f32_gups"] = None  # the pass also ran float64
+            out["bp_f64_gups"] = upd / max(r[2] for r in res) / 1e9
+        return out
+
+    def sample_desc(self):
+        return (f"{self.cores} processes x {self.k} contiguous detector rows (rows= of fbp.back_project) x first "
+                f"{self.na} of {self.n_proj} angles x full {self.n}x{self.n} slices: unmodified tomofuse.fbp "
+                f"(baseline/_ref) preprocess -> ramp_filter -> back_project float32 (the pipeline dtype); "
+                f"float64 back_project and ramp_filter timed separately; extrapolated linearly to the volume; "
+                f"CPU {self.cpu_model}")
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
 
 
 def run_reference_arm(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    gups, info = cpu_reference(cfg, args.steps, args.warmup, args.cpu_angles)
-    v = statistics.mean(gups)
+    if not os.path.isdir(os.path.join(REF, "tomofuse")):
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref not installed "
+                                                              "(tools/install_reference.sh)"}))
+        return
+    from oracle import phantom_cpu  # synthetic input for the sample (not the thing timed)
+
     n, n_proj = cfg["n"], cfg["n_proj"]
+    cores, na, rows = ref_sample(cfg, args.cpu_seconds)
+    raw = phantom_cpu.raw_counts(n_proj, n, n, n, n, range(na), rows, pixel_pitch=PITCH, voxel_pitch=PITCH, i0=I0)
+    ref = CpuReference(cfg, raw, cores, na)
+    gups = []
+    for it in range(args.warmup + args.steps):
+        r = ref.step()
+        if it >= args.warmup:
+            gups.append(r["chain_f32_gups"])
+    r64 = ref.step(do64=True)
+    ref.close()
+    v = statistics.mean(gups)
     total = n_proj * n ** 3
+    upd_step = ref.cores * ref.k * ref.na * n * n
     line = {
         "metric": METRIC, "value": round(v, 6), "unit": "GUPS", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(info["updates_per_step"] / (v * 1e9) * 1e3, 3),
+        "warmup": args.warmup, "ms_per_step": round(upd_step / (v * 1e9) * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (analytic 3-D Shepp-Logan raw counts)", "impl": "reference",
         "config": {"workload": workload_desc(cfg), "volume": [n, n, n], "n_proj": n_proj},
         "s_per_volume_extrapolated": round(total / (v * 1e9), 1),
-        "cpu_baseline": {"value": round(v, 6), "unit": "GUPS", "cores": info["cores"], "kind": info["kind"],
-                         "sample": info["sample"]},
+        "cpu_baseline": {"value": round(v, 6), "unit": "GUPS", "cores": ref.cores, "kind": "reference",
+                         "sample": ref.sample_desc(), "rows_per_process": ref.k,
+                         "bp_f32_gups": round(r64["bp_f32_gups"], 6), "bp_f64_gups": round(r64["bp_f64_gups"], 6),
+                         "ramp_filter_msamples_per_s": round(r64["ramp_filter_msamples_per_s"], 2)},
         "e2e": {"value": round(v, 6), "unit": "GUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-# ---------------------------------------------------------------- our arm
-def executed_updates(d, n_proj, k):
-    """Updates the BP kernel really executes: tiles wholly outside the FoV
-    are skipped (same fp64 test as bp_kernel), rows padded to 32."""
+# ---------------------------------------------------------------- roofline of K2
+def roofline(slab, bp_a0, bp_a1, k_rows, bp_ms, sm_mhz, peaks, tag):
+    """executed updates / t over min(R_fp32, R_smem(B)) at the
+    measured SM clock, B = algorithmic shared-memory tap bytes per update.
+    For the tensor-core K2 the tensor pipe's own busy fraction (MMA clocks of
+    the items the kernel issues / SM clocks) is reported beside it."""
+    f = (sm_mhz or 1965.0) * 1e6
+    w = slab.bp_work(bp_a0, bp_a1, k_rows)
+    t = bp_ms / 1e3
+    upd_s = w["executed_updates"] / t
+    r_fp32 = FP32_FMA_PER_CLK / 2 * SM_COUNT * f  # 2 FMA per update
+    tensor = bool(getattr(slab, "tensor", False))
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", f"bp_traffic_{tag}.json")))
+        if tr.get("tensor", False) == tensor:
+            traffic = tr
+    except (OSError, ValueError):
+        pass
+    out = {"bound": "fp32", "unit": "TFLOP/s"}
+    if tensor:
+        nr = 256 if k_rows > 128 else 128
+        tap_bytes = w["mma_items"] * 2 * nr * 16 * 2  # TMA: T_hi + T_lo boxes per item into shared memory
+        B = tap_bytes / w["executed_updates"]
+        mma_flops = w["mma_items"] * 3 * 2 * 128 * nr * 16
+        out["kernel"] = "bp_tc_kernel (K2, tcgen05)"
+        out["tensor_pipe"] = {
+            "frac": round(w["mma_clocks"] / SM_COUNT / f / t, 4), "mma_items_per_launch": w["mma_items"],
+            "mma_clocks_per_launch": w["mma_clocks"],
+            "note": "items x 3 fp16 MMAs of 128 x N x 16 at N/2 clk each (N = rows per CTA), over 148 SMs x the "
+                    "measured clock x K2's time: how busy the tensor pipe is",
+            "mma_tflops_executed": round(mma_flops / t / 1e12, 1),
+            "mma_peak_tflops_at_clock": round(TC_F16_FLOP_PER_CLK * SM_COUNT * f / 1e12, 1),
+            "bf16_tflops_sustained_measured": peaks.get("bf16_tflops_sustained"),
+            "bf16_measured_at_mhz": (peaks.get("clocks_under_load") or {}).get("sm_mhz_median")}
+    else:
+        B = w.get("smem_bytes_per_update") or 6.0
+        out["kernel"] = "bp_kernel (K2, CUDA cores)"
+    r_smem = SMEM_BYTES_PER_CLK * SM_COUNT * f / B
+    roof = min(r_fp32, r_smem)
+    out.update({
+        "achieved": round(upd_s * 4 / 1e12, 3), "peak": round(roof * 4 / 1e12, 3),
+        "frac": round(upd_s / roof, 4),
+        "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+        "traffic_detail": traffic,
+        "peak_source": (f"SURVEY 8(d): min(R_fp32, R_smem(B)) at the measured median SM clock {sm_mhz} MHz; "
+                        f"R_fp32 = 64 updates/clk/SM (2 FMA per update, 128 FMA/clk) x 148 SMs; R_smem = "
+                        f"127.69 B/clk/SM (measured LDS.128 roof, profiles/r01_smem_rate.jsonl) x 148 / B; "
+                        f"TFLOP/s here are 4 x updates/s (fp32-equivalent)"),
+        "algorithmic_smem_bytes_per_update": round(B, 4),
+        "roof_updates_per_s_e9": round(roof / 1e9, 1), "r_fp32_updates_per_s_e9": round(r_fp32 / 1e9, 1),
+        "r_smem_updates_per_s_e9": round(r_smem / 1e9, 1),
+        "executed_updates_per_launch": w["executed_updates"],
+        "executed_updates_note": "voxel x angle x row updates of the FoV-active tiles (out-of-FoV tiles skip the "
+                                 "angle loop), tile voxels clipped to the volume",
+        "bp_ms_per_launch": round(bp_ms, 3),
+        "bp_gups_executed": round(upd_s / 1e9, 1),
+    })
+    return out
+
+
+# ---------------------------------------------------------------- parity
+def parity_rows(n, count, seed=0):
+    """{0, N/2, N-1} + seeded random rows."""
     import numpy as np
 
-    cx, cy = (d.nx - 1) / 2.0, (d.ny - 1) / 2.0
-    R2 = ((d.nx - 1) / 2.0) ** 2  # normal scan, n_chan == nx, scale 1
-    active = 0
-    for ty in range(0, d.ny, TY):
-        for tx in range(0, d.nx, TX):
-            xs = np.arange(tx, min(tx + TX, d.nx))
-            ys = np.arange(ty, min(ty + TY, d.ny))
-            rr = ((xs[None, :] - cx) ** 2 + (ys[:, None] - cy) ** 2)
-            if (rr <= R2).any():
-                active += 1
-    return active * TX * TY * n_proj * (-(-k // ZB) * ZB), active
+    base = sorted({0, n // 2, n - 1})
+    rest = np.setdiff1d(np.arange(n), base)
+    extra = np.random.default_rng(seed).choice(rest, size=min(len(rest), max(0, count - len(base))), replace=False)
+    return sorted(base + [int(r) for r in extra])
 
 
+def parity_check(slab, raw, n_proj, n, count):
+    """Full n x n slices of rows {0, N/2, N-1} + seeded rows vs the float64
+    oracle (the reference chain restated in C, bit-identical to
+    tomofuse.fbp -- tests/test_cpu_host.py) on the same raw counts; the
+    error is split into K1 (our fp32 filtered rows vs the oracle's f64
+    filter) and BP (the f64 oracle back-projection of OUR filtered rows vs
+    our volume) on the first three rows."""
+    import numpy as np
+    import torch
+
+    from oracle import c_oracle as C
+    from oracle import fbp_oracle as O
+
+    rows = parity_rows(n, count)
+    raw_rows = raw[:, rows].cpu().numpy()
+    geom = O.make_geom(n_proj, len(rows), n, pixel_pitch=PITCH, voxel_pitch=PITCH)
+    t0 = time.perf_counter()
+    ref = C.fbp_rows(raw_rows, geom)
+    got = slab.vol[rows].cpu().numpy().astype(np.float64)
+    per = [float(np.linalg.norm(got[i] - ref[i]) / np.linalg.norm(ref[i])) for i in range(len(rows))]
+    out = {"rows": rows, "slices": "full", "tolerance": 1e-5,
+           "rel_l2_vs_f64_oracle": float(np.linalg.norm(got - ref) / np.linalg.norm(ref)),
+           "rel_l2_per_row_max": max(per), "max_abs": float(np.abs(got - ref).max()),
+           "max_abs_over_max_ref": float(np.abs(got - ref).max() / np.abs(ref).max())}
+    sub = rows[:3]
+    fg = slab.filter(raw[:, sub].contiguous(),
+                     out=torch.empty((n_proj, len(sub), n), device=raw.device)).cpu().numpy().astype(np.float64)
+    f64 = C.ramp_filter(C.preprocess(raw_rows[:, :3], I0), "ramlak", PITCH)
+    out["k1_rel_l2"] = float(np.linalg.norm(fg - f64) / np.linalg.norm(f64))
+    g3 = O.make_geom(n_proj, 3, n, pixel_pitch=PITCH, voxel_pitch=PITCH)
+    bp_of_ours = C.back_project(fg, g3)
+    out["bp_rel_l2"] = float(np.linalg.norm(got[:3] - bp_of_ours) / np.linalg.norm(bp_of_ours))
+    out["oracle_s"] = round(time.perf_counter() - t0, 1)
+    return out
+
+
+# ---------------------------------------------------------------- streamed (> HBM) configs
 def run_streamed(args, cfg, world, rank, local, dev):
-    """Volumes larger than (aggregate) HBM -- configs C4/C5: each GPU walks
-    its z-slab in sub-slabs; per sub-slab the raw counts are generated on the
-    device (K4; the host cannot hold a 1.9 TB C5 sinogram), filtered straight
-    into staging (K1), back-projected (K2), quantized (K3) and the uint16
-    slab is copied into a pinned host ring (2 slabs), overlapped on 2 streams."""
-    import ctypes
-
+    """Volumes larger than (aggregate) HBM -- configs C4/C5: a batch of
+    synthetic specimens, each streamed through engine.StreamedReconstructor
+    (the public host-fed API): pinned host raw counts -> H2D per z-sub-slab
+    -> K1 into tap planes -> K2 (tensor cores) -> K3 quantize -> uint16 D2H
+    into a pinned host volume, three streams overlapped.  The raw counts are
+    generated once before timing (K4 on the device, copied to pinned host
+    memory); a bounded sample of rows per specimen and GPU."""
     import torch
     import torch.distributed as dist
 
-    from paper_2505_13955_b200 import _lib
-    from paper_2505_13955_b200._lib import check, lib
-    from paper_2505_13955_b200.engine import SlabReconstructor, phantom_raw
+    from paper_2505_13955_b200.engine import StreamedReconstructor, phantom_raw
     from paper_2505_13955_b200.geometry import split_range
 
     p, d = geometry(cfg)
     n, n_proj = cfg["n"], cfg["n_proj"]
     r0, r1 = split_range(n, world)[rank]
-    if args.rows:
-        r1 = min(r1, r0 + args.rows)
-    S = min(args.slab_rows, r1 - r0)
-    eng = SlabReconstructor(p, d, i0=I0, rows=(0, S), device=dev)
-    raw = torch.empty((n_proj, S, n), dtype=torch.float32, device=dev)
-    q = [torch.empty((S, n, n), dtype=torch.uint16, device=dev) for _ in range(2)]
-    ring = [torch.empty((S, n, n), dtype=torch.uint16, pin_memory=True) for _ in range(2)]
-    s_comp = torch.cuda.current_stream(dev)
-    s_d2h = torch.cuda.Stream(dev)
-    d2h_done = [None, None]
-    bp_events = []
+    rows = min(args.rows or (r1 - r0), r1 - r0)
+    S = min(args.slab_rows, rows)
+    specimens = []
+    tmp = torch.empty((n_proj, S, n), dtype=torch.float32, device=dev)
+    for s in range(args.specimens):
+        # specimen s: the phantom at its own contrast (mu_max) and row band
+        s0 = r0 + (s * 97) % max(1, (r1 - r0) - rows + 1)
+        h = torch.empty((n_proj, rows, n), dtype=torch.float32, pin_memory=True)
+        for q0 in range(0, rows, S):
+            q1 = min(rows, q0 + S)
+            v = tmp[:, : q1 - q0]
+            phantom_raw(p, d, v, r0=s0 + q0, r1=s0 + q1, i0=I0, mu_max=3.5e-4 * (1.0 - 0.1 * s))
+            h[:, q0:q1].copy_(v)
+        specimens.append((s0, h, torch.empty((rows, n, n), dtype=torch.uint16, pin_memory=True)))
+    del tmp
+    st = StreamedReconstructor(p, d, i0=I0, slab_rows=S, device=dev)
 
-    def one_pass(record=False):
-        for i, s0 in enumerate(range(r0, r1, S)):
-            k = min(S, r1 - s0)
-            b = i % 2
-            src = raw.view(-1)[: n_proj * k * n].view(n_proj, k, n)
-            phantom_raw(p, d, src, r0=s0, r1=s0 + k, i0=I0)
-            check(lib().tf_filter_stage(eng.fplan.handle, eng.bplan.handle, ctypes.c_void_p(src.data_ptr()),
-                                        ctypes.c_void_p(eng.stage.data_ptr()), n_proj * k, I0, k, 0, None, None,
-                                        ctypes.c_void_p(s_comp.cuda_stream)))
-            if d2h_done[b] is not None:
-                s_comp.wait_event(d2h_done[b])
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(s_comp)
-            check(lib().tf_backproject(eng.bplan.handle, ctypes.c_void_p(eng.stage.data_ptr()), k,
-                                       ctypes.c_void_p(eng.vol.data_ptr()), 0, n_proj, 0, n, 0, n,
-                                       _lib.TF_BP_FINALIZE, ctypes.c_void_p(s_comp.cuda_stream)))
-            e1.record(s_comp)
-            if record:
-                bp_events.append((e0, e1, k))
-            check(lib().tf_quantize(ctypes.c_void_p(eng.vol.data_ptr()), _lib.TF_F32,
-                                    ctypes.c_void_p(q[b].data_ptr()), k * n * n, 0.0, 4e-4,
-                                    ctypes.c_void_p(s_comp.cuda_stream)))
-            ev = torch.cuda.Event()
-            ev.record(s_comp)
-            s_d2h.wait_event(ev)
-            with torch.cuda.stream(s_d2h):
-                ring[b][:k].copy_(q[b][:k], non_blocking=True)
-            dd = torch.cuda.Event()
-            dd.record(s_d2h)
-            d2h_done[b] = dd
-        s_comp.wait_stream(s_d2h)
+    def one_pass():
+        for s0, h_raw, h_vol in specimens:
+            st.run(h_raw, h_vol, row_range=(s0, s0 + rows), host_row0=s0, quantize=(0.0, 4e-4))
 
     for _ in range(args.warmup):
         one_pass()
@@ -330,7 +472,7 @@ def run_streamed(args, cfg, world, rank, local, dev):
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ea.record()
     for _ in range(args.steps):
-        one_pass(record=True)
+        one_pass()
     eb.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -340,55 +482,42 @@ def run_streamed(args, cfg, world, rank, local, dev):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = t.item()
-    rows_all = (r1 - r0) * world if args.rows else n
-    upd = n_proj * rows_all * n * n
-    bp_ms = sum(e0.elapsed_time(e1) for e0, e1, _ in bp_events)
-    bp_upd = sum(n_proj * k * n * n for _, _, k in bp_events)
+    upd = n_proj * rows * n * n * world * args.specimens
+    s_per_spec = ms / 1e3 / args.specimens * (r1 - r0) / rows  # one specimen's full volume on these GPUs
     if rank == 0:
+        sub = st.sub_slabs(specimens[0][0], specimens[0][0] + rows)
         line = {
             "metric": METRIC, "value": round(upd / (ms / 1e3) / 1e9, 3), "unit": "GUPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
-            "scaling": "strong" if not args.rows else "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (analytic 3-D Shepp-Logan raw counts generated on device per sub-slab)",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (analytic 3-D Shepp-Logan raw counts, one contrast per specimen, in pinned host "
+                    "memory before timing)",
             "config": {"workload": workload_desc(cfg), "volume": [n, n, n], "n_proj": n_proj,
-                       "mode": f"z-sub-slab streaming ({S} rows), uint16 volume D2H into a 2-slab pinned ring",
-                       "rows_per_gpu": r1 - r0, "sample": bool(args.rows),
-                       "s_per_volume_extrapolated": round(ms / 1e3 * n / rows_all, 2)},
-            "roofline": {"bound": "smem", "kernel": "bp_kernel (K2)",
-                         "bp_gups_full_count": round(bp_upd / (bp_ms / 1e3) / 1e9, 1)},
-            "clocks": clk, "gpu_launches": 5 * len(bp_events) // max(1, args.steps) * args.steps,
+                       "mode": (f"batch of {args.specimens} specimens, each {rows} rows per GPU host-streamed in "
+                                f"{S}-row z-sub-slabs (StreamedReconstructor: H2D / K1 taps + K2 tensor cores + "
+                                f"K3 quantize / uint16 D2H on 3 streams)"),
+                       "rows_per_gpu_per_specimen": rows, "sample": rows < (r1 - r0),
+                       "s_per_specimen_volume_extrapolated": round(s_per_spec, 2)},
+            "e2e": {"value": round(upd / (ms / 1e3) / 1e9, 3), "unit": "GUPS",
+                    "h2d_bytes_per_step": sum(h.numel() * 4 for _, h, _ in specimens),
+                    "d2h_bytes_per_step": sum(v.numel() * 2 for _, _, v in specimens),
+                    "path": "host pinned raw counts -> GPU -> host pinned uint16 volume, every step"},
+            "clocks": clk, "gpu_launches": 4 * len(sub) * args.specimens * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------- our arm
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg)
         return
-    if args.stream or cfg["n"] >= 4096 and int(os.environ.get("WORLD_SIZE", "1")) * 180e9 < 2.2 * 4 * cfg["n"] ** 3:
-        import torch
-        import torch.distributed as dist
-
-        os.environ.setdefault("NCCL_DEBUG", "WARN")
-        world = int(os.environ.get("WORLD_SIZE", "1"))
-        rank = int(os.environ.get("RANK", "0"))
-        local = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(local)
-        dev = torch.device("cuda", local)
-        if world > 1:
-            dist.init_process_group("nccl", device_id=dev)
-        run_streamed(args, cfg, world, rank, local, dev)
-        return
-
-    import numpy as np
     import torch
     import torch.distributed as dist
-
-    from paper_2505_13955_b200.engine import SlabReconstructor, phantom_raw
 
     os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -398,11 +527,18 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if args.stream or cfg["n"] >= 4096 and world * 180e9 < 2.2 * 4 * cfg["n"] ** 3:
+        run_streamed(args, cfg, world, rank, local, dev)
+        return
+
+    from paper_2505_13955_b200.engine import SlabReconstructor, StreamedReconstructor, phantom_raw
+    from paper_2505_13955_b200.geometry import split_range
+
+    numa = None
+    if world > 1:
         from paper_2505_13955_b200.hostnuma import bind_to_device
 
         numa = bind_to_device(local)  # pinned e2e buffers on the GPU's node (no-op on 1-node hosts)
-    else:
-        numa = None
     p, d = geometry(cfg)
     n, n_proj = cfg["n"], cfg["n_proj"]
     total_updates = n_proj * n * n * n
@@ -410,8 +546,8 @@ def main():
     # ---- setup: engine + synthetic raw counts generated on the device (K4)
     bp_a0, bp_a1 = 0, n_proj  # angles K2 runs on this rank
     angle_split = world > 1 and args.exchange.startswith("angles-")
-    if world > 1 and args.exchange.startswith("angles-"):
-        # P_proj: angle-split partials reduced onto the z-slab owners
+    if angle_split:
+        # P_proj: angle-split partials reduced onto the z-slab owners (CUDA-core K2 reduce epilogue)
         from paper_2505_13955_b200.distributed import AngleSplitReconstructor
 
         eng = slab = AngleSplitReconstructor(p, d, i0=I0, reduce=args.exchange[len("angles-"):], device=dev)
@@ -419,26 +555,29 @@ def main():
         phantom_raw(p, d, raw, a0=eng.a0, a1=eng.a1)
         k_rows = n
         bp_a0, bp_a1 = eng.a0, eng.a1
+        launches = 3  # K1 -> staging, K2 + reduce epilogue, finalize
 
         def step_parts():
             bp_ev[0].record()
-            eng.run(raw)  # K1, K2 with the reduction in its epilogue (or + NCCL), finalize
+            eng.run(raw)
             bp_ev[1].record()
     elif world > 1:
         from paper_2505_13955_b200.distributed import ZSlabReconstructor
 
         try:
             eng = ZSlabReconstructor(p, d, i0=I0, exchange_mode=args.exchange, device=dev)
-        except Exception as e:  # symmetric memory unavailable: same z-slab path, NCCL all-to-all
+        except Exception as e:  # symmetric memory unavailable: same z-slab path over NCCL all-gather
             if not args.exchange.startswith("p2p"):
                 raise
-            print(f"p2p exchange unavailable ({e}); using alltoall", file=sys.stderr)
-            args.exchange = "alltoall"
+            print(f"p2p exchange unavailable ({e}); using allgather", file=sys.stderr)
+            args.exchange = "allgather"
             eng = ZSlabReconstructor(p, d, i0=I0, exchange_mode=args.exchange, device=dev)
         raw = torch.empty(eng.chunk_shape(), dtype=torch.float32, device=dev)
         phantom_raw(p, d, raw, a0=eng.a0, a1=eng.a1)
         slab = eng.local
         k_rows = eng.r1 - eng.r0
+        # K1, [owner staging: exponent fill + tap staging | nothing], K2
+        launches = {"p2p": 4, "allgather": 4, "alltoall": 2, "p2p-zblocked": 2}[args.exchange]
 
         def step_parts():
             eng.filter(raw)
@@ -452,6 +591,7 @@ def main():
         raw = torch.empty((n_proj, n, n), dtype=torch.float32, device=dev)
         phantom_raw(p, d, raw)
         k_rows = n
+        launches = 3 if slab.tensor else 2  # K1 (+ the exponent fill of the tap planes), K2
 
         def step_parts():
             eng.filter_stage(raw)  # K1 fused: Beer-Lambert + ramp + feather -> tap planes (or staging)
@@ -467,7 +607,7 @@ def main():
     if world > 1:
         dist.barrier()
 
-    # ---- timed region: K device-resident steps
+    # ---- timed region: K device-resident steps (inputs >> L2)
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
@@ -477,15 +617,12 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    tensor = bool(getattr(slab, "tensor", False)) and not angle_split
     for e in evs:
         bp_ev = [e[1], e[2]]
         e[0].record()
         step_parts()
         e[3].record()
     torch.cuda.synchronize()
-    if tensor:  # the MMA items K2 issues per launch (same window test as the kernel, tf_bp_tc_work)
-        ksteps_per_launch = slab.bp_work(bp_a0, bp_a1)["mma_items"]
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -496,47 +633,16 @@ def main():
         dist.all_reduce(t_tot, op=dist.ReduceOp.MAX)
     ms_per_step = t_tot.item() / args.steps
     gups = total_updates / (ms_per_step / 1e3) / 1e9
-
-    # ---- roofline of the dominant kernel (K2 BP) on this rank
     bp_avg_ms = statistics.mean(bp_ms)
-    exec_upd, active_tiles = executed_updates(d, n_proj, k_rows)
-    sm_mhz = clk.get("sm_mhz") or 1965.0
-    smem_peak = SMEM_BYTES_PER_CLK * SM_COUNT * sm_mhz * 1e6 / 1e9  # GB/s
-    from paper_2505_13955_b200._lib import TF_BP_FINALIZE, lib as _tf_lib
+    roof = None
+    if not angle_split:
+        roof = roofline(slab, bp_a0, bp_a1, k_rows, bp_avg_ms, clk.get("sm_mhz"), load_peaks(),
+                        args.config if world == 1 else f"{args.config}_n{world}")
 
-    bpu, exe = ctypes.c_double(), ctypes.c_int64()
-    _tf_lib().tf_bp_kernel_info(slab.bplan.handle, TF_BP_FINALIZE, k_rows, bp_a0, bp_a1, ctypes.byref(bpu),
-                                ctypes.byref(exe))
-    bytes_per_update = bpu.value
-    exec_upd = exe.value  # the library's own count: FoV-active tiles x tile voxels x padded rows x angles
-    smem_achieved = exec_upd * bytes_per_update / (bp_avg_ms / 1e3) / 1e9
-    fp32_peak_tflops = 128 * 2 * SM_COUNT * sm_mhz * 1e6 / 1e12
-    fp32_achieved = exec_upd * 4 / (bp_avg_ms / 1e3) / 1e12
-    slab_updates = n_proj * k_rows * n * n
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
-    stage_bytes = slab.stage.numel()
-    vol_elems = slab.vol.numel() if hasattr(slab, "vol") else n * n * n
-    hbm_alg = stage_bytes + vol_elems * 4  # one pass over the staged slab + the volume write
-    traffic = None  # ncu dram bytes of this kernel/config, captured separately (profiles/)
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", f"bp_traffic_{args.config}.json")))
-        if world == 1:
-            traffic = {"bytes_per_launch": tr["dram_bytes_per_launch"], "algorithmic_bytes": hbm_alg,
-                       "ratio": round(tr["dram_bytes_per_launch"] / hbm_alg, 2), "source": tr["source"]}
-    except (OSError, KeyError, ValueError):
-        pass
-
-    # ---- e2e through host pinned buffers: StreamedReconstructor (public API)
+    # ---- e2e through host pinned buffers: StreamedReconstructor (public API), --e2e-steps steps
     e2e = None
-    if not args.no_e2e:
-        from paper_2505_13955_b200.engine import StreamedReconstructor
-        from paper_2505_13955_b200.geometry import split_range
-
-        ke = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 2))
+    if not args.no_e2e and not angle_split:
+        ke = args.e2e_steps if args.e2e_steps is not None else args.steps
         er0, er1 = split_range(n, world)[rank]
         ek = er1 - er0
         h_raw = torch.empty((n_proj, ek, n), dtype=torch.float32, pin_memory=True)
@@ -567,92 +673,55 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = te.item()
-        if world == 1 and rank == 0:  # the host-fed volume must equal the device-resident one
-            a_, b_ = h_vol[n // 2], slab.vol[n // 2].cpu()
-            if getattr(slab, "tensor", False):  # sub-slabs pick their own fp16 tap scale: fp32 roundoff
-                same = bool(float((a_ - b_).norm() / b_.norm()) < 1e-6)
-            else:
-                same = bool(torch.equal(a_, b_))
-        else:
-            same = None
+        same = None
+        if world == 1:  # the host-fed volume equals the device-resident one, bit for bit (sampled slices)
+            same = bool(all(torch.equal(h_vol[r], slab.vol[r].cpu()) for r in parity_rows(n, 8)))
         e2e = {"value": round(total_updates / (e2e_ms / 1e3) / 1e9, 3), "unit": "GUPS",
                "h2d_bytes_per_step": int(h_raw.numel() * 4), "d2h_bytes_per_step": int(h_vol.numel() * 4),
                "s_per_volume": round(e2e_ms / 1e3, 4), "steps": ke,
+               "vs_device_resident": round(e2e_ms / ms_per_step, 4),
                "path": f"engine.StreamedReconstructor: pinned host sinogram -> {args.slab_rows}-row z-sub-slabs, "
                        "H2D / kernels / D2H on 3 streams (double-buffered); bytes are per rank",
-               "matches_device_resident_volume": same,
+               "matches_device_resident_volume_bitwise": same,
                "host_numa": numa}
         del streamed
 
-    # ---- parity spot check on the bench data (rank 0): 2 rows x 256^2 centre tile vs the C oracle
+    # ---- parity on the bench data (rank 0, N=1): full slices vs the f64 oracle
     parity = None
     if rank == 0 and not args.no_parity and world == 1:
         try:
-            from oracle import c_oracle as C
-            from oracle import fbp_oracle as O
-
-            rows = [n // 2, n // 3]
-            t = min(256, n)
-            x0 = (n - t) // 2
-            raw_rows = raw[:, rows].cpu().numpy()
-            filt = O.ramp_filter(O.preprocess(raw_rows, I0), pixel_pitch=PITCH)
-            geom = O.make_geom(n_proj, len(rows), n, pixel_pitch=PITCH, voxel_pitch=PITCH)
-            tile = (x0, x0 + t, x0, x0 + t)
-            ref = C.back_project(filt, geom, tile=tile)[:, x0:x0 + t, x0:x0 + t]
-            got = slab.vol[rows][:, x0:x0 + t, x0:x0 + t].cpu().numpy().astype(np.float64)
-            parity = {"rel_l2_vs_f64_oracle": float(np.linalg.norm(got - ref) / np.linalg.norm(ref)),
-                      "max_abs": float(np.abs(got - ref).max()), "rows": rows, "tile": list(tile)}
+            parity = parity_check(slab, raw, n_proj, n, args.parity_rows)
         except Exception as ex:  # never let the checker break the bench line
             parity = {"error": repr(ex)}
 
-    # ---- CPU baseline (rank 0, N=1 only): the reference chain on the same raw rows
+    # ---- CPU baseline (rank 0, N=1 only): the unmodified reference on the same raw rows
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = os.cpu_count() or 1
-        na = args.cpu_angles or max(4, min(n_proj, int(2.5e8 / (n * n))))
-        rows_idx = np.linspace(0, n - 1, cores).astype(int)
-        raw_rows = raw[:na][:, rows_idx].cpu().numpy()
-        g_cpu, info = cpu_reference(cfg, 1, 0, na, raw_rows=raw_rows)
-        v = g_cpu[0]
-        cpu_baseline = {"value": round(v, 6), "unit": "GUPS", "cores": info["cores"], "kind": info["kind"],
-                        "sample": info["sample"] + " (same raw rows the GPU consumed)",
-                        "s_per_volume_extrapolated": round(total_updates / (v * 1e9), 1)}
+        if not os.path.isdir(os.path.join(REF, "tomofuse")):
+            cpu_baseline = {"error": "baseline/_ref not installed (tools/install_reference.sh)"}
+        else:
+            try:
+                cores, na, rows = ref_sample(cfg, args.cpu_seconds)
+                raw_rows = raw[:na][:, torch.from_numpy(rows).to(raw.device)].cpu().numpy()
+                ref = CpuReference(cfg, raw_rows, cores, na)
+                r32 = ref.step()
+                r64 = ref.step(do64=True)
+                ref.close()
+                v = r32["chain_f32_gups"]
+                cpu_baseline = {"value": round(v, 6), "unit": "GUPS", "cores": ref.cores, "kind": "reference",
+                                "sample": ref.sample_desc() + " (the raw rows the GPU consumed)",
+                                "rows_per_process": ref.k,
+                                "bp_f32_gups": round(r32["bp_f32_gups"], 6),
+                                "bp_f64_gups": round(r64["bp_f64_gups"], 6),
+                                "ramp_filter_msamples_per_s": round(r32["ramp_filter_msamples_per_s"], 2),
+                                "s_per_volume_extrapolated": round(total_updates / (v * 1e9), 1)}
+            except Exception as ex:
+                cpu_baseline = {"error": repr(ex)}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    tc_roof = None
-    if tensor:
-        # tensor-core K2: per angle and CTA (121 voxels padded to M = 128, x 128 rows) 3 fp16 MMAs of 128 x 128 x 16
-        # per K-step (T_hi W_hi + T_hi W_lo + T_lo W_hi), 1 or 2 K-steps by the tile's window
-        flops = ksteps_per_launch * 3 * 2 * 128 * 128 * 16
-        tflops = flops / (bp_avg_ms / 1e3) / 1e12
-        pk = peaks.get("bf16_tflops_sustained") or 1420.9
-        tc_roof = {
-            "bound": "tensor",
-            "kernel": "bp_tc_kernel (K2, tcgen05)",
-            "achieved": round(tflops, 1),
-            "peak": pk,
-            "unit": "TFLOP/s",
-            "frac": round(tflops / pk, 4),
-            "frac_of_burst": round(tflops / (peaks.get("bf16_tflops") or 1684.4), 4),
-            "traffic": None,
-            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (dense fp16 MMA runs at the bf16 rate; "
-                           "K2 is a 1-2 s kernel inside the step)",
-            "flops_per_launch": flops,
-            "flops_note": "executed MMA FLOPs of the GEMM formulation D[voxel][row] += W[voxel][chan] T[chan][row]: "
-                          "K-steps counted on the device (tf_bp_tc_count) x 3 split products x 2*128*128*16",
-            "mma_ksteps_per_launch": ksteps_per_launch,
-            "bp_ms_per_launch": round(bp_avg_ms, 3),
-            "bp_gups_full_count": round(slab_updates / (bp_avg_ms / 1e3) / 1e9, 1),
-            # per angle and CTA (11 x 11 voxels x 128 rows = 15488 updates), one K-step (97% of angles):
-            # TMA writes 2 x 128 rows x 16 ch x 2 B = 8 KB and the MMAs read B 3 x 4 KB; weights come
-            # from TMEM: 20 KB / 15488 updates
-            "smem_bytes_per_update": 1.32,
-            "hbm_gbs_algorithmic": round(hbm_alg / (bp_avg_ms / 1e3) / 1e9, 1),
-            "hbm_peak_measured": peaks.get("hbm_gbs"),
-        }
     line = {
         "metric": METRIC,
         "value": round(gups, 3),
@@ -671,44 +740,18 @@ def main():
                    "parallelism": (f"angle-split x{world} ({args.exchange}: partials reduced onto z-slab owners)"
                                    if angle_split else
                                    f"z-slab x{world}" + (f" ({args.exchange} exchange)" if world > 1 else "")),
+                   "k2": "tensor cores" if getattr(slab, "tensor", False) else "CUDA cores",
                    "l2": "inputs larger than L2 (raw %.1f GB, volume %.1f GB per step)" % (
-                       raw.numel() * 4 / 1e9, vol_elems * 4 / 1e9),
+                       raw.numel() * 4 / 1e9, n * n * k_rows * 4 / 1e9),
                    "step": ("K1 Beer-Lambert+ramp+feather -> z-blocked staging -> K2 back-projection of this "
                             "rank's angles over the whole volume, epilogue adds into each row's owner "
                             "(NVLink peer memory, or + NCCL reduce-scatter) -> FoV/scale finalize"
                             if angle_split else
                             EXCHANGE_STEP.get(args.exchange if world > 1 else "", EXCHANGE_STEP[""]))},
-        "roofline": tc_roof if tensor else {
-            "bound": "smem",
-            "kernel": "bp_kernel (K2)",
-            "achieved": round(smem_achieved, 1),
-            "peak": round(smem_peak, 1),
-            "unit": "GB/s",
-            "frac": round(smem_achieved / smem_peak, 4),
-            "traffic": traffic["bytes_per_launch"] if traffic else None,
-            "traffic_detail": traffic,
-            "peak_source": "measured 127.69 B/clk/SM (conflict-free LDS.128, tools/micro/smem_rate.cu, "
-                           "profiles/r01_smem_rate.jsonl) x 148 SMs x measured median SM clock "
-                           "(shared-memory data path; no tensor-core or HBM bound applies, SURVEY 8d)",
-            "roof_updates_per_s_e9": round(smem_peak / bytes_per_update, 1),
-            "algorithmic_bytes_per_update": bytes_per_update,
-            "bytes_note": "smem bytes the K2 variant gathers per update: 8 = two fp32 taps; 6 = x-pair "
-                          "kernel (3 taps shared by 2 voxels, taps held in registers)",
-            "bp_ms_per_launch": round(bp_avg_ms, 3),
-            "executed_updates_per_launch": exec_upd,
-            "active_tiles": active_tiles,
-            "bp_gups_executed": round(exec_upd / (bp_avg_ms / 1e3) / 1e9, 1),
-            "bp_gups_full_count": round(slab_updates / (bp_avg_ms / 1e3) / 1e9, 1),
-            "fp32_tflops": round(fp32_achieved, 2),
-            "fp32_frac": round(fp32_achieved / fp32_peak_tflops, 4),
-            "hbm_gbs_algorithmic": round(hbm_alg / (bp_avg_ms / 1e3) / 1e9, 1),
-            "hbm_peak_measured": peaks.get("hbm_gbs"),
-        },
+        "roofline": roof,
         "clocks": clk,
-        # our kernels per step: K1 + K2, + tf_bp_stage (allgather, p2p) or + tf_bp_finalize (angle split)
-        # (+2 with the tensor-core K2: tc_absmax_kernel for the fp16 tap scale, tc_convert_kernel)
-        "gpu_launches": ((3 if (world > 1 and (args.exchange in ("allgather", "p2p") or angle_split)) else 2)
-                         + (2 if tensor else 0)) * args.steps,
+        "gpu_launches": launches * args.steps,
+        "bp_share_of_step": round(bp_avg_ms / statistics.mean(step_ms), 4),
     }
     if e2e is not None:
         line["e2e"] = e2e

@@ -14,7 +14,7 @@
  *   FoV zeroing, then * (span/n_proj)                        fbp.py:246-251
  * and the float32 path mirrors numpy's float32 promotion of the same
  * expressions (frac cast to f32, line*weights in f32, f32 accumulate).
- * tests/test_oracle_golden.py pins both against reference-generated vectors.
+ * tests/test_cpu_host.py (the oracle-vs-golden tests) pins both against reference-generated vectors.
  */
 #include <math.h>
 #include <stdint.h>

@@ -9,7 +9,7 @@ would void the parity claims, so the package has no import of `oracle`.
 
 Parity pinning: every function below is checked against golden vectors that
 `tests/golden/make_golden.py` produced by importing the reference package
-itself (`tests/test_oracle_golden.py`).  Third-party arithmetic the reference
+itself (`tests/test_cpu_host.py`, the oracle-vs-golden tests).  Third-party arithmetic the reference
 delegates to:
 
 * numpy.fft.rfft/irfft (pocketfft, numpy 2.3.5 here) -- used the same way

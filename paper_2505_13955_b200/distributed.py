@@ -99,6 +99,29 @@ def zblocked(rows, weights=None):
     return full.reshape(-1)
 
 
+def tap_planes(rows, weights, bound):
+    """Host/torch restatement of K2-TC's tap planes (tf_filter_taps /
+    tf_bp_tc_stage with a bound): (A, k, n_chan) fp32 filtered rows ->
+    flat bytes [A][hi, lo][k/8][n_chan][8] fp16 of (rows * weights) * 2^e,
+    e = 14 - floor(log2(bound)), hi = fp16(x), lo = fp16(x - hi); rows past
+    k in the last 8-row group are zero here (the kernels leave them
+    unwritten).  The workspace header (per-row exponents) is not included."""
+    import math
+
+    import torch
+
+    A, k, n = rows.shape
+    e = min(100, max(-100, 14 - (math.frexp(bound)[1] - 1)))
+    x = (rows * weights) * (2.0 ** e)
+    hi = x.to(torch.float16)
+    lo = (x - hi.float()).to(torch.float16)
+    R8 = -(-k // 8)
+    out = torch.zeros((A, 2, R8 * 8, n), dtype=torch.float16, device=rows.device)
+    out[:, 0, :k] = hi
+    out[:, 1, :k] = lo
+    return out.view(A, 2, R8, 8, n).permute(0, 1, 2, 4, 3).contiguous().view(torch.uint8).reshape(-1)
+
+
 def exchange(send, recv, in_splits, out_splits, group=None):
     import torch.distributed as dist
 

@@ -298,6 +298,41 @@ def test_shim_rebinds_reference_surface():
     assert pipe_mod.back_project is orig and fbp_mod.reconstruct is orig
 
 
+def test_shim_binds_the_real_reference_modules():
+    """shim.install() on the unmodified reference package (baseline/_ref,
+    tools/install_reference.sh): every name pipeline.py:30 and fbp.py:75-275
+    expose is rebound, a module importing `from tomofuse.fbp import
+    back_project` afterwards (as test_fbp.py does) gets the GPU function,
+    and uninstall() restores the reference.  No compute: runs on CPU."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ref = os.path.join(root, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "tomofuse")):
+        pytest.skip("baseline/_ref not installed (tools/install_reference.sh)")
+    code = """
+import tomofuse.fbp as F, tomofuse.pipeline as P
+from paper_2505_13955_b200 import shim, fbp as G
+orig = {n: getattr(F, n) for n in shim.REBIND}
+done = shim.install()
+assert len(done) == 11, done
+for n, mods in shim.REBIND.items():
+    for m in mods:
+        assert getattr(__import__(m, fromlist=['x']), n) is getattr(G, n), (m, n)
+from tomofuse.fbp import back_project, ramp_filter
+assert back_project is G.back_project and ramp_filter is G.ramp_filter
+shim.uninstall()
+assert all(getattr(F, n) is f for n, f in orig.items())
+assert P.back_project.__module__ == 'tomofuse.fbp'
+print('SHIM_OK')
+"""
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([ref, root]))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0 and "SHIM_OK" in r.stdout, r.stderr[-2000:]
+
+
 def test_oracle_matches_reference_pipeline_run(golden):
     """pipeline.run over a 2x2 simulated grid == the serial float32 chain
     (pkg/tests/test_pipeline.py:102-112 tolerance 1e-5), through the oracle."""

@@ -572,7 +572,7 @@ def test_fused_filter_stage_equals_filter_then_stage(F, rows, offset):
         p = AcquisitionParams(n_proj=21, n_rows=rows, n_chan=48)
     d = VolumeDims(48, 48, rows)
     raw = _phantom_rows(p, d, 0, rows)
-    eng = SlabReconstructor(p, d, i0=1e5)
+    eng = SlabReconstructor(p, d, i0=1e5, tensor=False)
     eng.filter_stage(raw)
     fused = eng.stage.clone().view(torch.float32)
     filt = eng.filter(raw)
@@ -824,44 +824,38 @@ def test_tensor_core_bp_matches_oracle(F, case):
 
 
 def test_tensor_core_row_slabs_and_streaming(F):
-    """Tensor-core path over z-slabs and host-streamed sub-slabs: with the
-    same fp16 scale (the full volume's max |T| handed in, as the multi-GPU
-    z-slab split does with an all-reduce) a row's result does not depend on
-    the slab or the 128-row MMA block it sits in -- bit for bit; with each
-    sub-slab's own scale (streaming) it agrees to fp32 roundoff."""
+    """Tensor-core path over z-slabs and host-streamed sub-slabs: K1 scales
+    raw-count taps by one exponent from the analytic bound (never from the
+    data), so a row's result does not depend on the slab, the sub-slab or
+    the 128/256-row MMA block it sits in -- bit for bit."""
     import torch
 
     from paper_2505_13955_b200.engine import SlabReconstructor, StreamedReconstructor
     from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
 
     n = 64
-    p = AcquisitionParams(n_proj=90, n_rows=200, n_chan=n)
-    d = VolumeDims(n, n, 200)
-    raw = _phantom_rows(p, d, 0, 200)
-    fe = SlabReconstructor(p, d, i0=1e5, tensor=True)
-    full = fe.run(raw).cpu()
-    gmax = fe.tc_absmax().clone()
-    for r0, r1 in [(0, 32), (32, 200), (64, 192)]:
+    p = AcquisitionParams(n_proj=90, n_rows=300, n_chan=n)
+    d = VolumeDims(n, n, 300)
+    raw = _phantom_rows(p, d, 0, 300)
+    full = SlabReconstructor(p, d, i0=1e5, tensor=True).run(raw).cpu()
+    for r0, r1 in [(0, 32), (32, 300), (64, 192), (10, 268)]:
         pe = SlabReconstructor(p, d, i0=1e5, rows=(r0, r1), tensor=True)
-        pe.filter_stage(raw[:, r0:r1].contiguous())
-        pe.tc_absmax()
-        pe.tc_ws[:4].view(torch.int32).copy_(gmax)  # the all-reduced max of a z-slab split
-        pe.prepare_tc(use_max=True)
-        part = pe.backproject(prepared=True).cpu()
+        part = pe.run(raw[:, r0:r1].contiguous()).cpu()
         assert torch.equal(part, full[r0:r1]), (r0, r1)
     h_raw = raw.cpu().pin_memory()
-    h_vol = torch.empty((200, n, n), dtype=torch.float32).pin_memory()
+    h_vol = torch.empty((300, n, n), dtype=torch.float32).pin_memory()
     st = StreamedReconstructor(p, d, i0=1e5, slab_rows=64)
     assert st.eng.tensor
     st.run(h_raw, h_vol)
     torch.cuda.synchronize()
-    assert rel_l2(h_vol.numpy(), full.numpy()) < 1e-6
+    assert torch.equal(h_vol, full)
 
 
 def test_tensor_core_angle_chunks_and_depth_input(F):
-    """Angle-chunked TF_BP_ACCUMULATE passes on the tensor path agree with one
-    pass to fp32 roundoff (the RN flush blocks restart per launch), and depth
-    input (i0 <= 0) matches the CUDA-core kernel on the same depth."""
+    """Angle chunks chained with TF_BP_ACCUMULATE on the tensor path: cuts at
+    multiples of 16 angles (the absolute flush blocks) give the one-pass
+    volume bit for bit; other cuts agree to fp32 roundoff.  Depth input
+    (i0 <= 0, per-row exponents from the data) matches the CUDA-core kernel."""
     import torch
 
     from paper_2505_13955_b200 import _lib
@@ -874,13 +868,78 @@ def test_tensor_core_angle_chunks_and_depth_input(F):
     raw = _phantom_rows(p, d, 0, 40)
     eng = SlabReconstructor(p, d, i0=1e5, tensor=True)
     one = eng.run(raw).clone()
-    vol2 = torch.zeros_like(one)
-    cuts = [0, 7, 50, 51, 100]
-    for i, (a, b) in enumerate(zip(cuts[:-1], cuts[1:])):
-        flags = (_lib.TF_BP_ACCUMULATE if i else 0) | (_lib.TF_BP_FINALIZE if b == n_proj else 0)
-        eng.backproject(a, b, flags=flags, vol=vol2)
-    assert rel_l2(vol2.cpu().numpy(), one.cpu().numpy()) < 1e-6
+    for cuts, bitwise in (([0, 16, 48, 64, 100], True), ([0, 7, 50, 51, 100], False)):
+        vol2 = torch.zeros_like(one)
+        for i, (a, b) in enumerate(zip(cuts[:-1], cuts[1:])):
+            flags = (_lib.TF_BP_ACCUMULATE if i else 0) | (_lib.TF_BP_FINALIZE if b == n_proj else 0)
+            eng.backproject(a, b, flags=flags, vol=vol2)
+        if bitwise:
+            assert torch.equal(vol2, one)
+        else:
+            assert rel_l2(vol2.cpu().numpy(), one.cpu().numpy()) < 1e-6
     depth = -torch.log(torch.clamp(raw, min=1.0) / 1e5)
     got = SlabReconstructor(p, d, i0=0.0, tensor=True).run(depth).cpu().numpy()
     ref = SlabReconstructor(p, d, i0=0.0, tensor=False).run(depth).cpu().numpy()
     assert rel_l2(got, ref) < 2e-6
+
+
+@pytest.mark.parametrize("rows,offset", [(64, 0), (45, 0), (7, 0), (33, 13)])
+def test_filter_taps_equal_filter_then_tc_stage(F, rows, offset):
+    """K1 writing the tap planes directly (tf_filter_taps) == K1's natural
+    output staged by tf_bp_tc_stage with the same raw-count bound, bit for
+    bit, and == the host restatement distributed.tap_planes (feather, x 2^e,
+    fp16 hi/lo split)."""
+    import math as _m
+
+    import torch
+
+    from paper_2505_13955_b200.distributed import tap_planes
+    from paper_2505_13955_b200.engine import SlabReconstructor
+    from paper_2505_13955_b200.geometry import AcquisitionParams, ScanMode, VolumeDims
+
+    if offset:
+        p = AcquisitionParams(n_proj=20, n_rows=rows, n_chan=48, angle_span=2 * _m.pi,
+                              scan_mode=ScanMode.OFFSET, offset_chan=offset)
+    else:
+        p = AcquisitionParams(n_proj=21, n_rows=rows, n_chan=48)
+    d = VolumeDims(48, 48, rows)
+    raw = _phantom_rows(p, d, 0, rows)
+    eng = SlabReconstructor(p, d, i0=1e5, tensor=True)
+    eng.filter_stage(raw)
+    fused = eng.taps.clone()
+    filt = eng.filter(raw).clone()
+    eng.stage_rows(filt)
+    staged = eng.taps
+    w = torch.from_numpy(F.offset_weights(p)).float().cuda()
+    host = tap_planes(filt, w, eng.tap_bound())
+    hdr = fused.numel() - host.numel()
+    R8 = -(-rows // 8)
+    # the per-row exponents (header) and every real row's taps; rows past n_rows in the last
+    # 8-row group are left unwritten by K1 (tf_bp_tc_stage zero-fills them)
+    assert torch.equal(fused[: 4 * rows], staged[: 4 * rows])
+    valid = torch.zeros(R8 * 8, dtype=torch.bool)
+    valid[:rows] = True
+    valid = valid.view(R8, 8)[None, None, :, None, :].expand(p.n_proj, 2, R8, 48, 8).cuda()
+    planes = [t.view(torch.float16).view(p.n_proj, 2, R8, 48, 8)[valid] for t in (fused[hdr:], staged[hdr:], host)]
+    assert torch.equal(planes[0], planes[1])
+    assert torch.equal(planes[0], planes[2])
+
+
+def test_tensor_core_row_independence_and_data_scale(F):
+    """fbp.back_project on the tensor path scales each detector row by its
+    own exponent, so bumping one row changes no other row's result
+    (test_fbp.py:180-191, bitwise) however large the bump."""
+    rng = np.random.default_rng(9)
+    from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
+
+    params = AcquisitionParams(n_proj=40, n_rows=5, n_chan=48)
+    dims = VolumeDims(nx=48, ny=48, nz=5)
+    sino = rng.normal(size=(40, 5, 48))
+    base = F.back_project(sino, dims, params)
+    for bump in (1.0, 1e6):
+        bumped = sino.copy()
+        bumped[:, 2, :] += bump
+        out = F.back_project(bumped, dims, params)
+        diff = np.abs(out - base).reshape(5, -1).max(axis=1)
+        assert diff[2] > 0
+        assert np.all(diff[[0, 1, 3, 4]] == 0)

@@ -43,11 +43,14 @@ dist.gather(buf, gathered, dst=0)
 if rank == 0:
     full_raw = torch.empty((n_proj, rows, n), device=dev)
     phantom_raw(p, d, full_raw)
-    ref = SlabReconstructor(p, d, i0=1e5).run(full_raw)
+    # the same K2 kind: tensor cores for the natural-row exchanges, the CUDA-core kernel for the
+    # z-blocked landings and the angle-split reduce epilogue
+    tensor = bool(getattr(getattr(z, "local", None), "tensor", False))
+    ref = SlabReconstructor(p, d, i0=1e5, tensor=tensor).run(full_raw)
     got = torch.cat([g[: e - s] for g, (s, e) in zip(gathered, z.slabs)])
     same = torch.equal(got, ref)
     rel = float((got - ref).norm() / ref.norm())
-    print(f"rank0 world={world} exchange={args.exchange} bitwise_equal={same} rel_l2={rel:.3e} "
+    print(f"rank0 world={world} exchange={args.exchange} tensor={tensor} bitwise_equal={same} rel_l2={rel:.3e} "
           f"max_diff={float((got - ref).abs().max()):.3e}")
     # z-slabs are bitwise; angle-split sums in a different order (fp32 rounding)
     if same or (args.exchange.startswith("angles-") and rel < 1e-6):
