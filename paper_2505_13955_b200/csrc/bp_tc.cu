@@ -63,7 +63,10 @@ constexpr int kS = 8;           // ring depth in items
 constexpr int kP = 16;          // angles per accumulator block (absolute angle index / kP)
 constexpr int kG = 4;           // weight groups of 4 warps
 constexpr int kThreads = 64 + 128 * kG;
-constexpr int kLag = 8;         // a group flushes block j once it produces angle >= end(j) + kLag
+#ifndef TF_TC_LAG
+#define TF_TC_LAG 8
+#endif
+constexpr int kLag = TF_TC_LAG;  // a group flushes block j once it produces angle >= end(j) + kLag
 constexpr int kWPlane = kM * kK * 2;   // one fp16 plane of a slot's W tile (4 KB)
 constexpr float kOneStep = 14.9f;      // window test (fp32 margin below 15)
 static_assert(kMV <= kM, "tile fits the MMA's M");
@@ -88,7 +91,18 @@ struct TCArgs {
     int ntx, flags;
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
+#ifdef TF_TC_PROBE
+    long long* probe;  // tools/tc_probe.cu: per-CTA wait-cycle counters (never in the product library)
+#endif
 };
+
+#ifdef TF_TC_PROBE
+#define PROBE_T0(v) const long long v = clock64()
+#define PROBE_ADD(acc, t0) acc += clock64() - (t0)
+#else
+#define PROBE_T0(v)
+#define PROBE_ADD(acc, t0)
+#endif
 
 __device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
     uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
@@ -244,7 +258,11 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kS; ++s) {
+#ifdef TF_TC_PROBE_W_NONE  // probe builds only: weight warps absent from the ring
+            mbar_init(&full[s], 1);
+#else
             mbar_init(&full[s], 1 + 4);  // TMA arrive.expect_tx + the owning group's 4 warps
+#endif
             mbar_init(&empty[s], 1);     // MMA commit
         }
         for (int b = 0; b < 2; ++b) {
@@ -276,6 +294,8 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
         // ---- TMA producer (lane 0 issues; the whole warp walks the batches)
         if (lane == 0) tma_prefetch_desc(&map);
         int it = 0;
+        long long p_wait = 0;
+        PROBE_T0(p_start);
         for (int g0 = 0; g0 < n_ang; g0 += 32) {
             const TcBatch bt = tc_batch(g0, n_ang, dX, dY, a);
             for (int i = 0; i < bt.n; ++i) {
@@ -285,16 +305,30 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
                     const int ka = 2 * (a.a0 + g0 + i - a.ws_a0);
                     for (int ks = 0; ks < nk; ++ks, ++it) {
                         const int s = it % kS;
+                        PROBE_T0(pw);
                         if (it >= kS) mbar_wait(&empty[s], (uint32_t)((it / kS) - 1) & 1u);
+                        PROBE_ADD(p_wait, pw);
                         uint8_t* st = ring + s * Cfg::SLOT;
+#ifdef TF_TC_PROBE_NO_TMA  // probe builds only: timing without the tap loads
+                        mbar_arrive(&full[s]);
+                        (void)st, (void)c_lo, (void)ka;
+#else
                         mbar_arrive_expect_tx(&full[s], 2 * Cfg::TAP_PLANE);
                         tma_load_3d(st, &map, &full[s], 8 * (c_lo + kK * ks), zr0 / 8, ka);
                         tma_load_3d(st + Cfg::TAP_PLANE, &map, &full[s], 8 * (c_lo + kK * ks), zr0 / 8, ka + 1);
+#endif
                     }
                 }
                 __syncwarp();
             }
         }
+#ifdef TF_TC_PROBE
+        if (a.probe && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) {
+            a.probe[blockIdx.x * 16 + 0] = clock64() - p_start;
+            a.probe[blockIdx.x * 16 + 1] = p_wait;
+        }
+#endif
+        (void)p_wait;
     } else if (warp == 1) {
         // ---- MMA issue: the warp runs the loop (waits are warp-uniform), one elected lane issues
         if (n_ang > 0) {
@@ -308,6 +342,8 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
             const uint64_t dT = umma_sdesc(smem_u32(ring), 128, 256);
             const uint64_t dW = umma_sdesc(smem_u32(ring + 2 * Cfg::TAP_PLANE), 128, 256);
             int it = 0;
+            long long p_full = 0, p_free = 0, p_issue = 0;
+            PROBE_T0(p_start);
             for (int g0 = 0; g0 < n_ang; g0 += 32) {
                 const TcBatch bt = tc_batch(g0, n_ang, dX, dY, a);
                 for (int i = 0; i < bt.n; ++i) {
@@ -318,26 +354,53 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
                         const int s = it % kS;
                         const bool first = ks == 0 && (g == 0 || ab % kP == 0);
                         const bool last = ks == nk - 1 && (g == n_ang - 1 || (ab + 1) % kP == 0);
+                        PROBE_T0(q0);
+#ifndef TF_TC_PROBE_NO_ACCFREE  // probe builds only
                         if (first && lb >= 2) mbar_wait(&accfree[acc], (uint32_t)((lb >> 1) - 1) & 1u);
+#endif
+                        PROBE_ADD(p_free, q0);
+                        PROBE_T0(q1);
+#ifndef TF_TC_PROBE_MMA_NOWAIT  // probe builds only: MMAs on whatever the slot holds
                         mbar_wait(&full[s], (uint32_t)(it / kS) & 1u);
+#endif
+                        PROBE_ADD(p_full, q1);
+                        PROBE_T0(q2);
                         tc_fence_after();
                         if (elect_one()) {
                             const uint64_t so = (uint64_t)((s * Cfg::SLOT) >> 4);
                             const uint64_t th = dT + so, tl = th + (Cfg::TAP_PLANE >> 4);
                             const uint64_t wh = dW + so, wl = wh + (kWPlane >> 4);
                             const uint32_t td = tmem + (uint32_t)(acc * NR);
+#ifndef TF_TC_PROBE_NO_MMA  // probe builds only: timing without the MMAs
                             umma_f16_ss(td, wh, th, idesc, first ? 0u : 1u);
                             umma_f16_ss(td, wl, th, idesc, 1u);
                             umma_f16_ss(td, wh, tl, idesc, 1u);
+#else
+                            (void)td, (void)wh, (void)wl, (void)th, (void)tl;
+#endif
                             umma_commit(&empty[s]);  // frees the slot's taps and weights
                             if (last) umma_commit(&accfull[acc]);
                         }
                         __syncwarp();
+                        PROBE_ADD(p_issue, q2);
                     }
                 }
             }
+#ifdef TF_TC_PROBE
+            if (a.probe && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) {
+                a.probe[blockIdx.x * 16 + 2] = clock64() - p_start;
+                a.probe[blockIdx.x * 16 + 3] = p_full;
+                a.probe[blockIdx.x * 16 + 4] = p_free;
+                a.probe[blockIdx.x * 16 + 5] = p_issue;
+                a.probe[blockIdx.x * 16 + 6] = it;
+            }
+#endif
+            (void)p_full, (void)p_free, (void)p_issue;
         }
     } else {
+#ifdef TF_TC_PROBE_W_NONE
+        if (true) goto probe_done;
+#endif
         // ---- weight groups: angle g -> group g % kG (a batch of 32 splits evenly); one voxel row
         // per thread (TMEM lane quadrant = warp % 4); column slice grp of the master sum
         const int grp = (warp - 2) >> 2;
@@ -363,6 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
             const int acc = lb & 1;
             mbar_wait(&accfull[acc], (uint32_t)(lb >> 1) & 1u);
             tc_fence_after();
+#ifndef TF_TC_PROBE_NO_FLUSH  // probe builds only: timing without the TMEM reads
 #pragma unroll
             for (int c = 0; c < NC; c += 16) {
                 uint32_t v[16];
@@ -371,23 +435,32 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
 #pragma unroll
                 for (int j = 0; j < 16; ++j) master[c + j] = __fadd_rn(master[c + j], __uint_as_float(v[j]));
             }
+#endif
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&accfree[acc]);
         };
         const uint32_t wslot0 = smem_u32(ring + 2 * Cfg::TAP_PLANE) + (uint32_t)((m >> 3) * 256 + (m & 7) * 16);
         int flushed = 0, ibase = 0;
+        long long p_empty = 0, p_flush = 0;
+        PROBE_T0(p_start);
         for (int g0 = 0; g0 < n_ang; g0 += 32) {
             const TcBatch bt = tc_batch(g0, n_ang, dX, dY, a);
             for (int i = grp; i < bt.n; i += kG) {
                 const int ab = a.a0 + g0 + i;
                 // flush the blocks that ended kLag angles ago: this group's slot waits proved
                 // their MMAs retired, so the accfull waits return at once
+                PROBE_T0(q3);
                 while (flushed < n_blk && (blk0 + flushed + 1) * kP + kLag <= ab) flush(flushed++);
+                PROBE_ADD(p_flush, q3);
                 const TcWin w = tc_bcast(bt.w, i);
                 const int nk = 1 + ((bt.two >> i) & 1);
                 const int it0 = ibase + i + __popc(bt.two & ((1u << i) - 1u));
+#ifdef TF_TC_PROBE_W_IDLE  // probe builds only: no weight arithmetic
+                const float t = 0.f;
+#else
                 const float t = fmaxf(fmaf(fdy, w.C, fmaf(fdx, w.B, w.F0)), 0.f);
+#endif
                 const float fl = floorf(t);
                 const float f = t - fl;
                 const float g0w = 1.f - f;
@@ -403,7 +476,9 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
                     // tap o = floor(t) - 16 ks of this item's window; the pair (2j, 2j + 1) of
                     // halves holding it is jo = o >> 1 (o = -1: only f lands, in pair 0)
                     const int jo = real ? (o0 - kK * ks) >> 1 : -8;
+                    PROBE_T0(q4);
                     if (it >= kS) mbar_wait(&empty[s], (uint32_t)((it / kS) - 1) & 1u);
+                    PROBE_ADD(p_empty, q4);
                     const uint32_t wa = wslot0 + (uint32_t)(s * Cfg::SLOT);
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {  // 8-channel chunk c: pairs 4c .. 4c + 3
@@ -414,10 +489,16 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
                             vh[j] = jj == jo ? Xh : (jj == jo + 1 ? Yh : 0u);
                             vl[j] = jj == jo ? Xl : (jj == jo + 1 ? Yl : 0u);
                         }
+#ifndef TF_TC_PROBE_NO_WEIGHTS  // probe builds only: timing without the weight stores
                         sts128(wa + 128 * c, vh[0], vh[1], vh[2], vh[3]);
                         sts128(wa + kWPlane + 128 * c, vl[0], vl[1], vl[2], vl[3]);
+#else
+                        if (vh[0] == 0x7fffffffu && vl[3] == 0x7fffffffu) sts128(wa, vh[0], vh[1], vh[2], vh[3]);
+#endif
                     }
+#ifndef TF_TC_PROBE_NO_FENCE  // probe builds only
                     fence_proxy_async();  // generic-proxy stores -> visible to the tensor core
+#endif
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&full[s]);
                 }
@@ -425,6 +506,15 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
             ibase += bt.n + __popc(bt.two);
         }
         while (flushed < n_blk) flush(flushed++);
+#ifdef TF_TC_PROBE
+        if (a.probe && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024 && (warp == 2 || warp == 14)) {
+            const int o = warp == 2 ? 7 : 10;
+            a.probe[blockIdx.x * 16 + o] = clock64() - p_start;
+            a.probe[blockIdx.x * 16 + o + 1] = p_empty;
+            a.probe[blockIdx.x * 16 + o + 2] = p_flush;
+        }
+#endif
+        (void)p_empty, (void)p_flush;
         // ---- epilogue: master x 2^-e -> volume (fbp.py:247-251)
         if (inside) {
             const bool fin = (a.flags & TF_BP_FINALIZE) != 0;
@@ -441,6 +531,9 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
             }
         }
     }
+#ifdef TF_TC_PROBE_W_NONE
+probe_done:
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS));
@@ -576,6 +669,10 @@ int launch_tc(const CUtensorMap& map, const TCArgs& a, dim3 grid, cudaStream_t s
 
 }  // namespace
 
+#ifdef TF_TC_PROBE
+long long* g_tc_probe = nullptr;  // set by tools/tc_probe.cu's tf_bp_tc_probe (probe build only)
+#endif
+
 // shared with filter.cu (K1 writing tap planes directly)
 int64_t bp_tc_header_bytes(int n_rows) { return tc_header_bytes(n_rows); }
 int tc_uniform_exponents(void* taps, int n_rows, double bound, cudaStream_t s) {
@@ -705,6 +802,9 @@ extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* taps, int64_t 
     a.y0 = y0;
     a.y1 = y1;
     a.flags = flags & (TF_BP_ACCUMULATE | TF_BP_FINALIZE);
+#ifdef TF_TC_PROBE
+    a.probe = g_tc_probe;
+#endif
     const int nty = (g.ny + kTY - 1) / kTY;
     dim3 grid((unsigned)(a.ntx * nty), (unsigned)((n_rows + NR - 1) / NR));
     return NR == 256 ? launch_tc<256>(map, a, grid, as_stream(stream)) : launch_tc<128>(map, a, grid, as_stream(stream));

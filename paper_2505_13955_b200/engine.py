@@ -258,15 +258,19 @@ class StreamedReconstructor:
             self.s_d2h = torch.cuda.Stream(self.device)
 
     def sub_slabs(self, R0, R1):
-        """Sub-slab boundaries: full slabs in the middle and a geometric ramp
-        at both ends (32, 64, 128, ... rows) so that the un-overlapped
-        pipeline fill (first H2D) and drain (last D2H) are one 32-row slab
-        each, while every next slab's H2D still hides under the current
-        slab's compute (compute per row > copy per row).  When the range is
-        too short for the ramp up to `slab_rows` (a z-slab of one GPU among
-        several: 512 rows at N=4), the middle slab size halves until the ramp
-        fits, instead of falling back to two un-overlapped full slabs."""
+        """Sub-slab boundaries.  Tensor-core K2: uniform `slab_rows` slabs
+        (a short slab costs a full 128/256-row MMA block, so a ramp of small
+        slabs would waste tensor work; the un-overlapped fill and drain are
+        one slab's H2D and D2H).  CUDA-core K2: full slabs in the middle and
+        a geometric ramp at both ends (32, 64, 128, ... rows) so that the
+        fill (first H2D) and drain (last D2H) are one 32-row slab each,
+        while every next slab's H2D still hides under the current slab's
+        compute; when the range is too short for the ramp up to `slab_rows`
+        (a z-slab of one GPU among several: 512 rows at N=4), the middle
+        slab size halves until the ramp fits."""
         S = self.slab_rows
+        if self.eng.tensor:
+            return [(r, min(r + S, R1)) for r in range(R0, R1, S)]
 
         def ramp_to(s):
             r, e = [], 32

@@ -398,8 +398,12 @@ def test_streamed_sub_slabs_cover_rows_once(R0, R1, S):
     hides under the current slab's compute)."""
     from paper_2505_13955_b200.engine import StreamedReconstructor
 
+    class Eng:
+        tensor = False
+
     class Cfg:
         slab_rows = S
+        eng = Eng()
 
     cuts = StreamedReconstructor.sub_slabs(Cfg(), R0, R1)
     assert cuts[0][0] == R0 and cuts[-1][1] == R1
@@ -410,6 +414,25 @@ def test_streamed_sub_slabs_cover_rows_once(R0, R1, S):
     if R1 - R0 >= 128 and S >= 64:  # the ramp fits once the middle slab may shrink to 64 rows
         assert sizes[0] == 32 and sizes[-1] == 32
         assert all(sizes[i + 1] <= 2 * sizes[i] for i in range(len(sizes) // 2))
+
+
+@pytest.mark.parametrize("R0,R1,S", [(0, 2048, 256), (0, 1100, 256), (512, 1024, 256), (0, 96, 256)])
+def test_streamed_sub_slabs_tensor_core_uniform(R0, R1, S):
+    """Tensor-core K2: uniform slab_rows sub-slabs (a short slab costs a
+    whole MMA row block), the last one ragged."""
+    from paper_2505_13955_b200.engine import StreamedReconstructor
+
+    class Eng:
+        tensor = True
+
+    class Cfg:
+        slab_rows = S
+        eng = Eng()
+
+    cuts = StreamedReconstructor.sub_slabs(Cfg(), R0, R1)
+    assert cuts[0][0] == R0 and cuts[-1][1] == R1
+    assert all(cuts[i][1] == cuts[i + 1][0] for i in range(len(cuts) - 1))
+    assert all(b - a == S for a, b in cuts[:-1]) and 0 < cuts[-1][1] - cuts[-1][0] <= S
 
 
 def test_hostnuma_cpulist_parse():
