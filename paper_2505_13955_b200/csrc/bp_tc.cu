@@ -77,7 +77,7 @@ struct TcCfg {
     static constexpr int TAP_PLANE = NR * kK * 2;                   // one fp16 plane of a slot's taps
     static constexpr int SLOT = 2 * TAP_PLANE + 2 * kWPlane;        // taps hi, lo + W hi, lo
     static constexpr int NC = NR / kG;                              // master columns per thread
-    static constexpr int SMEM = kS * SLOT + NR * 8 + (2 * kS + 4) * 8 + 16;
+    static constexpr int SMEM = kS * SLOT + NR * 8 + (2 * kS + 4) * 8 + 16 + 4 * kS;
     static constexpr uint32_t TMEM_COLS = 2 * NR;
 };
 
@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
     uint64_t* accfull = empty + kS;   // [2]: block's MMAs done -> flush
     uint64_t* accfree = accfull + 2;  // [2]: block flushed by all 16 weight warps -> accumulator reusable
     uint32_t* tslot = reinterpret_cast<uint32_t*>(accfree + 2);
+    uint32_t* s_ctl = tslot + 4;  // [kS]: the slot's item control word (written by the TMA warp)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kS; ++s) {
@@ -291,44 +292,9 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
     const double dX = (double)X0 - a.cx, dY = (double)Y0 - a.cy;
 
     if (warp == 0) {
-        // ---- TMA producer (lane 0 issues; the whole warp walks the batches)
+        // the TMA loads are issued by the weight groups with their items (below); this warp only
+        // prefetches the tensor map
         if (lane == 0) tma_prefetch_desc(&map);
-        int it = 0;
-        long long p_wait = 0;
-        PROBE_T0(p_start);
-        for (int g0 = 0; g0 < n_ang; g0 += 32) {
-            const TcBatch bt = tc_batch(g0, n_ang, dX, dY, a);
-            for (int i = 0; i < bt.n; ++i) {
-                const int c_lo = __shfl_sync(0xffffffffu, bt.w.c_lo, i);
-                const int nk = 1 + ((bt.two >> i) & 1);
-                if (lane == 0) {
-                    const int ka = 2 * (a.a0 + g0 + i - a.ws_a0);
-                    for (int ks = 0; ks < nk; ++ks, ++it) {
-                        const int s = it % kS;
-                        PROBE_T0(pw);
-                        if (it >= kS) mbar_wait(&empty[s], (uint32_t)((it / kS) - 1) & 1u);
-                        PROBE_ADD(p_wait, pw);
-                        uint8_t* st = ring + s * Cfg::SLOT;
-#ifdef TF_TC_PROBE_NO_TMA  // probe builds only: timing without the tap loads
-                        mbar_arrive(&full[s]);
-                        (void)st, (void)c_lo, (void)ka;
-#else
-                        mbar_arrive_expect_tx(&full[s], 2 * Cfg::TAP_PLANE);
-                        tma_load_3d(st, &map, &full[s], 8 * (c_lo + kK * ks), zr0 / 8, ka);
-                        tma_load_3d(st + Cfg::TAP_PLANE, &map, &full[s], 8 * (c_lo + kK * ks), zr0 / 8, ka + 1);
-#endif
-                    }
-                }
-                __syncwarp();
-            }
-        }
-#ifdef TF_TC_PROBE
-        if (a.probe && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) {
-            a.probe[blockIdx.x * 16 + 0] = clock64() - p_start;
-            a.probe[blockIdx.x * 16 + 1] = p_wait;
-        }
-#endif
-        (void)p_wait;
     } else if (warp == 1) {
         // ---- MMA issue: the warp runs the loop (waits are warp-uniform), one elected lane issues
         if (n_ang > 0) {
@@ -344,48 +310,44 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
             int it = 0;
             long long p_full = 0, p_free = 0, p_issue = 0;
             PROBE_T0(p_start);
-            for (int g0 = 0; g0 < n_ang; g0 += 32) {
-                const TcBatch bt = tc_batch(g0, n_ang, dX, dY, a);
-                for (int i = 0; i < bt.n; ++i) {
-                    const int g = g0 + i, ab = a.a0 + g;
-                    const int lb = ab / kP - blk0, acc = lb & 1;
-                    const int nk = 1 + ((bt.two >> i) & 1);
-                    for (int ks = 0; ks < nk; ++ks, ++it) {
-                        const int s = it % kS;
-                        const bool first = ks == 0 && (g == 0 || ab % kP == 0);
-                        const bool last = ks == nk - 1 && (g == n_ang - 1 || (ab + 1) % kP == 0);
-                        PROBE_T0(q0);
-#ifndef TF_TC_PROBE_NO_ACCFREE  // probe builds only
-                        if (first && lb >= 2) mbar_wait(&accfree[acc], (uint32_t)((lb >> 1) - 1) & 1u);
-#endif
-                        PROBE_ADD(p_free, q0);
-                        PROBE_T0(q1);
+            // the loop does no index arithmetic of its own: each item's flags come with it (s_ctl),
+            // so the warp returns to the next full-barrier wait right after issuing
+            for (;; ++it) {
+                const int s = it & (kS - 1);
+                PROBE_T0(q1);
 #ifndef TF_TC_PROBE_MMA_NOWAIT  // probe builds only: MMAs on whatever the slot holds
-                        mbar_wait(&full[s], (uint32_t)(it / kS) & 1u);
+                mbar_wait(&full[s], (uint32_t)(it / kS) & 1u);
 #endif
-                        PROBE_ADD(p_full, q1);
-                        PROBE_T0(q2);
-                        tc_fence_after();
-                        if (elect_one()) {
-                            const uint64_t so = (uint64_t)((s * Cfg::SLOT) >> 4);
-                            const uint64_t th = dT + so, tl = th + (Cfg::TAP_PLANE >> 4);
-                            const uint64_t wh = dW + so, wl = wh + (kWPlane >> 4);
-                            const uint32_t td = tmem + (uint32_t)(acc * NR);
+                PROBE_ADD(p_full, q1);
+                const uint32_t ctl = *reinterpret_cast<volatile uint32_t*>(&s_ctl[s]);
+                const uint32_t acc = (ctl >> 2) & 1u;
+                PROBE_T0(q0);
+#ifndef TF_TC_PROBE_NO_ACCFREE  // probe builds only
+                if (ctl & 16u) mbar_wait(&accfree[acc], (ctl >> 5) & 1u);
+#endif
+                PROBE_ADD(p_free, q0);
+                PROBE_T0(q2);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint64_t so = (uint64_t)((s * Cfg::SLOT) >> 4);
+                    const uint64_t th = dT + so, tl = th + (Cfg::TAP_PLANE >> 4);
+                    const uint64_t wh = dW + so, wl = wh + (kWPlane >> 4);
+                    const uint32_t td = tmem + acc * NR;
 #ifndef TF_TC_PROBE_NO_MMA  // probe builds only: timing without the MMAs
-                            umma_f16_ss(td, wh, th, idesc, first ? 0u : 1u);
-                            umma_f16_ss(td, wl, th, idesc, 1u);
-                            umma_f16_ss(td, wh, tl, idesc, 1u);
+                    umma_f16_ss(td, wh, th, idesc, (ctl & 1u) ? 0u : 1u);
+                    umma_f16_ss(td, wl, th, idesc, 1u);
+                    umma_f16_ss(td, wh, tl, idesc, 1u);
 #else
-                            (void)td, (void)wh, (void)wl, (void)th, (void)tl;
+                    (void)td, (void)wh, (void)wl, (void)th, (void)tl;
 #endif
-                            umma_commit(&empty[s]);  // frees the slot's taps and weights
-                            if (last) umma_commit(&accfull[acc]);
-                        }
-                        __syncwarp();
-                        PROBE_ADD(p_issue, q2);
-                    }
+                    umma_commit(&empty[s]);  // frees the slot's taps and weights
+                    if (ctl & 2u) umma_commit(&accfull[acc]);
                 }
+                __syncwarp();
+                PROBE_ADD(p_issue, q2);
+                if (ctl & 8u) break;
             }
+            ++it;
 #ifdef TF_TC_PROBE
             if (a.probe && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) {
                 a.probe[blockIdx.x * 16 + 2] = clock64() - p_start;
@@ -479,6 +441,28 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
                     PROBE_T0(q4);
                     if (it >= kS) mbar_wait(&empty[s], (uint32_t)((it / kS) - 1) & 1u);
                     PROBE_ADD(p_empty, q4);
+                    if (q == 0 && lane == 0) {
+                        // this item's taps (the group's lane-quadrant-0 warp issues them as soon as the
+                        // slot is free) and the MMA warp's control word: accumulate = 0 (block's first
+                        // item), commit the block (its last), accumulator, end of launch, wait for the
+                        // accumulator's flush (block >= 2) and that wait's phase
+                        const int g = ab - a.a0, lb = ab / kP - blk0;
+                        const bool first = ks == 0 && (g == 0 || ab % kP == 0);
+                        const bool last = ks == nk - 1 && (g == n_ang - 1 || (ab + 1) % kP == 0);
+                        s_ctl[s] = (first ? 1u : 0u) | (last ? 2u : 0u) | ((uint32_t)(lb & 1) << 2) |
+                                   ((ks == nk - 1 && g == n_ang - 1) ? 8u : 0u) | ((first && lb >= 2) ? 16u : 0u) |
+                                   ((uint32_t)(((lb >> 1) - 1) & 1) << 5);
+                        uint8_t* st = ring + s * Cfg::SLOT;
+                        const int ka = 2 * (ab - a.ws_a0);
+#ifdef TF_TC_PROBE_NO_TMA  // probe builds only: timing without the tap loads
+                        mbar_arrive(&full[s]);
+                        (void)st, (void)ka;
+#else
+                        mbar_arrive_expect_tx(&full[s], 2 * Cfg::TAP_PLANE);
+                        tma_load_3d(st, &map, &full[s], 8 * (w.c_lo + kK * ks), zr0 / 8, ka);
+                        tma_load_3d(st + Cfg::TAP_PLANE, &map, &full[s], 8 * (w.c_lo + kK * ks), zr0 / 8, ka + 1);
+#endif
+                    }
                     const uint32_t wa = wslot0 + (uint32_t)(s * Cfg::SLOT);
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {  // 8-channel chunk c: pairs 4c .. 4c + 3

@@ -36,6 +36,7 @@ import ctypes
 
 import numpy as np
 
+from . import _lib
 from ._lib import check, lib
 from .engine import SlabReconstructor
 from .fbp import FilterSpec
@@ -374,3 +375,162 @@ class AngleSplitReconstructor:
 
     def updates(self) -> int:
         return (self.a1 - self.a0) * self.params.n_rows * self.dims.nx * self.dims.ny
+
+
+def chunk_plan(n_proj: int, world: int, rank: int, chunk: int):
+    """Angle chunks [j C, (j + 1) C) of the scan, this rank's share of each
+    (`split_range(len, world)[rank]`, absolute angles) and the offsets of the
+    shares in the rank's concatenated raw input."""
+    chunks = [(a, min(a + chunk, n_proj)) for a in range(0, n_proj, chunk)]
+    parts = []
+    for a, b in chunks:
+        n = b - a  # split_range semantics (the first n % world shares one longer); empty shares allowed
+        q, r = divmod(n, world)
+        s = rank * q + min(rank, r)
+        parts.append((a + s, a + s + q + (1 if rank < r else 0)))
+    offsets = [0]
+    for pa, pb in parts:
+        offsets.append(offsets[-1] + pb - pa)
+    return chunks, parts, offsets
+
+
+class ChunkedZSlabReconstructor:
+    """Z-slabs at C4 scale (4096^3 x 3600 on 4-8 GPUs): the p2p row-slab
+    exchange run over ascending angle chunks, so the receive and tap buffers
+    hold one chunk instead of the whole scan and the raw counts can stream
+    in from pinned host memory.
+
+    The angle range is cut into chunks [j C, (j + 1) C) with C a multiple of
+    16.  For chunk j, rank g filters its share `split_range(len, N)[g]` of
+    the chunk (so every rank ingests and filters 1/N of the projections,
+    north_star); K1's epilogue stores each owner's rows straight into the
+    owner's symmetric-memory receive buffer over NVLink (tf_filter_peers);
+    after a device-side barrier each owner stages the chunk's rows into tap
+    planes with the raw-count bound (tf_bp_tc_stage) and back-projects the
+    chunk on the tensor cores with TF_BP_ACCUMULATE (the last chunk also
+    FINALIZE).  Chunks ascend and start at multiples of 16 angles -- the
+    tensor-core kernel's absolute RN flush blocks -- so the N-GPU volume is
+    bitwise the 1-GPU single-pass volume.  This is the reference's
+    angle-chunked work units (pipeline.py:210-222, partition.py:200-260) on
+    real devices.
+
+    Raw counts: `run(raw)` with a device tensor holding this rank's angles
+    (`rank_angles()`, concatenated), or `run(raw_host)` with a pinned host
+    tensor of the same shape: each chunk's part is copied on a side stream
+    (double-buffered) while the previous chunk back-projects.
+    """
+
+    def __init__(self, params: AcquisitionParams, dims: VolumeDims, spec: FilterSpec | None = None,
+                 i0: float = 1e5, feather_band: int = 32, chunk: int | None = None, group=None, device=None,
+                 budget_bytes: float | None = None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        self.torch = torch
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.params, self.dims = params, dims
+        n_proj, n_rows, n_chan = params.n_proj, params.n_rows, params.n_chan
+        self.device = torch.device(device if device is not None else "cuda")
+        self.slabs = split_range(n_rows, self.world)
+        self.r0, self.r1 = self.slabs[self.rank]
+        k = self.r1 - self.r0
+        kmax = max(e - s for s, e in self.slabs)
+        if chunk is None:
+            # per angle of a chunk: receive rows + tap planes (4 B/sample each) + two raw part buffers
+            per_angle = 4.0 * kmax * n_chan * 2 + 2 * 4.0 * n_rows * n_chan / self.world
+            free = torch.cuda.mem_get_info(self.device)[0] if budget_bytes is None else budget_bytes
+            vol = 4.0 * k * dims.nx * dims.ny
+            chunk = int(max(16, (0.85 * free - vol) / per_angle) // 16 * 16)
+        if chunk % 16:
+            raise ValueError("angle chunks must be multiples of 16 angles (the tensor core flush blocks)")
+        self.C = min(chunk, -(-n_proj // 16) * 16)
+        self.chunks, self.parts, self.offsets = chunk_plan(n_proj, self.world, self.rank, self.C)
+        with torch.cuda.device(self.device):
+            self.local = SlabReconstructor(params, dims, spec, i0, feather_band, rows=(self.r0, self.r1),
+                                           device=self.device, tensor=True, n_angles=self.C)
+            buf = symm.empty(self.C * kmax * n_chan, dtype=torch.float32, device=self.device)
+            self.symm = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
+            self.recv = buf[: self.C * k * n_chan]
+            self.raw_buf = None
+            self.s_h2d = torch.cuda.Stream(self.device)
+        self._row0 = (ctypes.c_int32 * (self.world + 1))(*([s for s, _ in self.slabs] + [n_rows]))
+        self._ptrs = [int(self.symm.buffer_ptrs[s]) for s in range(self.world)]
+        self._ks = [e - s for s, e in self.slabs]
+        self.bound = self.local.tap_bound()
+
+    def rank_angles(self):
+        """This rank's angle ranges, one per chunk; run()'s raw input holds them concatenated."""
+        return list(self.parts)
+
+    def chunk_shape(self):
+        return (self.offsets[-1], self.params.n_rows, self.params.n_chan)
+
+    def _s(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def run(self, raw):
+        """raw: (A, n_rows, n_chan) fp32 counts of rank_angles(), on this device
+        or in pinned host memory -> this rank's volume slab in self.local.vol."""
+        torch = self.torch
+        p = self.params
+        n_chan = p.n_chan
+        host = not raw.is_cuda
+        cur = torch.cuda.current_stream(self.device)
+        if host and self.raw_buf is None:
+            mx = max(pb - pa for pa, pb in self.parts)
+            self.raw_buf = [torch.empty((max(mx, 1), p.n_rows, n_chan), dtype=torch.float32, device=self.device)
+                            for _ in range(2)]
+        k = self.r1 - self.r0
+        free_ev = [None, None]
+        copied = [None, None]
+
+        def copy(j):
+            b = j % 2
+            pa, pb = self.parts[j]
+            if j < 2:
+                self.s_h2d.wait_stream(cur)
+            if free_ev[b] is not None:
+                self.s_h2d.wait_event(free_ev[b])
+            with torch.cuda.stream(self.s_h2d):
+                self.raw_buf[b][: pb - pa].copy_(raw[self.offsets[j]: self.offsets[j + 1]], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.s_h2d)
+            copied[b] = ev
+
+        if host:
+            copy(0)
+        last = len(self.chunks) - 1
+        for j, ((ca, cb), (pa, pb)) in enumerate(zip(self.chunks, self.parts)):
+            if host:
+                if j + 1 <= last:
+                    copy(j + 1)
+                cur.wait_event(copied[j % 2])
+                src = self.raw_buf[j % 2][: pb - pa]
+            else:
+                src = raw[self.offsets[j]: self.offsets[j + 1]]
+            # owners finished staging the previous chunk out of their receive buffers
+            self.symm.barrier(channel=0)
+            if pb > pa:
+                # slab s's rows of my part land in rank s's buffer at the part's angle offset in the chunk
+                dst = (ctypes.c_void_p * self.world)(*[self._ptrs[s] + (pa - ca) * self._ks[s] * n_chan * 4
+                                                       for s in range(self.world)])
+                check(lib().tf_filter_peers(self.local.fplan.handle, ctypes.c_void_p(src.data_ptr()),
+                                            (pb - pa) * p.n_rows, self.local.i0, p.n_rows, self.world, self._row0,
+                                            dst, self._s()))
+            if host:
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                free_ev[j % 2] = ev
+            self.symm.barrier(channel=0)  # every rank's stores into my buffer have landed
+            n = cb - ca
+            self.local.stage_rows(self.recv[: n * k * n_chan].view(n, k, n_chan), rows_per_angle=k, r0=0,
+                                  a0=0, a1=n, t_bound=self.bound)
+            flags = (_lib.TF_BP_ACCUMULATE if j else 0) | (_lib.TF_BP_FINALIZE if j == last else 0)
+            self.local.backproject(ca, cb, flags=flags, taps_a0=ca, taps_a1=cb)
+        return self.local.vol
+
+    def updates(self) -> int:
+        return self.local.updates()

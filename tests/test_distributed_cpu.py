@@ -78,3 +78,57 @@ def test_exchange_layout_bytes():
     assert sum(ins) == 225 * 2048 * 2048
     assert sum(outs) == 1800 * 256 * 2048
     assert row0 == [0, 256, 512, 768, 1024, 1280, 1536, 1792, 2048]
+
+
+def _chunk_worker(rank, world, port, shape, chunk, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2505_13955_b200.distributed import chunk_plan, exchange
+        from paper_2505_13955_b200.geometry import split_range
+
+        n_proj, n_rows, n_chan = shape
+        full = _full(*shape)
+        slabs = split_range(n_rows, world)
+        r0, r1 = slabs[rank]
+        chunks, parts, offsets = chunk_plan(n_proj, world, rank, chunk)
+        plans = [chunk_plan(n_proj, world, r, chunk) for r in range(world)]
+        raw = torch.cat([full[a:b] for a, b in parts]) if offsets[-1] else full[:0]
+        assert raw.shape[0] == offsets[-1]
+        ok = True
+        for j, ((ca, cb), (pa, pb)) in enumerate(zip(chunks, parts)):
+            mine = raw[offsets[j]: offsets[j + 1]]  # this rank's part, as run() slices its input
+            send = torch.cat([mine[:, s:e].reshape(-1) for s, e in slabs])
+            ins = [(pb - pa) * (e - s) * n_chan for s, e in slabs]
+            outs = [(plans[r][1][j][1] - plans[r][1][j][0]) * (r1 - r0) * n_chan for r in range(world)]
+            recv = torch.empty(sum(outs))
+            exchange(send, recv, ins, outs)
+            # rank r's rows land at its part's angle offset in the chunk (run()'s dst pointers)
+            for r in range(world):
+                qa, qb = plans[r][1][j]
+                off = (qa - ca) * (r1 - r0) * n_chan
+                ok &= off == sum(outs[:r])
+            ok &= torch.equal(recv, full[ca:cb, r0:r1].reshape(-1))
+            ok &= ca % 16 == 0 and all(plans[r][0][j] == (ca, cb) for r in range(world))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shape,chunk", [(3, (50, 11, 5), 16), (2, (100, 10, 6), 32)])
+def test_chunked_zslab_exchange_plan(world, shape, chunk):
+    """ChunkedZSlabReconstructor's host logic (chunk_plan + the receive
+    offsets run() uses for K1's peer stores): every owner's receive buffer
+    holds exactly the chunk's angles of its rows, angle-ordered, and every
+    chunk starts at a multiple of 16 angles."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chunk_worker, args=(r, world, port, shape, chunk, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res

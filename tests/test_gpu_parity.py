@@ -470,8 +470,10 @@ def test_filter_slab_map_matches_host_restatement(F):
 
 
 def test_multi_gpu_zslab_bitwise(F):
-    """torchrun over all visible GPUs (>= 2): the z-slab NCCL path (both
-    exchanges) reproduces the 1-GPU volume bit for bit."""
+    """torchrun over all visible GPUs (>= 2): every z-slab exchange (NCCL
+    all-to-all / all-gather, NVLink p2p stores, and the angle-chunked p2p
+    path with device or pinned-host raw counts) reproduces the 1-GPU volume
+    of the same K2 bit for bit."""
     import os
     import subprocess
     import sys
@@ -482,7 +484,7 @@ def test_multi_gpu_zslab_bitwise(F):
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for i, mode in enumerate(("alltoall", "allgather", "p2p", "p2p-zblocked")):
+    for i, mode in enumerate(("alltoall", "allgather", "p2p", "p2p-zblocked", "chunked", "chunked-host")):
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
                "--master-addr", "127.0.0.1", "--master-port", str(29500 + i),
                os.path.join(root, "tools", "mgpu_check.py"), "--exchange", mode]

@@ -11,7 +11,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import torch.distributed as dist
 
-from paper_2505_13955_b200.distributed import AngleSplitReconstructor, ZSlabReconstructor
+from paper_2505_13955_b200.distributed import (AngleSplitReconstructor, ChunkedZSlabReconstructor,
+                                                ZSlabReconstructor)
 from paper_2505_13955_b200.engine import SlabReconstructor, phantom_raw
 from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
 
@@ -28,10 +29,19 @@ p = AcquisitionParams(n_proj=n_proj, n_rows=rows, n_chan=n, pixel_pitch=12.0)
 d = VolumeDims(n, n, rows, voxel_pitch=12.0)
 if args.exchange.startswith("angles-"):
     z = AngleSplitReconstructor(p, d, i0=1e5, reduce=args.exchange[len("angles-"):], device=dev)
+elif args.exchange.startswith("chunked"):  # angle-chunked p2p z-slabs (48-angle chunks), device or host input
+    z = ChunkedZSlabReconstructor(p, d, i0=1e5, chunk=48, device=dev)
 else:
     z = ZSlabReconstructor(p, d, i0=1e5, exchange_mode=args.exchange, device=dev)
 chunk = torch.empty(z.chunk_shape(), device=dev)
-phantom_raw(p, d, chunk, a0=z.a0, a1=z.a1)
+if args.exchange.startswith("chunked"):
+    for (pa, pb), o in zip(z.rank_angles(), z.offsets):
+        if pb > pa:
+            phantom_raw(p, d, chunk[o: o + pb - pa], a0=pa, a1=pb)
+    if args.exchange == "chunked-host":
+        chunk = chunk.cpu().pin_memory()
+else:
+    phantom_raw(p, d, chunk, a0=z.a0, a1=z.a1)
 vol = z.run(chunk)
 vol = z.run(chunk)  # a second step exercises the buffer-reuse ordering
 torch.cuda.synchronize()
@@ -46,6 +56,8 @@ if rank == 0:
     # the same K2 kind: tensor cores for the natural-row exchanges, the CUDA-core kernel for the
     # z-blocked landings and the angle-split reduce epilogue
     tensor = bool(getattr(getattr(z, "local", None), "tensor", False))
+    if args.exchange.startswith("chunked"):
+        print(f"chunks {z.chunks}")
     ref = SlabReconstructor(p, d, i0=1e5, tensor=tensor).run(full_raw)
     got = torch.cat([g[: e - s] for g, (s, e) in zip(gathered, z.slabs)])
     same = torch.equal(got, ref)

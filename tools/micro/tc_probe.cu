@@ -7,7 +7,11 @@
 #ifndef TF_TC_NOPROBE  // -DTF_TC_NOPROBE: the same experiment knobs, uninstrumented timing
 #define TF_TC_PROBE 1
 #endif
+#ifdef TF_TC_SRC  // an alternative K2-TC source (A/B timing against an older revision)
+#include TF_TC_SRC
+#else
 #include "../../paper_2505_13955_b200/csrc/bp_tc.cu"
+#endif
 
 extern "C" TF_API int tf_bp_tc_probe(void* buf) {
 #ifdef TF_TC_PROBE
