@@ -97,12 +97,21 @@ typedef struct {
     const double *w;
     double *out;
     int n_proj, n_rows, n_chan, nx, ny, a0, a1, x0, x1, y0, y1, use_f32;
+    int n_bands, band;  /* work unit = (detector row, band of `band` image rows) */
     double step, cx, cy, sc, axis, R2, sc2;
 } bp_ctx;
 
-/* One detector row == one volume slice (geometry.py:134-139). */
-static void bp_row(long r, void *vctx) {
-    const bp_ctx *g = (const bp_ctx *)vctx;
+/* One detector row == one volume slice (geometry.py:134-139); a work unit is
+ * one slice's band of image rows [y0 + b*band, ...), so a single slice also
+ * spreads over the threads.  Every voxel still sums its angles in ascending
+ * order exactly as fbp.py:233-245, so the split does not change any bit. */
+static void bp_row(long u, void *vctx) {
+    const bp_ctx *g0 = (const bp_ctx *)vctx;
+    const long r = u / g0->n_bands;
+    bp_ctx gb = *g0;
+    gb.y0 = g0->y0 + (int)(u % g0->n_bands) * g0->band;
+    gb.y1 = gb.y0 + g0->band < g0->y1 ? gb.y0 + g0->band : g0->y1;
+    const bp_ctx *g = &gb;
     int n = g->n_chan, tw = g->x1 - g->x0, th = g->y1 - g->y0;
     size_t plane = (size_t)g->nx * g->ny;
     double *acc = (double *)calloc((size_t)tw * th, sizeof(double));
@@ -198,7 +207,13 @@ int oracle_back_project(const double *sino, int n_proj, int n_rows, int n_chan,
     double R = offset_chan != 0 ? half + fabs((double)offset_chan) : half;
     g.R2 = R * R;
     g.sc2 = g.sc * g.sc;
-    parallel_for(n_rows, n_threads, bp_row, &g);
+    /* enough units for the threads even for one slice: bands of >= 16 image rows */
+    int nt = n_threads > 0 ? n_threads : 1;
+    int want = (4 * nt + n_rows - 1) / n_rows;
+    g.band = (y1 - y0 + want - 1) / want;
+    if (g.band < 16) g.band = 16;
+    g.n_bands = (y1 - y0 + g.band - 1) / g.band;
+    parallel_for((long)n_rows * g.n_bands, n_threads, bp_row, &g);
     free(w);
     return 0;
 }
