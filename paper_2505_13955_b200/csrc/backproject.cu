@@ -577,6 +577,7 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
         };
         std::stable_sort(act.begin(), act.end(), [&](int a, int b) { return morton(a) < morton(b); });
         p->n_active[shape] = (int)act.size();
+        p->n_tiles[shape] = ntx * nty;
         act.insert(act.end(), inact.begin(), inact.end());
         orders[shape] = act;
     }
@@ -589,6 +590,8 @@ extern "C" int tf_bp_plan_create(const tf_geometry* g, int feather_band, tf_bp_p
     for (int i = 0; i < g->n_chan; ++i) wf[i] = (float)w[i];
     cudaError_t e = cudaMalloc(&p->d_trig, sizeof(double2) * g->n_proj);
     for (int s = 0; s < kNumTileShapes && e == cudaSuccess; ++s) {
+        p->h_order[s] = new int[orders[s].size()];
+        std::copy(orders[s].begin(), orders[s].end(), p->h_order[s]);
         e = cudaMalloc(&p->d_order[s], sizeof(int) * orders[s].size());
         if (e == cudaSuccess)
             e = cudaMemcpy(p->d_order[s], orders[s].data(), sizeof(int) * orders[s].size(), cudaMemcpyHostToDevice);
@@ -609,7 +612,10 @@ extern "C" int tf_bp_plan_destroy(tf_bp_plan* p) {
     if (!p) return TF_OK;
     cudaFree(p->d_trig);
     cudaFree(p->d_w);
-    for (int s = 0; s < kNumTileShapes; ++s) cudaFree(p->d_order[s]);
+    for (int s = 0; s < kNumTileShapes; ++s) {
+        cudaFree(p->d_order[s]);
+        delete[] p->h_order[s];
+    }
     delete p;
     return TF_OK;
 }

@@ -21,7 +21,9 @@ struct tf_bp_plan {
     double2* d_trig;  // (cos, sin) of k * (span / n_proj), fp64 libm, per angle
     float* d_w;       // feather weights (fp32, as numpy casts them)
     int* d_order[kNumTileShapes];  // tile launch order (Morton, FoV-active first) per tile shape
+    int* h_order[kNumTileShapes];  // host copies (per-call tile lists of restricted tensor-core calls)
     int n_active[kNumTileShapes];
+    int n_tiles[kNumTileShapes];
     double cx, cy, scale, axis, R2, sc2;
     float angle_wf;
 };

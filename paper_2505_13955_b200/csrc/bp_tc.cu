@@ -59,14 +59,25 @@ namespace {
 constexpr int kTX = kTileShape[kShapeTc][0], kTY = kTileShape[kShapeTc][1], kMV = kTX * kTY;
 constexpr int kM = 128;         // MMA M = TMEM lanes: voxel rows of the tile
 constexpr int kK = 16;          // channels per item (one fp16 MMA K-step)
-constexpr int kS = 8;           // ring depth in items
-constexpr int kP = 16;          // angles per accumulator block (absolute angle index / kP)
+#ifndef TF_TC_S
+#define TF_TC_S 8
+#endif
+constexpr int kS = TF_TC_S;     // ring depth in items
+#ifndef TF_TC_P
+#define TF_TC_P 16
+#endif
+constexpr int kP = TF_TC_P;     // angles per accumulator block (absolute angle index / kP)
 constexpr int kG = 4;           // weight groups of 4 warps
 constexpr int kThreads = 64 + 128 * kG;
 #ifndef TF_TC_LAG
-#define TF_TC_LAG 8
+#define TF_TC_LAG 14
 #endif
-constexpr int kLag = TF_TC_LAG;  // a group flushes block j once it produces angle >= end(j) + kLag
+// a group flushes block j before it produces its first angle >= end(j) + kLag: by then the group's own
+// slot waits proved block j's MMAs retired (no wait on accfull), and every group still flushes before
+// the MMA warp needs the accumulator again at angle end(j) + kP (kLag <= kP: no group has to wait for
+// a slot the MMA warp could only free after that)
+constexpr int kLag = TF_TC_LAG;
+static_assert(kLag <= kP, "a block is flushed before its accumulator is needed again");
 constexpr int kWPlane = kM * kK * 2;   // one fp16 plane of a slot's W tile (4 KB)
 constexpr float kOneStep = 14.9f;      // window test (fp32 margin below 15)
 static_assert(kMV <= kM, "tile fits the MMA's M");
@@ -83,7 +94,9 @@ struct TcCfg {
 
 struct TCArgs {
     const double2* trig;
-    const int* order;
+    const int* tiles;   // work list: FoV-active tiles (Morton order) of one z-block
+    int n_tiles, n_work;  // tiles per z-block; work items = z-blocks x n_tiles
+    unsigned* sync;     // grid-barrier counter of the lockstep rounds (workspace header, zeroed per call)
     const int* e_rows;  // per-row tap exponent (workspace header)
     float* vol;
     int a0, a1, ws_a0, n_rows, nx, ny;
@@ -208,61 +221,41 @@ __device__ __forceinline__ bool tc_outside_fov(int x, int y, const TCArgs& a) {
     return rr > a.R2;
 }
 
+// Persistent, lockstep: the grid is one CTA per SM (cooperative launch) and
+// CTA b processes the work items w = r G + b (r = 0, 1, ...) of the list of
+// (z-block, FoV-active tile) pairs, z-block outer, tiles in Morton order.  A
+// grid-wide barrier between rounds keeps the G CTAs of a round -- a compact
+// patch of Morton-adjacent tiles -- at the same angle within a few percent,
+// so the patch's tap windows are fetched from DRAM once and re-read from L2
+// by its other CTAs (a grid of one CTA per tile let resident CTAs sit at
+// unrelated angles: 2.4 TB of DRAM reads per C3 volume, 62% L2 hits).  The
+// ring slots, their phases and the accumulator ping-pong run on across the
+// rounds; each round resets the RN master sum and ends with the epilogue.
 template <int NR>
 __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constant__ CUtensorMap map, const TCArgs a) {
     using Cfg = TcCfg<NR>;
     constexpr int NC = Cfg::NC;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
-    const int tx = tile % a.ntx, ty = tile / a.ntx;
-    const int X0 = tx * kTX, Y0 = ty * kTY;
-    const int zr0 = blockIdx.y * NR;
-    const int xe = min(X0 + kTX, a.nx), ye = min(Y0 + kTY, a.ny);
-    const int ux0 = max(X0, a.x0), ux1 = min(xe, a.x1);
-    const int uy0 = max(Y0, a.y0), uy1 = min(ye, a.y1);
-    if (ux0 >= ux1 || uy0 >= uy1) return;
     const size_t plane = (size_t)a.nx * a.ny;
-    {
-        // every voxel of the tile outside the FoV: skip the angle loop (fp64 test on the voxel
-        // nearest the rotation centre and its neighbours, as the CUDA-core kernel)
-        int nxv = (int)fmin(fmax(rint(a.cx), (double)X0), (double)(xe - 1));
-        int nyv = (int)fmin(fmax(rint(a.cy), (double)Y0), (double)(ye - 1));
-        bool all_out = true;
-        for (int ddx = -1; ddx <= 1; ++ddx)
-            for (int ddy = -1; ddy <= 1; ++ddy) {
-                int xx = min(max(nxv + ddx, X0), xe - 1), yy = min(max(nyv + ddy, Y0), ye - 1);
-                all_out = all_out && tc_outside_fov(xx, yy, a);
-            }
-        if (all_out) {
-            if (a.flags & TF_BP_FINALIZE) {
-                const int nz = min(NR, a.n_rows - zr0);
-                for (int i = threadIdx.x; i < kMV * nz; i += blockDim.x) {
-                    int z = i / kMV, r = i % kMV;
-                    int x = X0 + (r % kTX), y = Y0 + (r / kTX);
-                    if (x >= ux0 && x < ux1 && y >= uy0 && y < uy1)
-                        a.vol[(size_t)(zr0 + z) * plane + (size_t)y * a.nx + x] = 0.f;
-                }
-            }
-            return;
-        }
-    }
+    const int G = gridDim.x;
+    const int n_rounds = a.n_work > (int)blockIdx.x ? (a.n_work - 1 - (int)blockIdx.x) / G + 1 : 0;
 
     uint8_t* const ring = smem;  // [kS] slots: T_hi, T_lo, W_hi, W_lo
-    float* s_up = reinterpret_cast<float*>(ring + kS * Cfg::SLOT);  // per row 2^e and 2^-e (exact scalings)
+    float* s_up = reinterpret_cast<float*>(ring + kS * Cfg::SLOT);  // per row of the round: 2^e and 2^-e
     float* s_dn = s_up + NR;
     uint64_t* full = reinterpret_cast<uint64_t*>(s_dn + NR);
     uint64_t* empty = full + kS;
     uint64_t* accfull = empty + kS;   // [2]: block's MMAs done -> flush
     uint64_t* accfree = accfull + 2;  // [2]: block flushed by all 16 weight warps -> accumulator reusable
     uint32_t* tslot = reinterpret_cast<uint32_t*>(accfree + 2);
-    uint32_t* s_ctl = tslot + 4;  // [kS]: the slot's item control word (written by the TMA warp)
+    uint32_t* s_ctl = tslot + 4;  // [kS]: the slot's item control word (written by its producer group)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kS; ++s) {
 #ifdef TF_TC_PROBE_W_NONE  // probe builds only: weight warps absent from the ring
             mbar_init(&full[s], 1);
 #else
-            mbar_init(&full[s], 1 + 4);  // TMA arrive.expect_tx + the owning group's 4 warps
+            mbar_init(&full[s], 1 + 4);  // the group's TMA arrive.expect_tx + its 4 warps
 #endif
             mbar_init(&empty[s], 1);     // MMA commit
         }
@@ -271,11 +264,6 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
             mbar_init(&accfree[b], 4 * kG);
         }
         fence_barrier_init();
-    }
-    for (int i = threadIdx.x; i < NR; i += blockDim.x) {
-        const int e = zr0 + i < a.n_rows ? a.e_rows[zr0 + i] : 0;  // |e| <= 100: normal powers of two
-        s_up[i] = __int_as_float((127 + e) << 23);
-        s_dn[i] = __int_as_float((127 - e) << 23);
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
@@ -289,15 +277,12 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
     const int n_ang = a.a1 - a.a0;
     const int blk0 = a.a0 / kP;  // first absolute block
     const int n_blk = n_ang > 0 ? (a.a1 - 1) / kP - blk0 + 1 : 0;
-    const double dX = (double)X0 - a.cx, dY = (double)Y0 - a.cy;
 
     if (warp == 0) {
-        // the TMA loads are issued by the weight groups with their items (below); this warp only
-        // prefetches the tensor map
         if (lane == 0) tma_prefetch_desc(&map);
     } else if (warp == 1) {
         // ---- MMA issue: the warp runs the loop (waits are warp-uniform), one elected lane issues
-        if (n_ang > 0) {
+        if (n_ang > 0 && n_rounds > 0) {
             // D f32, A = W f16 K-major (smem), B = T f16 MN-major (smem), M = 128, N = NR
             constexpr uint32_t idesc =
                 (1u << 4) | (1u << 16) | ((uint32_t)(NR >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);
@@ -313,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
             // the loop does no index arithmetic of its own: each item's flags come with it (s_ctl),
             // so the warp returns to the next full-barrier wait right after issuing
             for (;; ++it) {
-                const int s = it & (kS - 1);
+                const int s = it % kS;
                 PROBE_T0(q1);
 #ifndef TF_TC_PROBE_MMA_NOWAIT  // probe builds only: MMAs on whatever the slot holds
                 mbar_wait(&full[s], (uint32_t)(it / kS) & 1u);
@@ -335,7 +320,9 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
                     const uint32_t td = tmem + acc * NR;
 #ifndef TF_TC_PROBE_NO_MMA  // probe builds only: timing without the MMAs
                     umma_f16_ss(td, wh, th, idesc, (ctl & 1u) ? 0u : 1u);
+#ifndef TF_TC_PROBE_NO_WLO  // probe builds only: precision experiment without the W_lo T_hi product
                     umma_f16_ss(td, wl, th, idesc, 1u);
+#endif
                     umma_f16_ss(td, wh, tl, idesc, 1u);
 #else
                     (void)td, (void)wh, (void)wl, (void)th, (void)tl;
@@ -349,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
             }
             ++it;
 #ifdef TF_TC_PROBE
-            if (a.probe && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024) {
+            if (a.probe && lane == 0 && blockIdx.x < 1024) {
                 a.probe[blockIdx.x * 16 + 2] = clock64() - p_start;
                 a.probe[blockIdx.x * 16 + 3] = p_full;
                 a.probe[blockIdx.x * 16 + 4] = p_free;
@@ -372,126 +359,189 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
         const int vx = m % kTX, vy = m / kTX;
         const float fdx = (float)vx, fdy = (float)vy;
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);  // this warp's TMEM lanes
-        const int x = X0 + vx, y = Y0 + vy;
-        const bool inside = real && x >= ux0 && x < ux1 && y >= uy0 && y < uy1;
-        const int zc0 = zr0 + grp * NC;  // first volume row of this thread's master columns
-        float master[NC];
-#pragma unroll
-        for (int j = 0; j < NC; ++j) master[j] = 0.f;
-        if ((a.flags & TF_BP_ACCUMULATE) && inside) {  // continue unscaled partial sums: x 2^e is exact
-            const float* src = a.vol + (size_t)y * a.nx + x;
-#pragma unroll
-            for (int j = 0; j < NC; ++j)
-                if (zc0 + j < a.n_rows) master[j] = src[(size_t)(zc0 + j) * plane] * s_up[grp * NC + j];
-        }
-        auto flush = [&](int lb) {  // master (+)= accumulator of local block lb, round to nearest
-            const int acc = lb & 1;
-            mbar_wait(&accfull[acc], (uint32_t)(lb >> 1) & 1u);
-            tc_fence_after();
-#ifndef TF_TC_PROBE_NO_FLUSH  // probe builds only: timing without the TMEM reads
-#pragma unroll
-            for (int c = 0; c < NC; c += 16) {
-                uint32_t v[16];
-                TC_LD16(tl + (uint32_t)(acc * NR + grp * NC + c), v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                for (int j = 0; j < 16; ++j) master[c + j] = __fadd_rn(master[c + j], __uint_as_float(v[j]));
-            }
-#endif
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&accfree[acc]);
-        };
         const uint32_t wslot0 = smem_u32(ring + 2 * Cfg::TAP_PLANE) + (uint32_t)((m >> 3) * 256 + (m & 7) * 16);
-        int flushed = 0, ibase = 0;
+        int it_round = 0;   // items before this round (every group counts the same sequence)
+        int blk_round = 0;  // accumulator blocks before this round (the ping-pong parity runs on)
         long long p_empty = 0, p_flush = 0;
         PROBE_T0(p_start);
-        for (int g0 = 0; g0 < n_ang; g0 += 32) {
-            const TcBatch bt = tc_batch(g0, n_ang, dX, dY, a);
-            for (int i = grp; i < bt.n; i += kG) {
-                const int ab = a.a0 + g0 + i;
-                // flush the blocks that ended kLag angles ago: this group's slot waits proved
-                // their MMAs retired, so the accfull waits return at once
-                PROBE_T0(q3);
-                while (flushed < n_blk && (blk0 + flushed + 1) * kP + kLag <= ab) flush(flushed++);
-                PROBE_ADD(p_flush, q3);
-                const TcWin w = tc_bcast(bt.w, i);
-                const int nk = 1 + ((bt.two >> i) & 1);
-                const int it0 = ibase + i + __popc(bt.two & ((1u << i) - 1u));
+        for (int r = 0; r < n_rounds; ++r) {
+            const int wi = r * G + (int)blockIdx.x;
+            const int zb = wi / a.n_tiles;
+            const int tile = a.tiles[wi - zb * a.n_tiles];
+            const int X0 = (tile % a.ntx) * kTX, Y0 = (tile / a.ntx) * kTY;
+            const int zr0 = zb * NR;
+            const int xe = min(X0 + kTX, a.nx), ye = min(Y0 + kTY, a.ny);
+            const int ux0 = max(X0, a.x0), ux1 = min(xe, a.x1);
+            const int uy0 = max(Y0, a.y0), uy1 = min(ye, a.y1);
+            const double dX = (double)X0 - a.cx, dY = (double)Y0 - a.cy;
+            const int x = X0 + vx, y = Y0 + vy;
+            const bool inside = real && x >= ux0 && x < ux1 && y >= uy0 && y < uy1;
+            const int zc0 = zr0 + grp * NC;  // first volume row of this thread's master columns
+            // this round's per-row scalings (the previous round's epilogue is done with them)
+            named_bar_sync(1, 128 * kG);
+            for (int i = threadIdx.x - 64; i < NR; i += 128 * kG) {
+                const int e = zr0 + i < a.n_rows ? a.e_rows[zr0 + i] : 0;  // |e| <= 100: normal powers of two
+                s_up[i] = __int_as_float((127 + e) << 23);
+                s_dn[i] = __int_as_float((127 - e) << 23);
+            }
+            named_bar_sync(1, 128 * kG);
+            float master[NC];
+#pragma unroll
+            for (int j = 0; j < NC; ++j) master[j] = 0.f;
+            if ((a.flags & TF_BP_ACCUMULATE) && inside) {  // continue unscaled partial sums: x 2^e is exact
+                const float* src = a.vol + (size_t)y * a.nx + x;
+#pragma unroll
+                for (int j = 0; j < NC; ++j)
+                    if (zc0 + j < a.n_rows) master[j] = src[(size_t)(zc0 + j) * plane] * s_up[grp * NC + j];
+            }
+            auto flush = [&](int lb) {  // master (+)= accumulator of block lb of the round, round to nearest
+                const int gb = blk_round + lb, acc = gb & 1;
+                mbar_wait(&accfull[acc], (uint32_t)(gb >> 1) & 1u);
+                tc_fence_after();
+#ifndef TF_TC_PROBE_NO_FLUSH  // probe builds only: timing without the TMEM reads
+#pragma unroll
+                for (int c = 0; c < NC; c += 16) {
+                    uint32_t v[16];
+                    TC_LD16(tl + (uint32_t)(acc * NR + grp * NC + c), v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) master[c + j] = __fadd_rn(master[c + j], __uint_as_float(v[j]));
+                }
+#endif
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&accfree[acc]);
+            };
+            const bool last_round = r == n_rounds - 1;
+            int flushed = 0, ibase = it_round;
+            for (int g0 = 0; g0 < n_ang; g0 += 32) {
+                const TcBatch bt = tc_batch(g0, n_ang, dX, dY, a);
+                for (int i = grp; i < bt.n; i += kG) {
+                    const int ab = a.a0 + g0 + i;
+                    // flush the blocks that ended kLag angles ago: this group's slot waits proved
+                    // their MMAs retired, so the accfull waits return at once
+                    PROBE_T0(q3);
+                    while (flushed < n_blk && (blk0 + flushed + 1) * kP + kLag <= ab) flush(flushed++);
+                    PROBE_ADD(p_flush, q3);
+                    const TcWin w = tc_bcast(bt.w, i);
+                    const int nk = 1 + ((bt.two >> i) & 1);
+                    const int it0 = ibase + i + __popc(bt.two & ((1u << i) - 1u));
 #ifdef TF_TC_PROBE_W_IDLE  // probe builds only: no weight arithmetic
-                const float t = 0.f;
+                    const float t = 0.f;
 #else
-                const float t = fmaxf(fmaf(fdy, w.C, fmaf(fdx, w.B, w.F0)), 0.f);
+                    const float t = fmaxf(fmaf(fdy, w.C, fmaf(fdx, w.B, w.F0)), 0.f);
 #endif
-                const float fl = floorf(t);
-                const float f = t - fl;
-                const float g0w = 1.f - f;
-                const __half h0 = __float2half_rn(g0w), h1 = __float2half_rn(f);
-                const __half l0 = __float2half_rn(g0w - __half2float(h0)), l1 = __float2half_rn(f - __half2float(h1));
-                const __half z = __ushort_as_half(0);
-                const int o0 = (int)fl;
-                const bool odd = o0 & 1;
-                const uint32_t Xh = odd ? pack_h2(z, h0) : pack_h2(h0, h1), Yh = odd ? pack_h2(h1, z) : 0u;
-                const uint32_t Xl = odd ? pack_h2(z, l0) : pack_h2(l0, l1), Yl = odd ? pack_h2(l1, z) : 0u;
-                for (int ks = 0; ks < nk; ++ks) {
-                    const int it = it0 + ks, s = it % kS;
-                    // tap o = floor(t) - 16 ks of this item's window; the pair (2j, 2j + 1) of
-                    // halves holding it is jo = o >> 1 (o = -1: only f lands, in pair 0)
-                    const int jo = real ? (o0 - kK * ks) >> 1 : -8;
-                    PROBE_T0(q4);
-                    if (it >= kS) mbar_wait(&empty[s], (uint32_t)((it / kS) - 1) & 1u);
-                    PROBE_ADD(p_empty, q4);
-                    if (q == 0 && lane == 0) {
-                        // this item's taps (the group's lane-quadrant-0 warp issues them as soon as the
-                        // slot is free) and the MMA warp's control word: accumulate = 0 (block's first
-                        // item), commit the block (its last), accumulator, end of launch, wait for the
-                        // accumulator's flush (block >= 2) and that wait's phase
-                        const int g = ab - a.a0, lb = ab / kP - blk0;
-                        const bool first = ks == 0 && (g == 0 || ab % kP == 0);
-                        const bool last = ks == nk - 1 && (g == n_ang - 1 || (ab + 1) % kP == 0);
-                        s_ctl[s] = (first ? 1u : 0u) | (last ? 2u : 0u) | ((uint32_t)(lb & 1) << 2) |
-                                   ((ks == nk - 1 && g == n_ang - 1) ? 8u : 0u) | ((first && lb >= 2) ? 16u : 0u) |
-                                   ((uint32_t)(((lb >> 1) - 1) & 1) << 5);
-                        uint8_t* st = ring + s * Cfg::SLOT;
-                        const int ka = 2 * (ab - a.ws_a0);
+                    const float fl = floorf(t);
+                    const float f = t - fl;
+                    const float g0w = 1.f - f;
+                    const __half h0 = __float2half_rn(g0w), h1 = __float2half_rn(f);
+                    const __half l0 = __float2half_rn(g0w - __half2float(h0)), l1 = __float2half_rn(f - __half2float(h1));
+                    const __half z = __ushort_as_half(0);
+                    const int o0 = (int)fl;
+                    const bool odd = o0 & 1;
+                    const uint32_t Xh = odd ? pack_h2(z, h0) : pack_h2(h0, h1), Yh = odd ? pack_h2(h1, z) : 0u;
+                    const uint32_t Xl = odd ? pack_h2(z, l0) : pack_h2(l0, l1), Yl = odd ? pack_h2(l1, z) : 0u;
+                    for (int ks = 0; ks < nk; ++ks) {
+                        const int it = it0 + ks, s = it % kS;
+                        // tap o = floor(t) - 16 ks of this item's window; the pair (2j, 2j + 1) of
+                        // halves holding it is jo = o >> 1 (o = -1: only f lands, in pair 0)
+                        const int jo = real ? (o0 - kK * ks) >> 1 : -8;
+                        PROBE_T0(q4);
+                        if (it >= kS) mbar_wait(&empty[s], (uint32_t)((it / kS) - 1) & 1u);
+                        PROBE_ADD(p_empty, q4);
+                        if (q == 0 && lane == 0) {
+                            // this item's taps (the group's lane-quadrant-0 warp issues them as soon as
+                            // the slot is free) and the MMA warp's control word: accumulate = 0 (block's
+                            // first item), commit the block (its last), accumulator, end of the CTA's
+                            // work, wait for the accumulator's flush (from the third block on) and that
+                            // wait's phase
+                            const int g = ab - a.a0, gb = blk_round + ab / kP - blk0;
+                            const bool first = ks == 0 && (g == 0 || ab % kP == 0);
+                            const bool last = ks == nk - 1 && (g == n_ang - 1 || (ab + 1) % kP == 0);
+                            s_ctl[s] = (first ? 1u : 0u) | (last ? 2u : 0u) | ((uint32_t)(gb & 1) << 2) |
+                                       ((last_round && ks == nk - 1 && g == n_ang - 1) ? 8u : 0u) |
+                                       ((first && gb >= 2) ? 16u : 0u) | ((uint32_t)(((gb >> 1) - 1) & 1) << 5);
+                            uint8_t* st = ring + s * Cfg::SLOT;
+                            const int ka = 2 * (ab - a.ws_a0);
 #ifdef TF_TC_PROBE_NO_TMA  // probe builds only: timing without the tap loads
-                        mbar_arrive(&full[s]);
-                        (void)st, (void)ka;
+                            mbar_arrive(&full[s]);
+                            (void)st, (void)ka;
 #else
-                        mbar_arrive_expect_tx(&full[s], 2 * Cfg::TAP_PLANE);
-                        tma_load_3d(st, &map, &full[s], 8 * (w.c_lo + kK * ks), zr0 / 8, ka);
-                        tma_load_3d(st + Cfg::TAP_PLANE, &map, &full[s], 8 * (w.c_lo + kK * ks), zr0 / 8, ka + 1);
+                            mbar_arrive_expect_tx(&full[s], 2 * Cfg::TAP_PLANE);
+                            tma_load_3d(st, &map, &full[s], 8 * (w.c_lo + kK * ks), zr0 / 8, ka);
+                            tma_load_3d(st + Cfg::TAP_PLANE, &map, &full[s], 8 * (w.c_lo + kK * ks), zr0 / 8,
+                                        ka + 1);
 #endif
-                    }
-                    const uint32_t wa = wslot0 + (uint32_t)(s * Cfg::SLOT);
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {  // 8-channel chunk c: pairs 4c .. 4c + 3
-                        uint32_t vh[4], vl[4];
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int jj = 4 * c + j;
-                            vh[j] = jj == jo ? Xh : (jj == jo + 1 ? Yh : 0u);
-                            vl[j] = jj == jo ? Xl : (jj == jo + 1 ? Yl : 0u);
                         }
+                        const uint32_t wa = wslot0 + (uint32_t)(s * Cfg::SLOT);
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) {  // 8-channel chunk c: pairs 4c .. 4c + 3
+                            uint32_t vh[4], vl[4];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const int jj = 4 * c + j;
+                                vh[j] = jj == jo ? Xh : (jj == jo + 1 ? Yh : 0u);
+                                vl[j] = jj == jo ? Xl : (jj == jo + 1 ? Yl : 0u);
+                            }
 #ifndef TF_TC_PROBE_NO_WEIGHTS  // probe builds only: timing without the weight stores
-                        sts128(wa + 128 * c, vh[0], vh[1], vh[2], vh[3]);
-                        sts128(wa + kWPlane + 128 * c, vl[0], vl[1], vl[2], vl[3]);
+                            sts128(wa + 128 * c, vh[0], vh[1], vh[2], vh[3]);
+                            sts128(wa + kWPlane + 128 * c, vl[0], vl[1], vl[2], vl[3]);
 #else
-                        if (vh[0] == 0x7fffffffu && vl[3] == 0x7fffffffu) sts128(wa, vh[0], vh[1], vh[2], vh[3]);
+                            if (vh[0] == 0x7fffffffu && vl[3] == 0x7fffffffu) sts128(wa, vh[0], vh[1], vh[2], vh[3]);
 #endif
-                    }
+                        }
 #ifndef TF_TC_PROBE_NO_FENCE  // probe builds only
-                    fence_proxy_async();  // generic-proxy stores -> visible to the tensor core
+                        fence_proxy_async();  // generic-proxy stores -> visible to the tensor core
 #endif
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&full[s]);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&full[s]);
+                    }
+                }
+                ibase += bt.n + __popc(bt.two);
+            }
+            while (flushed < n_blk) flush(flushed++);
+            it_round = ibase;
+            blk_round += n_blk;
+            // ---- epilogue: master x 2^-e -> volume (fbp.py:247-251)
+            if (inside) {
+                const bool fin = (a.flags & TF_BP_FINALIZE) != 0;
+                const bool zero = fin && tc_outside_fov(x, y, a);
+                float* out = a.vol + (size_t)y * a.nx + x;
+#pragma unroll
+                for (int j = 0; j < NC; ++j) {
+                    const int zz = zc0 + j;
+                    if (zz < a.n_rows) {
+                        float val = master[j] * s_dn[grp * NC + j];
+                        if (fin) val = zero ? 0.f : val * a.angle_wf;
+                        out[(size_t)zz * plane] = val;
+                    }
                 }
             }
-            ibase += bt.n + __popc(bt.two);
+            // ---- lockstep: the next round starts when every CTA has finished this one.  Every CTA
+            // counts every round it ran; a CTA with a next round waits for all G of this round (all G
+            // ran round r whenever any CTA has a round r + 1).  A wait far beyond any round's length
+            // means a CTA was never scheduled: trap instead of hanging.
+            named_bar_sync(1, 128 * kG);
+            if (threadIdx.x == 64) {
+                __threadfence();
+                atomicAdd(a.sync, 1u);
+#ifndef TF_TC_PROBE_NO_LOCKSTEP  // probe builds only: rounds without the grid barrier
+                if (!last_round) {
+#else
+                if (false) {
+#endif
+                    const unsigned target = (unsigned)(r + 1) * (unsigned)G;
+                    const long long t0 = clock64();
+                    while (*reinterpret_cast<volatile unsigned*>(a.sync) < target) {
+                        __nanosleep(64);
+                        if (clock64() - t0 > 20000000000LL) __trap();
+                    }
+                    __threadfence();
+                }
+            }
         }
-        while (flushed < n_blk) flush(flushed++);
 #ifdef TF_TC_PROBE
-        if (a.probe && lane == 0 && blockIdx.y == 0 && blockIdx.x < 1024 && (warp == 2 || warp == 14)) {
+        if (a.probe && lane == 0 && blockIdx.x < 1024 && (warp == 2 || warp == 14)) {
             const int o = warp == 2 ? 7 : 10;
             a.probe[blockIdx.x * 16 + o] = clock64() - p_start;
             a.probe[blockIdx.x * 16 + o + 1] = p_empty;
@@ -499,21 +549,6 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
         }
 #endif
         (void)p_empty, (void)p_flush;
-        // ---- epilogue: master x 2^-e -> volume (fbp.py:247-251)
-        if (inside) {
-            const bool fin = (a.flags & TF_BP_FINALIZE) != 0;
-            const bool zero = fin && tc_outside_fov(x, y, a);
-            float* out = a.vol + (size_t)y * a.nx + x;
-#pragma unroll
-            for (int j = 0; j < NC; ++j) {
-                const int zz = zc0 + j;
-                if (zz < a.n_rows) {
-                    float val = master[j] * s_dn[grp * NC + j];
-                    if (fin) val = zero ? 0.f : val * a.angle_wf;
-                    out[(size_t)zz * plane] = val;
-                }
-            }
-        }
     }
 #ifdef TF_TC_PROBE_W_NONE
 probe_done:
@@ -521,6 +556,21 @@ probe_done:
     tc_fence_before();
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS));
+}
+
+// FINALIZE over the tiles wholly outside the field of view (not in the persistent kernel's work
+// list): zeros inside the requested tile (fbp.py:247-250 masks them)
+__global__ void tc_zero_tiles_kernel(float* __restrict__ vol, const int* __restrict__ tiles, int n_tiles, int ntx,
+                                     int nx, int ny, int n_rows, int x0, int x1, int y0, int y1) {
+    const long long per = (long long)kMV * n_rows;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n_tiles * per;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int t = tiles[i / per];
+        const long long r = i % per;
+        const int z = (int)(r / kMV), v = (int)(r % kMV);
+        const int x = (t % ntx) * kTX + v % kTX, y = (t / ntx) * kTY + v / kTX;
+        if (x >= x0 && x < x1 && y >= y0 && y < y1 && x < nx && y < ny) vol[((size_t)z * ny + y) * nx + x] = 0.f;
+    }
 }
 
 // ---- tap planes from natural-layout filtered rows (the fbp.back_project input) -------------
@@ -605,7 +655,7 @@ __global__ void tc_stage_kernel(const float* __restrict__ sino, const float* __r
 // Items (MMA K-steps) a launch issues: the same window test as bp_tc_kernel, per FoV-active tile
 // and angle (one block per tile; every z-block issues the same items).
 __global__ void tc_work_kernel(TCArgs a, int n_active, unsigned long long* __restrict__ out) {
-    const int tile = a.order[blockIdx.x];
+    const int tile = a.tiles[blockIdx.x];
     const int X0 = (tile % a.ntx) * kTX, Y0 = (tile / a.ntx) * kTY;
     const double dX = (double)X0 - a.cx, dY = (double)Y0 - a.cy;
     unsigned long long n = 0;
@@ -616,21 +666,25 @@ __global__ void tc_work_kernel(TCArgs a, int n_active, unsigned long long* __res
 }
 
 // ---- workspace geometry ----------------------------------------------------------------------
-// [header: int32 e[n_rows] | uint32 rowmax[n_rows], padded to 1 KB][taps: angle-major planes]
-int64_t tc_header_bytes(int n_rows) { return ((int64_t)8 * n_rows + 1023) / 1024 * 1024; }
+// [header: int32 e[n_rows] | uint32 rowmax[n_rows] | grid-barrier counter (64 B) | int32 tile list of a
+//  restricted call (one per tile of the plane), padded to 1 KB][taps: angle-major planes]
+int64_t tc_header_bytes(const tf_bp_plan* p, int n_rows) {
+    return ((int64_t)8 * n_rows + 64 + 4 * (int64_t)p->n_tiles[kShapeTc] + 1023) / 1024 * 1024;
+}
 int64_t tc_angle_bytes(const tf_bp_plan* p, int n_rows) {
     return (int64_t)2 * ((n_rows + 7) / 8) * p->g.n_chan * 16;
 }
 int* tc_exp_ptr(void* ws) { return static_cast<int*>(ws); }
 unsigned* tc_max_ptr(void* ws, int n_rows) { return reinterpret_cast<unsigned*>(static_cast<int*>(ws) + n_rows); }
-__half* tc_taps_ptr(void* ws, int n_rows) {
-    return reinterpret_cast<__half*>(static_cast<uint8_t*>(ws) + tc_header_bytes(n_rows));
+unsigned* tc_sync_ptr(void* ws, int n_rows) { return reinterpret_cast<unsigned*>(static_cast<int*>(ws) + 2 * n_rows); }
+int* tc_tiles_ptr(void* ws, int n_rows) { return static_cast<int*>(ws) + 2 * n_rows + 16; }
+__half* tc_taps_ptr(const tf_bp_plan* p, void* ws, int n_rows) {
+    return reinterpret_cast<__half*>(static_cast<uint8_t*>(ws) + tc_header_bytes(p, n_rows));
 }
 
 TCArgs make_args(const tf_bp_plan* p) {
     TCArgs a{};
     a.trig = p->d_trig;
-    a.order = p->d_order[kShapeTc];
     a.nx = p->g.nx;
     a.ny = p->g.ny;
     a.ntx = (p->g.nx + kTX - 1) / kTX;
@@ -645,9 +699,20 @@ TCArgs make_args(const tf_bp_plan* p) {
 }
 
 template <int NR>
-int launch_tc(const CUtensorMap& map, const TCArgs& a, dim3 grid, cudaStream_t s) {
-    TF_CUDA_TRY(cudaFuncSetAttribute(bp_tc_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<NR>::SMEM));
-    bp_tc_kernel<NR><<<grid, kThreads, TcCfg<NR>::SMEM, s>>>(map, a);
+int launch_tc(const CUtensorMap& map, const TCArgs& a, cudaStream_t s) {
+    auto* fn = bp_tc_kernel<NR>;
+    TF_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<NR>::SMEM));
+    int dev = 0, sms = 0, per_sm = 0;
+    TF_CUDA_TRY(cudaGetDevice(&dev));
+    TF_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, TcCfg<NR>::SMEM));
+    if (per_sm < 1) return set_error(TF_ERR_UNSUPPORTED, "bp_tc_kernel does not fit on an SM");
+    // every CTA of a round must be resident for the lockstep barrier: a cooperative launch
+    const unsigned grid = (unsigned)std::min<long long>((long long)sms * per_sm, a.n_work);
+    TCArgs args = a;
+    CUtensorMap m = map;
+    void* kargs[] = {&m, &args};
+    TF_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kThreads), kargs, TcCfg<NR>::SMEM, s));
     return check_launch("bp_tc_kernel");
 }
 
@@ -658,7 +723,7 @@ long long* g_tc_probe = nullptr;  // set by tools/tc_probe.cu's tf_bp_tc_probe (
 #endif
 
 // shared with filter.cu (K1 writing tap planes directly)
-int64_t bp_tc_header_bytes(int n_rows) { return tc_header_bytes(n_rows); }
+int64_t bp_tc_header_bytes(const tf_bp_plan* p, int n_rows) { return tc_header_bytes(p, n_rows); }
 int tc_uniform_exponents(void* taps, int n_rows, double bound, cudaStream_t s) {
     tc_exponent_kernel<<<(n_rows + 255) / 256, 256, 0, s>>>(nullptr, tc_exp_ptr(taps), n_rows, (float)bound, 1.f);
     return check_launch("tc_exponent_kernel");
@@ -687,7 +752,7 @@ extern "C" int tf_bp_tc_supported(const tf_bp_plan* p) {
 
 extern "C" int64_t tf_bp_tc_taps_bytes(const tf_bp_plan* p, int n_rows, int n_angles) {
     if (!p || n_rows < 0 || n_angles < 0) return -1;
-    return tc_header_bytes(n_rows) + (int64_t)n_angles * tc_angle_bytes(p, n_rows);
+    return tc_header_bytes(p, n_rows) + (int64_t)n_angles * tc_angle_bytes(p, n_rows);
 }
 
 extern "C" int tf_bp_tc_set_exponent(const tf_bp_plan* p, void* taps, int n_rows, double t_bound, void* stream) {
@@ -732,7 +797,7 @@ extern "C" int tf_bp_tc_stage(const tf_bp_plan* p, const float* sino, int rows_p
         const long long items = (long long)(a1 - a0) * ((k + 7) / 8) * p->g.n_chan;
         const int grid = (int)std::min<long long>((items + 255) / 256, 148LL * 16);
         tc_stage_kernel<<<grid, 256, 0, s>>>(sino, w, rows_per_angle, r0, k, a0, a1 - a0, p->g.n_chan,
-                                             tc_exp_ptr(taps), tc_taps_ptr(taps, k));
+                                             tc_exp_ptr(taps), tc_taps_ptr(p, taps, k));
     }
     return check_launch("tc_stage_kernel");
 }
@@ -762,7 +827,8 @@ extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* taps, int64_t 
     PFN_encodeTiled_t enc = encode_fn();
     if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     CUtensorMap map;
-    void* data = tc_taps_ptr(const_cast<void*>(taps), n_rows);
+    void* ws = const_cast<void*>(taps);
+    void* data = tc_taps_ptr(p, ws, n_rows);
     // dim 0 = (channel, row-in-group) flattened: a box row is 16 channels x 8 rows = 256 contiguous
     // bytes; channel c starts at element 8 c.  dim 1 = 8-row group, dim 2 = (angle, plane).
     cuuint64_t dims[3] = {(cuuint64_t)8 * g.n_chan, (cuuint64_t)R8, (cuuint64_t)(2 * (taps_a1 - taps_a0))};
@@ -773,9 +839,11 @@ extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* taps, int64_t 
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+    cudaStream_t s = as_stream(stream);
 
     TCArgs a = make_args(p);
-    a.e_rows = tc_exp_ptr(const_cast<void*>(taps));
+    a.e_rows = tc_exp_ptr(ws);
+    a.sync = tc_sync_ptr(ws, n_rows);
     a.vol = vol;
     a.a0 = a0;
     a.a1 = a1;
@@ -789,9 +857,40 @@ extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* taps, int64_t 
 #ifdef TF_TC_PROBE
     a.probe = g_tc_probe;
 #endif
-    const int nty = (g.ny + kTY - 1) / kTY;
-    dim3 grid((unsigned)(a.ntx * nty), (unsigned)((n_rows + NR - 1) / NR));
-    return NR == 256 ? launch_tc<256>(map, a, grid, as_stream(stream)) : launch_tc<128>(map, a, grid, as_stream(stream));
+    // the work list: the FoV-active tiles of the plan (Morton order), or of them the ones overlapping
+    // a restricted tile -- copied into the workspace header
+    const int n_act = p->n_active[kShapeTc];
+    if (x0 == 0 && x1 == g.nx && y0 == 0 && y1 == g.ny) {
+        a.tiles = p->d_order[kShapeTc];
+        a.n_tiles = n_act;
+    } else {
+        std::vector<int> sel;
+        for (int i = 0; i < n_act; ++i) {
+            const int t = p->h_order[kShapeTc][i];
+            const int X0 = (t % a.ntx) * kTX, Y0 = (t / a.ntx) * kTY;
+            if (X0 < x1 && X0 + kTX > x0 && Y0 < y1 && Y0 + kTY > y0) sel.push_back(t);
+        }
+        if (!sel.empty())
+            TF_CUDA_TRY(cudaMemcpyAsync(tc_tiles_ptr(ws, n_rows), sel.data(), sizeof(int) * sel.size(),
+                                        cudaMemcpyHostToDevice, s));
+        a.tiles = tc_tiles_ptr(ws, n_rows);
+        a.n_tiles = (int)sel.size();
+    }
+    a.n_work = a.n_tiles * ((n_rows + NR - 1) / NR);
+    if (a.flags & TF_BP_FINALIZE) {  // the FoV-inactive tiles are only masked: zeros
+        const int n_in = p->n_tiles[kShapeTc] - n_act;
+        if (n_in > 0) {
+            const long long n = (long long)n_in * kMV * n_rows;
+            const int grid = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+            tc_zero_tiles_kernel<<<grid, 256, 0, s>>>(vol, p->d_order[kShapeTc] + n_act, n_in, a.ntx, g.nx, g.ny, n_rows,
+                                                      x0, x1, y0, y1);
+            int st = check_launch("tc_zero_tiles_kernel");
+            if (st) return st;
+        }
+    }
+    if (a.n_work == 0) return TF_OK;
+    TF_CUDA_TRY(cudaMemsetAsync(a.sync, 0, sizeof(unsigned), s));
+    return NR == 256 ? launch_tc<256>(map, a, s) : launch_tc<128>(map, a, s);
 }
 
 extern "C" int tf_bp_tc_work(const tf_bp_plan* p, int n_rows, int a0, int a1, int64_t* items,
@@ -810,6 +909,7 @@ extern "C" int tf_bp_tc_work(const tf_bp_plan* p, int n_rows, int a0, int a1, in
         TCArgs a = make_args(p);
         a.a0 = a0;
         a.a1 = a1;
+        a.tiles = p->d_order[kShapeTc];
         if (e == cudaSuccess) {
             tc_work_kernel<<<na, 256>>>(a, na, d);
             e = cudaGetLastError();

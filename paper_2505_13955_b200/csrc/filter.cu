@@ -1130,7 +1130,7 @@ extern "C" int tf_filter_taps(const tf_filter_plan* p, const tf_bp_plan* bp, con
     if (st) return st;
     if (n_lines == 0) return TF_OK;
     OutMap map{};
-    st = build_map(map, reinterpret_cast<float*>(static_cast<uint8_t*>(taps) + bp_tc_header_bytes(rows_per_angle)),
+    st = build_map(map, reinterpret_cast<float*>(static_cast<uint8_t*>(taps) + bp_tc_header_bytes(bp, rows_per_angle)),
                    n_lines, rows_per_angle, 0, nullptr, nullptr);
     if (st) return st;
     map.zblocked = 2;

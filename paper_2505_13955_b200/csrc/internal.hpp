@@ -17,7 +17,7 @@ const float* bp_plan_weights(const tf_bp_plan* p);  // device feather weights, n
 int bp_plan_n_chan(const tf_bp_plan* p);
 int check_launch(const char* what);
 // K2-TC tap-plane workspace (bp_tc.cu), for K1 writing it directly (filter.cu)
-int64_t bp_tc_header_bytes(int n_rows);
+int64_t bp_tc_header_bytes(const tf_bp_plan* p, int n_rows);
 int tc_uniform_exponents(void* taps, int n_rows, double bound, cudaStream_t s);
 int tc_row_exponents(void* taps, const float* lines, int rows_per_angle, int n_ang, int n_chan, const float* w,
                      double factor, cudaStream_t s);
