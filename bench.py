@@ -61,6 +61,9 @@ EXCHANGE_STEP = {
                     "buffer over NVLink -> K2 (CUDA-core kernel)",
     "allgather": "K1 Beer-Lambert+ramp -> NCCL all-gather of natural rows -> owner stages its rows into tap "
                  "planes -> K2 tensor-core back-projection",
+    "p2p-chunked": "per ascending angle chunk: K1 Beer-Lambert+ramp of this rank's share -> natural rows stored into "
+                   "the owners' receive buffers over NVLink -> owner stages the chunk into tap planes -> K2 "
+                   "tensor-core back-projection with TF_BP_ACCUMULATE (bitwise the single pass)",
 }
 
 
@@ -72,7 +75,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--exchange", default="p2p",
-                    choices=["alltoall", "allgather", "p2p", "p2p-zblocked", "angles-p2p", "angles-nccl"])
+                    choices=["alltoall", "allgather", "p2p", "p2p-zblocked", "p2p-chunked", "angles-p2p",
+                             "angles-nccl"])
+    ap.add_argument("--chunk", type=int, default=None, help="p2p-chunked: angles per chunk (multiple of 16)")
     ap.add_argument("--e2e-steps", type=int, default=None, help="default: --steps")
     ap.add_argument("--slab-rows", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")
@@ -564,6 +569,28 @@ def main():
             bp_ev[0].record()
             eng.run(raw)
             bp_ev[1].record()
+    elif world > 1 and (args.exchange == "p2p-chunked" or (
+            args.exchange == "p2p" and 4.0 * (2 * n_proj * (n / world) * n + (n / world) * n * n + n_proj / world * n * n)
+            > 0.8 * torch.cuda.get_device_properties(dev).total_memory)):
+        # the whole scan's receive + tap buffers do not fit next to the slab (C4): angle-chunked exchange
+        from paper_2505_13955_b200.distributed import ChunkedZSlabReconstructor
+
+        args.exchange = "p2p-chunked"
+        raw_bytes = 4.0 * (n_proj / world) * n * n
+        eng = ChunkedZSlabReconstructor(p, d, i0=I0, chunk=args.chunk, device=dev,
+                                        budget_bytes=torch.cuda.mem_get_info(dev)[0] - raw_bytes - 4e9)
+        raw = torch.empty(eng.chunk_shape(), dtype=torch.float32, device=dev)
+        for (pa, pb), o in zip(eng.rank_angles(), eng.offsets):
+            if pb > pa:
+                phantom_raw(p, d, raw[o: o + pb - pa], a0=pa, a1=pb)
+        slab = eng.local
+        k_rows = eng.r1 - eng.r0
+        launches = 4 * len(eng.chunks)  # per chunk: K1, exponent fill + tap staging, K2
+
+        def step_parts():
+            bp_ev[0].record()
+            eng.run(raw)
+            bp_ev[1].record()
     elif world > 1:
         from paper_2505_13955_b200.distributed import ZSlabReconstructor
 
@@ -638,13 +665,14 @@ def main():
     gups = total_updates / (ms_per_step / 1e3) / 1e9
     bp_avg_ms = statistics.mean(bp_ms)
     roof = None
-    if not angle_split:
+    chunked = args.exchange == "p2p-chunked" and world > 1
+    if not angle_split and not chunked:
         roof = roofline(slab, bp_a0, bp_a1, k_rows, bp_avg_ms, clk.get("sm_mhz"), load_peaks(),
                         args.config if world == 1 else f"{args.config}_n{world}")
 
     # ---- e2e through host pinned buffers: StreamedReconstructor (public API), --e2e-steps steps
     e2e = None
-    if not args.no_e2e and not angle_split:
+    if not args.no_e2e and not angle_split and not chunked:
         ke = args.e2e_steps if args.e2e_steps is not None else args.steps
         er0, er1 = split_range(n, world)[rank]
         ek = er1 - er0
@@ -740,6 +768,7 @@ def main():
         "dtype": "f32",
         "data": "synthetic (analytic 3-D Shepp-Logan raw counts generated on device, i0=1e5)",
         "config": {"workload": workload_desc(cfg), "volume": [n, n, n], "n_proj": n_proj,
+                   "chunks": (len(eng.chunks) if chunked else None),
                    "parallelism": (f"angle-split x{world} ({args.exchange}: partials reduced onto z-slab owners)"
                                    if angle_split else
                                    f"z-slab x{world}" + (f" ({args.exchange} exchange)" if world > 1 else "")),
