@@ -463,11 +463,12 @@ def run_streamed(args, cfg, world, rank, local, dev):
             h[:, q0:q1].copy_(v)
         specimens.append((s0, h, torch.empty((rows, n, n), dtype=torch.uint16, pin_memory=True)))
     del tmp
+    torch.cuda.empty_cache()
     st = StreamedReconstructor(p, d, i0=I0, slab_rows=S, device=dev)
+    jobs = [(h_raw, h_vol, (s0, s0 + rows), s0) for s0, h_raw, h_vol in specimens]
 
-    def one_pass():
-        for s0, h_raw, h_vol in specimens:
-            st.run(h_raw, h_vol, row_range=(s0, s0 + rows), host_row0=s0, quantize=(0.0, 4e-4))
+    def one_pass():  # the batch as one sub-slab stream (StreamedReconstructor.run_batch)
+        st.run_batch(jobs, quantize=(0.0, 4e-4))
 
     for _ in range(args.warmup):
         one_pass()
@@ -502,8 +503,8 @@ def run_streamed(args, cfg, world, rank, local, dev):
                     "memory before timing)",
             "config": {"workload": workload_desc(cfg), "volume": [n, n, n], "n_proj": n_proj,
                        "mode": (f"batch of {args.specimens} specimens, each {rows} rows per GPU host-streamed in "
-                                f"{S}-row z-sub-slabs (StreamedReconstructor: H2D / K1 taps + K2 tensor cores + "
-                                f"K3 quantize / uint16 D2H on 3 streams)"),
+                                f"{S}-row z-sub-slabs as one stream (StreamedReconstructor.run_batch: H2D / K1 "
+                                f"taps + K2 tensor cores + K3 quantize / uint16 D2H on 3 streams)"),
                        "rows_per_gpu_per_specimen": rows, "sample": rows < (r1 - r0),
                        "s_per_specimen_volume_extrapolated": round(s_per_spec, 2)},
             "e2e": {"value": round(upd / (ms / 1e3) / 1e9, 3), "unit": "GUPS",

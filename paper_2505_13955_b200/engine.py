@@ -252,7 +252,7 @@ class StreamedReconstructor:
                                          device=self.device, tensor=tensor)
             shape = (params.n_proj, k, params.n_chan)
             self.raw = [torch.empty(shape, dtype=torch.float32, device=self.device) for _ in range(2)]
-            self.vol = [self.eng.vol, torch.empty_like(self.eng.vol)]
+            self.vol = [self.eng.vol, None]  # the second fp32 slab only without quantize (allocated on use)
             self.s_h2d = torch.cuda.Stream(self.device)
             self.s_comp = torch.cuda.Stream(self.device)
             self.s_d2h = torch.cuda.Stream(self.device)
@@ -311,21 +311,34 @@ class StreamedReconstructor:
         uint16 when `quantize` = (lo, hi) (K3 runs per slab on the device, so
         only 2 B/voxel cross PCIe).  Work is queued on this object's streams
         (ordered after the current stream); returns the last D2H event."""
+        return self.run_batch([(raw_host, vol_host, row_range, host_row0)], quantize)
+
+    def run_batch(self, jobs, quantize=None):
+        """A batch of specimens (the reference's SpecimenSet groups,
+        pipeline.py:119-161) as ONE sub-slab stream: jobs = [(raw_host,
+        vol_host, row_range, host_row0), ...], each as in run().  The next
+        specimen's first H2D overlaps the previous one's last sub-slab, so
+        the pipeline fills and drains once per batch, not per specimen."""
         torch = self.torch
         p, d = self.params, self.dims
-        R0, R1 = row_range if row_range is not None else (0, p.n_rows)
         n = p.n_chan
         line = n * 4
         plane = d.nx * d.ny * (2 if quantize is not None else 4)
         if quantize is not None and getattr(self, "_q", None) is None:
             self._q = [torch.empty(self.vol[0].shape, dtype=torch.uint16, device=self.device) for _ in range(2)]
+        if quantize is None and self.vol[1] is None:
+            self.vol[1] = torch.empty_like(self.vol[0])
         cur = torch.cuda.current_stream(self.device)
         for s in (self.s_h2d, self.s_comp, self.s_d2h):
             s.wait_stream(cur)
         raw_free = [None, None]
-        vol_free = [None, None]
+        out_free = [None, None]
         done = None
-        for i, (r0, r1) in enumerate(self.sub_slabs(R0, R1)):
+        tasks = []
+        for raw_host, vol_host, row_range, host_row0 in jobs:
+            R0, R1 = row_range if row_range is not None else (0, p.n_rows)
+            tasks += [(raw_host, vol_host, R0, host_row0, r0, r1) for r0, r1 in self.sub_slabs(R0, R1)]
+        for i, (raw_host, vol_host, R0, host_row0, r0, r1) in enumerate(tasks):
             k = r1 - r0
             b = i % 2
             # H2D: rows [r0, r1) of every angle (n_proj strided chunks)
@@ -341,13 +354,15 @@ class StreamedReconstructor:
             ev = torch.cuda.Event()
             ev.record(self.s_comp)
             raw_free[b] = ev
-            if vol_free[b] is not None:
-                self.s_comp.wait_event(vol_free[b])
-            self.eng.backproject(stream=self.s_comp, vol=self.vol[b], n_rows=k)
-            src_vol = self.vol[b]
+            if out_free[b] is not None:
+                self.s_comp.wait_event(out_free[b])
+            # with K3 the fp32 slab is consumed on the compute stream itself: one buffer suffices
+            vol = self.vol[0] if quantize is not None else self.vol[b]
+            self.eng.backproject(stream=self.s_comp, vol=vol, n_rows=k)
+            src_vol = vol
             if quantize is not None:  # fbp.quantize on the device (K3)
                 lo, hi = quantize
-                check(lib().tf_quantize(_ptr(self.vol[b]), _lib.TF_F32, _ptr(self._q[b]), k * d.nx * d.ny,
+                check(lib().tf_quantize(_ptr(vol), _lib.TF_F32, _ptr(self._q[b]), k * d.nx * d.ny,
                                         float(lo), float(hi), ctypes.c_void_p(self.s_comp.cuda_stream)))
                 src_vol = self._q[b]
             comp_done = torch.cuda.Event()
@@ -358,7 +373,7 @@ class StreamedReconstructor:
                          self.s_d2h)
             ev = torch.cuda.Event()
             ev.record(self.s_d2h)
-            vol_free[b] = ev
+            out_free[b] = ev
             done = ev
         for s in (self.s_h2d, self.s_comp, self.s_d2h):
             cur.wait_stream(s)

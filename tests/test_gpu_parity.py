@@ -945,3 +945,37 @@ def test_tensor_core_row_independence_and_data_scale(F):
         diff = np.abs(out - base).reshape(5, -1).max(axis=1)
         assert diff[2] > 0
         assert np.all(diff[[0, 1, 3, 4]] == 0)
+
+
+def test_streamed_batch_of_specimens_equals_single_runs(F):
+    """StreamedReconstructor.run_batch (a batch of specimens as one
+    sub-slab stream, uint16 out through K3) == each specimen's own
+    device-resident reconstruction quantized, bit for bit (the reference's
+    SpecimenSet groups, pipeline.py:119-161)."""
+    import torch
+
+    from paper_2505_13955_b200.engine import SlabReconstructor, StreamedReconstructor, phantom_raw
+    from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
+
+    n, rows, n_proj = 64, 300, 60
+    p = AcquisitionParams(n_proj=n_proj, n_rows=rows, n_chan=n, pixel_pitch=12.0)
+    d = VolumeDims(n, n, rows, voxel_pitch=12.0)
+    jobs, refs = [], []
+    for s, (r0, r1) in enumerate([(0, 300), (40, 200)]):
+        raw = torch.empty((n_proj, rows, n), device="cuda")
+        phantom_raw(p, d, raw, i0=1e5, mu_max=3.5e-4 * (1 - 0.2 * s))
+        full = SlabReconstructor(p, d, i0=1e5).run(raw)
+        q = torch.empty(full.shape, dtype=torch.uint16, device="cuda")
+        from paper_2505_13955_b200._lib import TF_F32, check, lib
+        import ctypes
+        check(lib().tf_quantize(ctypes.c_void_p(full.data_ptr()), TF_F32, ctypes.c_void_p(q.data_ptr()), full.numel(),
+                                0.0, 4e-4, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        refs.append(q[r0:r1].cpu())
+        h_raw = raw[:, r0:r1].contiguous().cpu().pin_memory()
+        h_vol = torch.zeros((r1 - r0, n, n), dtype=torch.uint16).pin_memory()
+        jobs.append((h_raw, h_vol, (r0, r1), r0))
+    st = StreamedReconstructor(p, d, i0=1e5, slab_rows=128)
+    st.run_batch(jobs, quantize=(0.0, 4e-4))
+    torch.cuda.synchronize()
+    for (_, h_vol, _, _), ref in zip(jobs, refs):
+        assert torch.equal(h_vol, ref)
