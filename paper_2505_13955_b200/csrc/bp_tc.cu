@@ -153,13 +153,6 @@ __device__ __forceinline__ uint32_t pack_h2(__half lo, __half hi) {
     return (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
 }
 
-// L2 prefetch of a tensor-map box (no shared-memory destination, no barrier)
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(map)),
-                 "r"(c0), "r"(c1), "r"(c2)
-                 : "memory");
-}
-
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -431,9 +424,6 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
                     while (flushed < n_blk && (blk0 + flushed + 1) * kP + kLag <= ab) flush(flushed++);
                     PROBE_ADD(p_flush, q3);
                     const TcWin w = tc_bcast(bt.w, i);
-#ifdef TF_TC_L2_PREFETCH
-                    const int c_next = __shfl_sync(0xffffffffu, bt.w.c_lo, min(i + kG, 31));
-#endif
                     const int nk = 1 + ((bt.two >> i) & 1);
                     const int it0 = ibase + i + __popc(bt.two & ((1u << i) - 1u));
 #ifdef TF_TC_PROBE_W_IDLE  // probe builds only: no weight arithmetic
@@ -482,13 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
                             tma_load_3d(st + Cfg::TAP_PLANE, &map, &full[s], 8 * (w.c_lo + kK * ks), zr0 / 8,
                                         ka + 1);
 #endif
-#ifdef TF_TC_L2_PREFETCH
-                            // the group's next angle (4 angles on): warm its boxes in L2
-                            if (ks == 0 && i + kG < bt.n) {
-                                tma_prefetch_3d(&map, 8 * c_next, zr0 / 8, ka + 2 * kG);
-                                tma_prefetch_3d(&map, 8 * c_next, zr0 / 8, ka + 2 * kG + 1);
-                            }
-#endif
+
                         }
                         const uint32_t wa = wslot0 + (uint32_t)(s * Cfg::SLOT);
 #pragma unroll

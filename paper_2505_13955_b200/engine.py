@@ -256,6 +256,12 @@ class StreamedReconstructor:
             self.s_h2d = torch.cuda.Stream(self.device)
             self.s_comp = torch.cuda.Stream(self.device)
             self.s_d2h = torch.cuda.Stream(self.device)
+        # buffer parity and the events guarding the double buffers persist across calls, so
+        # back-to-back calls with join=False overlap one call's last D2H with the next one's
+        # first H2D (the pipeline fills and drains once per sequence of calls)
+        self._n = 0
+        self._raw_free = [None, None]
+        self._out_free = [None, None]
 
     def sub_slabs(self, R0, R1):
         """Sub-slab boundaries.  Tensor-core K2: uniform `slab_rows` slabs
@@ -304,16 +310,25 @@ class StreamedReconstructor:
         check(lib().tf_copy2d_async(ctypes.c_void_p(dst), dpitch, ctypes.c_void_p(src), spitch, width, height,
                                     ctypes.c_void_p(stream.cuda_stream)))
 
-    def run(self, raw_host, vol_host, row_range=None, host_row0=0, quantize=None):
+    def run(self, raw_host, vol_host, row_range=None, host_row0=0, quantize=None, join=True):
         """raw_host: pinned (n_proj, H, n_chan) fp32 counts holding detector
         rows [host_row0, host_row0 + H); vol_host: pinned (R, ny, nx) fp32
         receiving volume rows `row_range` = [r0, r1) (default: all rows), or
         uint16 when `quantize` = (lo, hi) (K3 runs per slab on the device, so
         only 2 B/voxel cross PCIe).  Work is queued on this object's streams
-        (ordered after the current stream); returns the last D2H event."""
-        return self.run_batch([(raw_host, vol_host, row_range, host_row0)], quantize)
+        (ordered after the current stream); returns the last D2H event.
+        join=False leaves the work on this object's streams (the caller
+        waits on the returned event or calls join()), so the next call's
+        first H2D overlaps this call's last D2H."""
+        return self.run_batch([(raw_host, vol_host, row_range, host_row0)], quantize, join)
 
-    def run_batch(self, jobs, quantize=None):
+    def join(self):
+        """Make the current stream wait for everything queued on this object's streams."""
+        cur = self.torch.cuda.current_stream(self.device)
+        for s in (self.s_h2d, self.s_comp, self.s_d2h):
+            cur.wait_stream(s)
+
+    def run_batch(self, jobs, quantize=None, join=True):
         """A batch of specimens (the reference's SpecimenSet groups,
         pipeline.py:119-161) as ONE sub-slab stream: jobs = [(raw_host,
         vol_host, row_range, host_row0), ...], each as in run().  The next
@@ -331,16 +346,16 @@ class StreamedReconstructor:
         cur = torch.cuda.current_stream(self.device)
         for s in (self.s_h2d, self.s_comp, self.s_d2h):
             s.wait_stream(cur)
-        raw_free = [None, None]
-        out_free = [None, None]
+        raw_free, out_free = self._raw_free, self._out_free
         done = None
         tasks = []
         for raw_host, vol_host, row_range, host_row0 in jobs:
             R0, R1 = row_range if row_range is not None else (0, p.n_rows)
             tasks += [(raw_host, vol_host, R0, host_row0, r0, r1) for r0, r1 in self.sub_slabs(R0, R1)]
-        for i, (raw_host, vol_host, R0, host_row0, r0, r1) in enumerate(tasks):
+        for raw_host, vol_host, R0, host_row0, r0, r1 in tasks:
             k = r1 - r0
-            b = i % 2
+            b = self._n % 2
+            self._n += 1
             # H2D: rows [r0, r1) of every angle (n_proj strided chunks)
             if raw_free[b] is not None:
                 self.s_h2d.wait_event(raw_free[b])
@@ -375,8 +390,8 @@ class StreamedReconstructor:
             ev.record(self.s_d2h)
             out_free[b] = ev
             done = ev
-        for s in (self.s_h2d, self.s_comp, self.s_d2h):
-            cur.wait_stream(s)
+        if join:
+            self.join()
         return done
 
     def updates(self, row_range=None) -> int:

@@ -979,3 +979,33 @@ def test_streamed_batch_of_specimens_equals_single_runs(F):
     torch.cuda.synchronize()
     for (_, h_vol, _, _), ref in zip(jobs, refs):
         assert torch.equal(h_vol, ref)
+
+
+def test_streamed_steps_pipelined_across_calls(F):
+    """run(join=False) back to back (a step's last D2H overlapping the next
+    step's first H2D, the buffers' parity and guards carried across calls)
+    gives every step's volume bit for bit."""
+    import torch
+
+    from paper_2505_13955_b200.engine import SlabReconstructor, StreamedReconstructor, phantom_raw
+    from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
+
+    n, rows, n_proj = 64, 600, 48
+    p = AcquisitionParams(n_proj=n_proj, n_rows=rows, n_chan=n, pixel_pitch=12.0)
+    d = VolumeDims(n, n, rows, voxel_pitch=12.0)
+    st = StreamedReconstructor(p, d, i0=1e5, slab_rows=256)
+    outs, refs = [], []
+    for s in range(3):
+        raw = torch.empty((n_proj, rows, n), device="cuda")
+        phantom_raw(p, d, raw, i0=1e5, mu_max=3.5e-4 * (1 - 0.2 * s))
+        refs.append(SlabReconstructor(p, d, i0=1e5).run(raw).cpu())
+        h_raw = raw.cpu().pin_memory()
+        h_vol = torch.zeros((rows, n, n), dtype=torch.float32).pin_memory()
+        outs.append((h_raw, h_vol))
+    torch.cuda.synchronize()
+    for h_raw, h_vol in outs:
+        st.run(h_raw, h_vol, join=False)
+    st.join()
+    torch.cuda.synchronize()
+    for (_, h_vol), ref in zip(outs, refs):
+        assert torch.equal(h_vol, ref)
