@@ -368,15 +368,15 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
             const int wi = r * G + (int)blockIdx.x;
             const int zb = wi / a.n_tiles;
             const int tile = a.tiles[wi - zb * a.n_tiles];
-            const int X0 = (tile % a.ntx) * kTX, Y0 = (tile / a.ntx) * kTY;
             const int zr0 = zb * NR;
-            const int xe = min(X0 + kTX, a.nx), ye = min(Y0 + kTY, a.ny);
-            const int ux0 = max(X0, a.x0), ux1 = min(xe, a.x1);
-            const int uy0 = max(Y0, a.y0), uy1 = min(ye, a.y1);
-            const double dX = (double)X0 - a.cx, dY = (double)Y0 - a.cy;
-            const int x = X0 + vx, y = Y0 + vy;
-            const bool inside = real && x >= ux0 && x < ux1 && y >= uy0 && y < uy1;
-            const int zc0 = zr0 + grp * NC;  // first volume row of this thread's master columns
+            // this thread's voxel (x, y) inside the requested tile?  Recomputed for the epilogue
+            // rather than kept live through the angle loop (register pressure)
+            auto voxel = [&](int& x, int& y) {
+                x = (tile % a.ntx) * kTX + vx;
+                y = (tile / a.ntx) * kTY + vy;
+                return real && x < a.nx && y < a.ny && x >= a.x0 && x < a.x1 && y >= a.y0 && y < a.y1;
+            };
+            const double dX = (double)((tile % a.ntx) * kTX) - a.cx, dY = (double)((tile / a.ntx) * kTY) - a.cy;
             // this round's per-row scalings (the previous round's epilogue is done with them)
             named_bar_sync(1, 128 * kG);
             for (int i = threadIdx.x - 64; i < NR; i += 128 * kG) {
@@ -388,11 +388,15 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
             float master[NC];
 #pragma unroll
             for (int j = 0; j < NC; ++j) master[j] = 0.f;
-            if ((a.flags & TF_BP_ACCUMULATE) && inside) {  // continue unscaled partial sums: x 2^e is exact
-                const float* src = a.vol + (size_t)y * a.nx + x;
+            if (a.flags & TF_BP_ACCUMULATE) {  // continue unscaled partial sums: x 2^e is exact
+                int x, y;
+                if (voxel(x, y)) {
+                    const int zc0 = zr0 + grp * NC;
+                    const float* src = a.vol + (size_t)y * a.nx + x;
 #pragma unroll
-                for (int j = 0; j < NC; ++j)
-                    if (zc0 + j < a.n_rows) master[j] = src[(size_t)(zc0 + j) * plane] * s_up[grp * NC + j];
+                    for (int j = 0; j < NC; ++j)
+                        if (zc0 + j < a.n_rows) master[j] = src[(size_t)(zc0 + j) * plane] * s_up[grp * NC + j];
+                }
             }
             auto flush = [&](int lb) {  // master (+)= accumulator of block lb of the round, round to nearest
                 const int gb = blk_round + lb, acc = gb & 1;
@@ -504,7 +508,9 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
             it_round = ibase;
             blk_round += n_blk;
             // ---- epilogue: master x 2^-e -> volume (fbp.py:247-251)
-            if (inside) {
+            int x, y;
+            if (voxel(x, y)) {
+                const int zc0 = zr0 + grp * NC;  // first volume row of this thread's master columns
                 const bool fin = (a.flags & TF_BP_FINALIZE) != 0;
                 const bool zero = fin && tc_outside_fov(x, y, a);
                 float* out = a.vol + (size_t)y * a.nx + x;
