@@ -1,5 +1,2 @@
-rm -f tools/micro/libtomofuse_probe*.so
-for r in 1 2; do
-timeout 200 python tools/tc_probe.py --build --n 2048 --n-proj 1800 --rows 1024 --reps 2 --define TF_TC_NOPROBE --src tools/micro/bp_tc_r2.cu 2>&1 | tail -1
-timeout 200 python tools/tc_probe.py --build --n 2048 --n-proj 1800 --rows 1024 --reps 2 --define TF_TC_NOPROBE --define TF_TC_SPIN_MMA --src tools/micro/bp_tc_r2.cu 2>&1 | tail -1
-done
+make -s -C oracle >/dev/null 2>&1
+timeout 3000 python -m pytest tests -m gpu -q -x -p dropin_plugin 2>&1 | tail -6
