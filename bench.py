@@ -89,6 +89,9 @@ def parse():
     ap.add_argument("--rows", type=int, default=None,
                     help="streaming mode: reconstruct only this many rows per specimen and GPU (bounded sample)")
     ap.add_argument("--specimens", type=int, default=2, help="streaming mode: synthetic specimens per batch")
+    ap.add_argument("--angle-chunk", default="auto",
+                    help="streaming mode: angles per H2D/K1/K2 chunk of a sub-slab ('auto': only when a whole scan "
+                         "does not fit)")
     ap.add_argument("--cpu-seconds", type=float, default=6.0, help="target CPU seconds per reference sample")
     return ap.parse_args()
 
@@ -464,7 +467,9 @@ def run_streamed(args, cfg, world, rank, local, dev):
         specimens.append((s0, h, torch.empty((rows, n, n), dtype=torch.uint16, pin_memory=True)))
     del tmp
     torch.cuda.empty_cache()
-    st = StreamedReconstructor(p, d, i0=I0, slab_rows=S, device=dev)
+    free_gb = torch.cuda.mem_get_info(dev)[0] / 1e9
+    ac = args.angle_chunk if args.angle_chunk == "auto" else int(args.angle_chunk)
+    st = StreamedReconstructor(p, d, i0=I0, slab_rows=S, device=dev, angle_chunk=ac)
     jobs = [(h_raw, h_vol, (s0, s0 + rows), s0) for s0, h_raw, h_vol in specimens]
 
     def one_pass():  # the batch as one sub-slab stream (StreamedReconstructor.run_batch)
@@ -504,14 +509,19 @@ def run_streamed(args, cfg, world, rank, local, dev):
             "config": {"workload": workload_desc(cfg), "volume": [n, n, n], "n_proj": n_proj,
                        "mode": (f"batch of {args.specimens} specimens, each {rows} rows per GPU host-streamed in "
                                 f"{S}-row z-sub-slabs as one stream (StreamedReconstructor.run_batch: H2D / K1 "
-                                f"taps + K2 tensor cores + K3 quantize / uint16 D2H on 3 streams)"),
+                                f"taps + K2 tensor cores + K3 quantize / uint16 D2H on 3 streams"
+                                + (f"; each sub-slab's angles in chunks of {st.angle_chunk} chained with "
+                                   f"TF_BP_ACCUMULATE" if st.angle_chunk else "") + ")"),
+                       "angle_chunk": st.angle_chunk, "device_free_gb_at_setup": round(free_gb, 1),
                        "rows_per_gpu_per_specimen": rows, "sample": rows < (r1 - r0),
                        "s_per_specimen_volume_extrapolated": round(s_per_spec, 2)},
             "e2e": {"value": round(upd / (ms / 1e3) / 1e9, 3), "unit": "GUPS",
                     "h2d_bytes_per_step": sum(h.numel() * 4 for _, h, _ in specimens),
                     "d2h_bytes_per_step": sum(v.numel() * 2 for _, _, v in specimens),
                     "path": "host pinned raw counts -> GPU -> host pinned uint16 volume, every step"},
-            "clocks": clk, "gpu_launches": 4 * len(sub) * args.specimens * args.steps,
+            # per angle chunk: K1's exponent fill, K1, K2; per sub-slab: the FoV-zero pass and K3
+            "clocks": clk, "gpu_launches": (3 * -(-n_proj // (st.angle_chunk or n_proj)) + 2) * len(sub)
+                                           * args.specimens * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -239,7 +239,7 @@ class StreamedReconstructor:
 
     def __init__(self, params: AcquisitionParams, dims: VolumeDims, spec: FilterSpec | None = None,
                  i0: float = 1e5, feather_band: int = 32, slab_rows: int = 256, device=None,
-                 tensor: bool | None = None):
+                 tensor: bool | None = None, angle_chunk: int | str | None = "auto"):
         import torch
 
         self.torch = torch
@@ -248,9 +248,13 @@ class StreamedReconstructor:
         self.slab_rows = min(slab_rows, params.n_rows)
         k = self.slab_rows
         with torch.cuda.device(self.device):
+            self.angle_chunk = self._chunk(angle_chunk, tensor)
+            A = self.angle_chunk or params.n_proj
             self.eng = SlabReconstructor(params, dims, spec, i0, feather_band, rows=(0, k),
-                                         device=self.device, tensor=tensor)
-            shape = (params.n_proj, k, params.n_chan)
+                                         device=self.device, tensor=tensor, n_angles=A)
+            if self.angle_chunk and not self.eng.tensor:
+                raise ValueError("angle chunks need the tensor-core K2 (blocks of 16 absolute angles chain exactly)")
+            shape = (A, k, params.n_chan)
             self.raw = [torch.empty(shape, dtype=torch.float32, device=self.device) for _ in range(2)]
             self.vol = [self.eng.vol, None]  # the second fp32 slab only without quantize (allocated on use)
             self.s_h2d = torch.cuda.Stream(self.device)
@@ -259,9 +263,36 @@ class StreamedReconstructor:
         # buffer parity and the events guarding the double buffers persist across calls, so
         # back-to-back calls with join=False overlap one call's last D2H with the next one's
         # first H2D (the pipeline fills and drains once per sequence of calls)
-        self._n = 0
+        self._n = 0  # raw-buffer parity (per H2D chunk)
+        self._m = 0  # output-buffer parity (per sub-slab)
         self._raw_free = [None, None]
         self._out_free = [None, None]
+
+    def _chunk(self, angle_chunk, tensor):
+        """Angles per H2D / K1 / K2 chunk of a sub-slab (None: all).  "auto"
+        chunks only when the double-buffered raw counts, the tap planes and
+        the fp32 + uint16 volume slabs of whole-scan sub-slabs would not fit
+        in the device's free memory less 4 GiB (C5: 7200 x 8192 x 256-row
+        sub-slabs); chunks are multiples of 16 angles, so chaining them with
+        TF_BP_ACCUMULATE gives the single-pass volume bit for bit."""
+        p, d, k = self.params, self.dims, self.slab_rows
+        if angle_chunk is None or (tensor is False) or (tensor is None and not tensor_default()):
+            return None
+        if angle_chunk != "auto":
+            a = max(16, int(angle_chunk) // 16 * 16)
+            return a if a < p.n_proj else None
+        free, _ = self.torch.cuda.mem_get_info(self.device)
+        # blocks the caching allocator holds but no tensor uses are free for these buffers too
+        free += self.torch.cuda.memory_reserved(self.device) - self.torch.cuda.memory_allocated(self.device)
+        line = k * p.n_chan * 4  # raw fp32 and fp16 hi/lo taps: 4 B per sample each
+        fixed = k * d.nx * d.ny * (4 + 2)  # fp32 slab + the uint16 slab
+        budget = free - (4 << 30) - fixed  # a 4 GiB margin for the plan, workspaces and the allocator
+        if 3 * line * p.n_proj <= budget:
+            return None
+        a = int(budget // (3 * line)) // 16 * 16
+        if a < 16:
+            raise ValueError(f"a {k}-row sub-slab does not fit in device memory; lower slab_rows")
+        return a
 
     def sub_slabs(self, R0, R1):
         """Sub-slab boundaries.  Tensor-core K2: uniform `slab_rows` slabs
@@ -315,7 +346,9 @@ class StreamedReconstructor:
         rows [host_row0, host_row0 + H); vol_host: pinned (R, ny, nx) fp32
         receiving volume rows `row_range` = [r0, r1) (default: all rows), or
         uint16 when `quantize` = (lo, hi) (K3 runs per slab on the device, so
-        only 2 B/voxel cross PCIe).  Work is queued on this object's streams
+        only 2 B/voxel cross PCIe).  With `angle_chunk` each sub-slab's
+        angles stream in chunks (H2D / K1 / K2 with TF_BP_ACCUMULATE), which
+        lets whole-width sub-slabs fit when the scan does not (C5).  Work is queued on this object's streams
         (ordered after the current stream); returns the last D2H event.
         join=False leaves the work on this object's streams (the caller
         waits on the returned event or calls join()), so the next call's
@@ -340,13 +373,15 @@ class StreamedReconstructor:
         line = n * 4
         plane = d.nx * d.ny * (2 if quantize is not None else 4)
         if quantize is not None and getattr(self, "_q", None) is None:
-            self._q = [torch.empty(self.vol[0].shape, dtype=torch.uint16, device=self.device) for _ in range(2)]
+            self._q = torch.empty(self.vol[0].shape, dtype=torch.uint16, device=self.device)
         if quantize is None and self.vol[1] is None:
             self.vol[1] = torch.empty_like(self.vol[0])
         cur = torch.cuda.current_stream(self.device)
         for s in (self.s_h2d, self.s_comp, self.s_d2h):
             s.wait_stream(cur)
         raw_free, out_free = self._raw_free, self._out_free
+        A = self.angle_chunk or p.n_proj
+        chunks = [(a, min(a + A, p.n_proj)) for a in range(0, p.n_proj, A)]
         done = None
         tasks = []
         for raw_host, vol_host, row_range, host_row0 in jobs:
@@ -354,32 +389,41 @@ class StreamedReconstructor:
             tasks += [(raw_host, vol_host, R0, host_row0, r0, r1) for r0, r1 in self.sub_slabs(R0, R1)]
         for raw_host, vol_host, R0, host_row0, r0, r1 in tasks:
             k = r1 - r0
-            b = self._n % 2
-            self._n += 1
-            # H2D: rows [r0, r1) of every angle (n_proj strided chunks)
-            if raw_free[b] is not None:
-                self.s_h2d.wait_event(raw_free[b])
-            self._copy2d(self.raw[b].data_ptr(), k * line, raw_host.data_ptr() + (r0 - host_row0) * line,
-                         raw_host.shape[1] * line, k * line, p.n_proj, self.s_h2d)
-            h2d_done = torch.cuda.Event()
-            h2d_done.record(self.s_h2d)
-            # compute
-            self.s_comp.wait_event(h2d_done)
-            self.eng.filter_stage(self.raw[b].view(-1)[: p.n_proj * k * n], stream=self.s_comp, n_rows=k)
-            ev = torch.cuda.Event()
-            ev.record(self.s_comp)
-            raw_free[b] = ev
-            if out_free[b] is not None:
-                self.s_comp.wait_event(out_free[b])
+            o = self._m % 2
+            self._m += 1
             # with K3 the fp32 slab is consumed on the compute stream itself: one buffer suffices
-            vol = self.vol[0] if quantize is not None else self.vol[b]
-            self.eng.backproject(stream=self.s_comp, vol=vol, n_rows=k)
+            vol = self.vol[0] if quantize is not None else self.vol[o]
+            for a, b in chunks:
+                rb = self._n % 2
+                self._n += 1
+                # H2D: rows [r0, r1) of angles [a, b) (b - a strided chunks)
+                if raw_free[rb] is not None:
+                    self.s_h2d.wait_event(raw_free[rb])
+                self._copy2d(self.raw[rb].data_ptr(), k * line,
+                             raw_host.data_ptr() + (a * raw_host.shape[1] + r0 - host_row0) * line,
+                             raw_host.shape[1] * line, k * line, b - a, self.s_h2d)
+                h2d_done = torch.cuda.Event()
+                h2d_done.record(self.s_h2d)
+                # compute: K1 into the tap planes of this chunk, K2 over its angles
+                self.s_comp.wait_event(h2d_done)
+                self.eng.filter_stage(self.raw[rb].view(-1)[: (b - a) * k * n], stream=self.s_comp, n_rows=k)
+                ev = torch.cuda.Event()
+                ev.record(self.s_comp)
+                raw_free[rb] = ev
+                if a == 0 and quantize is None and out_free[o] is not None:
+                    self.s_comp.wait_event(out_free[o])  # vol[o]'s previous D2H
+                flags = (_lib.TF_BP_ACCUMULATE if a > 0 else 0) | (_lib.TF_BP_FINALIZE if b == p.n_proj else 0)
+                self.eng.backproject(a0=a, a1=b, flags=flags, stream=self.s_comp, vol=vol, n_rows=k, taps_a0=a,
+                                     taps_a1=b)
             src_vol = vol
-            if quantize is not None:  # fbp.quantize on the device (K3)
+            if quantize is not None:  # fbp.quantize on the device (K3) into the one uint16 slab
                 lo, hi = quantize
-                check(lib().tf_quantize(_ptr(vol), _lib.TF_F32, _ptr(self._q[b]), k * d.nx * d.ny,
+                o = 0
+                if out_free[0] is not None:
+                    self.s_comp.wait_event(out_free[0])  # its previous D2H (far shorter than a sub-slab)
+                check(lib().tf_quantize(_ptr(vol), _lib.TF_F32, _ptr(self._q), k * d.nx * d.ny,
                                         float(lo), float(hi), ctypes.c_void_p(self.s_comp.cuda_stream)))
-                src_vol = self._q[b]
+                src_vol = self._q
             comp_done = torch.cuda.Event()
             comp_done.record(self.s_comp)
             # D2H: contiguous volume slab
@@ -388,7 +432,7 @@ class StreamedReconstructor:
                          self.s_d2h)
             ev = torch.cuda.Event()
             ev.record(self.s_d2h)
-            out_free[b] = ev
+            out_free[o] = ev
             done = ev
         if join:
             self.join()

@@ -1009,3 +1009,40 @@ def test_streamed_steps_pipelined_across_calls(F):
     torch.cuda.synchronize()
     for (_, h_vol), ref in zip(outs, refs):
         assert torch.equal(h_vol, ref)
+
+
+@pytest.mark.parametrize("chunk", [16, 48, 70])
+def test_streamed_angle_chunks_bitwise(F, chunk):
+    """StreamedReconstructor(angle_chunk=...) streams each sub-slab's angles
+    in chunks (H2D / K1 / K2 chained with TF_BP_ACCUMULATE) -- the C5 path,
+    where a whole scan of a full-width sub-slab does not fit -- and gives the
+    device-resident volume bit for bit, fp32 and quantized, including a short
+    last chunk (chunks round down to multiples of 16 angles)."""
+    import torch
+
+    from paper_2505_13955_b200.engine import SlabReconstructor, StreamedReconstructor, phantom_raw
+    from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
+
+    n, rows, n_proj = 64, 300, 90
+    p = AcquisitionParams(n_proj=n_proj, n_rows=rows, n_chan=n, pixel_pitch=12.0)
+    d = VolumeDims(n, n, rows, voxel_pitch=12.0)
+    raw = torch.empty((n_proj, rows, n), device="cuda")
+    phantom_raw(p, d, raw, i0=1e5)
+    ref = SlabReconstructor(p, d, i0=1e5).run(raw).cpu()
+    st = StreamedReconstructor(p, d, i0=1e5, slab_rows=128, angle_chunk=chunk)
+    assert st.angle_chunk == chunk // 16 * 16
+    h_raw = raw.cpu().pin_memory()
+    h_vol = torch.zeros((rows, n, n), dtype=torch.float32).pin_memory()
+    st.run(h_raw, h_vol)
+    h_q = torch.zeros((rows, n, n), dtype=torch.uint16).pin_memory()
+    st.run(h_raw, h_q, quantize=(0.0, 4e-4))
+    torch.cuda.synchronize()
+    assert torch.equal(h_vol, ref)
+    q = torch.empty(ref.shape, dtype=torch.uint16, device="cuda")
+    from paper_2505_13955_b200._lib import TF_F32, check, lib
+    import ctypes
+    rc = ref.cuda()
+    check(lib().tf_quantize(ctypes.c_void_p(rc.data_ptr()), TF_F32, ctypes.c_void_p(q.data_ptr()), ref.numel(),
+                            0.0, 4e-4, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert torch.equal(h_q, q.cpu())
