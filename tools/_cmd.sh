@@ -1,4 +1,2 @@
-timeout 1500 python bench.py --config c5 --steps 1 --warmup 1 --rows 256 --slab-rows 256 --specimens 2 > gpurun_out/bench_c5_chunked.json 2> gpurun_out/bench_c5_chunked.err
-for f in gpurun_out/bench_c5_chunked.json; do python -c "
-import json,sys; d=json.loads(open('$f').read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['config']['angle_chunk'], d['config']['device_free_gb_at_setup'], d['clocks'])"; done
-tail -3 gpurun_out/bench_c5_chunked.err
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:ramp_filter -c 1 -o gpurun_out/r02_ncu_k1_c3_512 -f python tools/bp_launch.py --rows 512 > gpurun_out/ncu_k1.log 2>&1
+tail -2 gpurun_out/ncu_k1.log
