@@ -55,7 +55,7 @@ def _worker(rank, world, port, shape, q, zb=False):
 
 @pytest.mark.parametrize("world,shape,zb", [(2, (12, 10, 8), False), (3, (7, 11, 5), False),
                                            (2, (1800 // 60, 64, 16), False), (2, (12, 70, 8), True),
-                                           (3, (7, 40, 5), True)])
+                                           (3, (7, 40, 5), True), (8, (30, 20, 6), False)])
 def test_row_slab_all_to_all_layout(world, shape, zb):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -116,7 +116,7 @@ def _chunk_worker(rank, world, port, shape, chunk, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,shape,chunk", [(3, (50, 11, 5), 16), (2, (100, 10, 6), 32)])
+@pytest.mark.parametrize("world,shape,chunk", [(3, (50, 11, 5), 16), (2, (100, 10, 6), 32), (8, (90, 20, 5), 32)])
 def test_chunked_zslab_exchange_plan(world, shape, chunk):
     """ChunkedZSlabReconstructor's host logic (chunk_plan + the receive
     offsets run() uses for K1's peer stores): every owner's receive buffer
