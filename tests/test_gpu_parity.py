@@ -776,6 +776,10 @@ TC_CASES = {
     "pitch": (dict(n_proj=50, n_rows=32, n_chan=64, pixel_pitch=1.0), dict(nx=70, ny=70, nz=32, voxel_pitch=1.3)),
     "ragged": (dict(n_proj=37, n_rows=45, n_chan=61), dict(nx=61, ny=53, nz=45)),
     "rows300": (dict(n_proj=40, n_rows=300, n_chan=64), dict(nx=64, ny=64, nz=300)),
+    # voxel / pixel pitch 2.0: a tile's window spans up to 10 sqrt(2) 2 + 2 = 30.3 channels, so most
+    # angles take two K-steps (the support limit is 2.12); and 0.5 (a quarter of the window)
+    "coarse": (dict(n_proj=48, n_rows=24, n_chan=160, pixel_pitch=1.0), dict(nx=72, ny=80, nz=24, voxel_pitch=2.0)),
+    "fine": (dict(n_proj=48, n_rows=24, n_chan=64, pixel_pitch=2.0), dict(nx=120, ny=110, nz=24, voxel_pitch=1.0)),
 }
 
 
