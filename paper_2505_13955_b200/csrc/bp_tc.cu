@@ -24,23 +24,25 @@
 // block is added with round-to-nearest into a master sum kept in the weight
 // warps' registers.
 //
-// CTA (576 threads, one per SM) = one 11 x 11 tile x NR rows (NR = 256, or
-// 128 for short slabs), TMEM = two ping-pong accumulators of NR columns:
-//   warp 0      TMA producer: the fp64 window origin per angle and two
-//               cp.async.bulk.tensor boxes per item (T_hi, T_lo: 16 channels
-//               x NR rows, MN-major canonical layout) into an 8-slot ring; the
-//               OOB zero fill is the reference's zero guard for off-detector
-//               taps;
+// CTA (576 threads, one per SM, persistent) = one 11 x 11 tile x NR rows per
+// round (NR = 256, or 128 for short slabs), TMEM = two ping-pong accumulators
+// of NR columns:
+//   warp 0      prefetches the tensor map;
 //   warp 1      TMEM owner and MMA issuer: per item, one elected lane issues 3
 //               tcgen05.mma.kind::f16 (A = W from shared memory, K-major; B =
-//               T, MN-major), one tcgen05.commit frees the slot;
+//               T, MN-major), one tcgen05.commit frees the slot; the item's
+//               flags arrive in a control word with the slot;
 //   warps 2-17  four weight groups of 4 warps (group g: angles = g mod 4; one
 //               voxel row per thread): fp32 t relative to the fp64 window
-//               origin, the fp16 hi/lo W rows stored to the slot's A tiles.
-//               Every warp also owns NR/4 columns of the RN master sum of its
-//               32 voxels (64 registers at NR = 256): it flushes finished
-//               blocks (tcgen05.ld + fadd.rn) and writes the epilogue (x 2^-e,
-//               FoV mask and angle weight, fbp.py:247-251).
+//               origin, the fp16 hi/lo W rows stored to the slot's A tiles;
+//               the group's lane-quadrant-0 warp also issues the item's tap
+//               box (one cp.async.bulk.tensor: T_hi and T_lo, 16 channels x
+//               NR rows, MN-major canonical layout; the OOB zero fill is the
+//               reference's zero guard for off-detector taps) and writes its
+//               control word.  Every warp also owns NR/4 columns of the RN
+//               master sum of its 32 voxels (64 registers at NR = 256): it
+//               flushes finished blocks (tcgen05.ld + fadd.rn) and writes the
+//               epilogue (x 2^-e, FoV mask and angle weight, fbp.py:247-251).
 // The tap ring and the weight ring share one "full" mbarrier per slot (TMA
 // transaction bytes + 4 weight-warp arrivals) and one "empty" barrier (the
 // MMA commit), so the MMA warp waits once per item.
@@ -472,9 +474,8 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
                             (void)st, (void)ka;
 #else
                             mbar_arrive_expect_tx(&full[s], 2 * Cfg::TAP_PLANE);
+                            // one box holds both planes (T_hi, T_lo are adjacent along the map's dim 2)
                             tma_load_3d(st, &map, &full[s], 8 * (w.c_lo + kK * ks), zr0 / 8, ka);
-                            tma_load_3d(st + Cfg::TAP_PLANE, &map, &full[s], 8 * (w.c_lo + kK * ks), zr0 / 8,
-                                        ka + 1);
 #endif
 
                         }
@@ -840,7 +841,7 @@ extern "C" int tf_backproject_tc(const tf_bp_plan* p, const void* taps, int64_t 
     // bytes; channel c starts at element 8 c.  dim 1 = 8-row group, dim 2 = (angle, plane).
     cuuint64_t dims[3] = {(cuuint64_t)8 * g.n_chan, (cuuint64_t)R8, (cuuint64_t)(2 * (taps_a1 - taps_a0))};
     cuuint64_t strides[2] = {(cuuint64_t)g.n_chan * 16u, (cuuint64_t)R8 * g.n_chan * 16u};
-    cuuint32_t box[3] = {(cuuint32_t)(8 * kK), (cuuint32_t)(NR / 8), 1u};
+    cuuint32_t box[3] = {(cuuint32_t)(8 * kK), (cuuint32_t)(NR / 8), 2u};  // T_hi and T_lo of one step
     cuuint32_t estr[3] = {1u, 1u, 1u};
     CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, data, dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
