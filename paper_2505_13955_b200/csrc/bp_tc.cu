@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
         const uint32_t wslot0 = smem_u32(ring + 2 * Cfg::TAP_PLANE) + (uint32_t)((m >> 3) * 256 + (m & 7) * 16);
         int it_round = 0;   // items before this round (every group counts the same sequence)
         int blk_round = 0;  // accumulator blocks before this round (the ping-pong parity runs on)
-        long long p_empty = 0, p_flush = 0;
+        long long p_empty = 0, p_flush = 0, p_tail = 0;
         PROBE_T0(p_start);
         for (int r = 0; r < n_rounds; ++r) {
             const int wi = r * G + (int)blockIdx.x;
@@ -505,6 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
                 }
                 ibase += bt.n + __popc(bt.two);
             }
+            PROBE_T0(q5);
             while (flushed < n_blk) flush(flushed++);
             it_round = ibase;
             blk_round += n_blk;
@@ -547,8 +548,10 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
                     __threadfence();
                 }
             }
+            PROBE_ADD(p_tail, q5);
         }
 #ifdef TF_TC_PROBE
+        if (a.probe && lane == 0 && blockIdx.x < 1024 && warp == 2) a.probe[blockIdx.x * 16 + 13] = p_tail;
         if (a.probe && lane == 0 && blockIdx.x < 1024 && (warp == 2 || warp == 14)) {
             const int o = warp == 2 ? 7 : 10;
             a.probe[blockIdx.x * 16 + o] = clock64() - p_start;
@@ -556,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1) bp_tc_kernel(const __grid_constan
             a.probe[blockIdx.x * 16 + o + 2] = p_flush;
         }
 #endif
-        (void)p_empty, (void)p_flush;
+        (void)p_empty, (void)p_flush, (void)p_tail;
     }
 #ifdef TF_TC_PROBE_W_NONE
 probe_done:

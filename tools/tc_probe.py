@@ -7,7 +7,7 @@ expressed per MMA item.
 Slots: 0 TMA total, 1 TMA wait(empty); 2 MMA total, 3 MMA wait(full),
 4 MMA wait(accfree), 5 MMA issue (fence + elect + 3 MMA + commits +
 syncwarp), 6 items; 7/10 weight warp (group 0 / group 3) total, 8/11
-wait(empty), 9/12 flush.
+wait(empty), 9/12 flush; 13 group 0's end-of-round flush + epilogue + grid barrier.
 """
 
 from __future__ import annotations
@@ -107,7 +107,8 @@ def main():
            "tma_total": per(0), "tma_wait_empty": per(1),
            "mma_total": per(2), "mma_wait_full": per(3), "mma_wait_accfree": per(4), "mma_issue": per(5),
            "w0_total": per(7), "w0_wait_empty": per(8), "w0_flush": per(9),
-           "w3_total": per(10), "w3_wait_empty": per(11), "w3_flush": per(12)}
+           "w3_total": per(10), "w3_wait_empty": per(11), "w3_flush": per(12),
+           "w0_round_tail": per(13)}
     out["ms_best"] = round(best, 3)
     out["variant"] = out["variant"] + (f" src={os.path.basename(a.src)}" if a.src else "")
     print(json.dumps({k2: (round(x, 1) if isinstance(x, float) else x) for k2, x in out.items()}), flush=True)
