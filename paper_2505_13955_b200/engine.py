@@ -278,9 +278,8 @@ class StreamedReconstructor:
         p, d, k = self.params, self.dims, self.slab_rows
         if angle_chunk is None or (tensor is False) or (tensor is None and not tensor_default()):
             return None
-        if angle_chunk != "auto":
-            a = max(16, int(angle_chunk) // 16 * 16)
-            return a if a < p.n_proj else None
+        if angle_chunk != "auto":  # a chunk covering the scan is no chunking
+            return None if int(angle_chunk) >= p.n_proj else max(16, int(angle_chunk) // 16 * 16)
         free, _ = self.torch.cuda.mem_get_info(self.device)
         # blocks the caching allocator holds but no tensor uses are free for these buffers too
         free += self.torch.cuda.memory_reserved(self.device) - self.torch.cuda.memory_allocated(self.device)

@@ -435,6 +435,53 @@ def test_streamed_sub_slabs_tensor_core_uniform(R0, R1, S):
     assert all(b - a == S for a, b in cuts[:-1]) and 0 < cuts[-1][1] - cuts[-1][0] <= S
 
 
+@pytest.mark.parametrize("n,n_proj,k,free_gb,expect", [
+    (2048, 1800, 256, 178, None),      # C3: a whole-scan 256-row sub-slab fits
+    (8192, 7200, 256, 178, "chunk"),   # C5: it does not; chunks sized from the free memory
+    (8192, 7200, 256, 130, "chunk"),
+    (8192, 7200, 512, 178, "raise"),   # the fp32 + uint16 slabs alone exceed the device
+])
+def test_streamed_angle_chunk_sizing(monkeypatch, n, n_proj, k, free_gb, expect):
+    """StreamedReconstructor._chunk("auto"): no chunking when 2 raw buffers + tap planes of the
+    whole scan fit beside the volume slabs; otherwise the largest multiple of 16 angles that
+    fits (free memory less 4 GiB); an explicit chunk rounds down to 16 and disables itself when
+    it covers the scan."""
+    import torch
+
+    from paper_2505_13955_b200 import engine
+    from paper_2505_13955_b200.engine import StreamedReconstructor
+    from paper_2505_13955_b200.geometry import AcquisitionParams, VolumeDims
+
+    monkeypatch.setattr(torch.cuda, "mem_get_info", lambda dev=None: (int(free_gb * 1e9), int(180e9)))
+    monkeypatch.setattr(torch.cuda, "memory_reserved", lambda dev=None: 0)
+    monkeypatch.setattr(torch.cuda, "memory_allocated", lambda dev=None: 0)
+    monkeypatch.setattr(engine, "tensor_default", lambda: True)
+
+    class Cfg:
+        params = AcquisitionParams(n_proj=n_proj, n_rows=n, n_chan=n, pixel_pitch=12.0)
+        dims = VolumeDims(n, n, n, voxel_pitch=12.0)
+        slab_rows = k
+
+    cfg = Cfg()
+    cfg.torch = torch
+    cfg.device = None
+    if expect == "raise":
+        with pytest.raises(ValueError):
+            StreamedReconstructor._chunk(cfg, "auto", None)
+        return
+    a = StreamedReconstructor._chunk(cfg, "auto", None)
+    if expect is None:
+        assert a is None
+    else:
+        line = k * n * 4
+        budget = free_gb * 1e9 - (4 << 30) - k * n * n * 6
+        assert a % 16 == 0 and 16 <= a < n_proj
+        assert 3 * line * a <= budget < 3 * line * (a + 16)
+    assert StreamedReconstructor._chunk(cfg, 100, None) == 96
+    assert StreamedReconstructor._chunk(cfg, n_proj, None) is None
+    assert StreamedReconstructor._chunk(cfg, "auto", False) is None  # CUDA-core K2: never chunked
+
+
 def test_hostnuma_cpulist_parse():
     """hostnuma._parse_cpulist reads sysfs local_cpulist syntax."""
     from paper_2505_13955_b200.hostnuma import _parse_cpulist
